@@ -1,0 +1,4 @@
+// main() for the GoogleTest stand-in (see gtest/gtest.h).
+#include <gtest/gtest.h>
+
+int main(int argc, char** argv) { return ::testing::RunAllTests(argc, argv); }

@@ -1,0 +1,161 @@
+/*
+ * rvk_gpu.h -- C-ABI of the B200 (sm_100a) per-cluster velocity-profile
+ * estimator: RANSAC inlier selection + least-squares (v_x, v_y) refit +
+ * heading.
+ *
+ * This is the drop-in boundary. Each entry point replaces one call of the
+ * reference C++ API (proj/include/rvk, citations are relative to
+ * /root/reference/proj) with plain pointers and sizes:
+ *
+ *   rvk_run_ransac     <- rvk::run_ransac      include/rvk/ransac.hpp:128-129
+ *                                               (impl src/ransac.cpp:283-344)
+ *   rvk_estimate_all   <- rvk::estimate_all    include/rvk/velocity.hpp:123-125
+ *                                               (impl src/velocity.cpp:219-248)
+ *   rvk_ransac_estimate   run_ransac followed by estimate_all on the same
+ *                         clusters (the pipeline of tools/rvk_main.cpp:134-144
+ *                         and src/bench.cpp:615-627), masks never leave HBM.
+ *   rvk_trial_counts   <- per-(cluster, trial) count_trial_inliers
+ *                         (src/ransac.cpp:270-272) as scored inside run_ransac
+ *                         (src/ransac.cpp:309-319); exact for every trial.
+ *   rvk_seed_pairs     <- rvk::draw_seed_pair  src/ransac.cpp:256-268
+ *   rvk_cluster_thresholds <- normalize_cluster + mad_threshold
+ *                         (src/ransac.cpp:214-239, ransac.hpp:53-84)
+ *
+ * The C++ layer paper_2012_12618_b200/csrc/rvk_dropin.cpp re-exports the
+ * reference's own C++ signatures on top of these, so unchanged callers link
+ * against it.
+ *
+ * Data layout (CSR, one "frame" per call):
+ *   offsets[n_clusters + 1]  int64, offsets[0] == 0, ascending; cluster c owns
+ *                            points [offsets[c], offsets[c+1]).
+ *   azimuth[P], doppler[P]   float64, P = offsets[n_clusters]; the points of
+ *                            each cluster in the order gather_cluster_points
+ *                            produces (src/ransac.cpp:346-360): this is exactly
+ *                            Eigen::ArrayX2d's column-major [az(n) | dop(n)]
+ *                            split into two SoA arrays.
+ *   mask[P]                  uint8 0/1, aligned with the points (InlierMask::mask).
+ *
+ * Host entry points take HOST pointers, copy to the device, run, and copy back
+ * before returning (synchronous, like the reference). The *_device variants
+ * take DEVICE pointers and a cudaStream_t (as void*) and are asynchronous.
+ *
+ * Errors: every entry point returns an rvk_status. The message is available
+ * from rvk_last_error() (thread-local). Validation order and messages follow
+ * the reference so the C++ layer can rethrow the same exception types:
+ *   RVK_EINVAL              -> std::invalid_argument   (ransac.cpp:285-290,
+ *                                                        velocity.cpp:222-224,231-233)
+ *   RVK_ECLUSTER_TOO_SMALL  -> rvk::ClusterTooSmall     (ransac.cpp:295-299);
+ *                              rvk_last_error_cluster() = offending cluster.
+ *   RVK_ECUDA / RVK_ENOMEM  -> std::runtime_error (no CPU fallback exists).
+ *
+ * Threading: re-entrant; one lazily created device context per (process,
+ * device) under a mutex; each calling thread gets its own stream and
+ * workspace. `workers` is accepted for signature parity with the reference
+ * and ignored: the device grid replaces the std::thread team
+ * (include/rvk/parallel.hpp:23-54). Results are bit-identical for any
+ * device, grid or batch composition (the reference's worker-count
+ * invariance, ransac.hpp:124-125).
+ */
+#ifndef RVK_GPU_H_
+#define RVK_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RVK_GPU_ABI_VERSION 1
+
+typedef enum rvk_status {
+  RVK_OK = 0,
+  RVK_EINVAL = 1,
+  RVK_ECLUSTER_TOO_SMALL = 2,
+  RVK_ECUDA = 3,
+  RVK_ENOMEM = 4
+} rvk_status;
+
+/* Mirrors rvk::RansacParams (include/rvk/ransac.hpp:19-23). */
+typedef struct rvk_ransac_params {
+  int32_t max_trials;      /* line hypotheses per cluster, >= 1 (default 256) */
+  int32_t reserved;        /* must be 0 */
+  double threshold_scale;  /* > 0 (default 1.0) */
+  uint64_t rng_seed;       /* KeyedRng seed (default 0) */
+} rvk_ransac_params;
+
+/* Mirrors rvk::VelocityEstimate (include/rvk/types.hpp:57-65). */
+typedef struct rvk_estimate {
+  int64_t frame_id;
+  int32_t cluster_id;
+  int32_t inlier_count;
+  double v_x;
+  double v_y;
+  double heading;        /* valid iff has_heading */
+  int32_t has_heading;   /* std::optional<double>::has_value() */
+  int32_t condition_ok;
+} rvk_estimate;
+
+/* Library / device info. */
+int32_t rvk_abi_version(void);
+const char* rvk_last_error(void);
+int32_t rvk_last_error_cluster(void);
+/* Number of device kernels this thread launched since the last reset. */
+int64_t rvk_kernel_launches(void);
+void rvk_reset_kernel_launches(void);
+
+/* rvk::run_ransac (src/ransac.cpp:283-344).
+ *   rng_cluster_index: optional [n_clusters] RNG key per cluster; NULL means
+ *   the positional index c, as in the reference (ransac.cpp:314). Batched
+ *   multi-frame calls pass the frame-local index.
+ *   Outputs (caller-allocated): inlier_count[C], winning_trial[C], mask[P]. */
+int rvk_run_ransac(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                   const double* doppler, const rvk_ransac_params* params,
+                   const int32_t* rng_cluster_index, int32_t workers, int32_t* inlier_count,
+                   int32_t* winning_trial, uint8_t* mask);
+
+/* rvk::estimate_all (src/velocity.cpp:219-248) over CSR-gathered clusters.
+ *   cluster_ids[C] = Cluster::cluster_id (copied to the estimates). */
+int rvk_estimate_all(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                     const double* azimuth, const double* doppler, const int32_t* cluster_ids,
+                     const uint8_t* mask, int32_t workers, rvk_estimate* out);
+
+/* run_ransac + estimate_all fused; any output pointer may be NULL. */
+int rvk_ransac_estimate(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                        const double* azimuth, const double* doppler, const int32_t* cluster_ids,
+                        const rvk_ransac_params* params, const int32_t* rng_cluster_index,
+                        int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                        rvk_estimate* out);
+
+/* Device-pointer variant of rvk_ransac_estimate (all arrays in HBM, async on
+ * `stream`, a cudaStream_t or NULL for the legacy default stream). The
+ * caller must keep the inputs alive until the stream reaches this point. */
+int rvk_ransac_estimate_device(int64_t frame_id, int32_t n_clusters, int64_t n_points,
+                               const int64_t* d_offsets, const double* d_azimuth,
+                               const double* d_doppler, const int32_t* d_cluster_ids,
+                               const rvk_ransac_params* params, const int32_t* d_rng_cluster_index,
+                               int32_t* d_inlier_count, int32_t* d_winning_trial, uint8_t* d_mask,
+                               rvk_estimate* d_out, void* stream);
+
+/* Exact per-(cluster, trial) inlier counts, counts[c * max_trials + t]
+ * (the `counts` vector of src/ransac.cpp:308-319). */
+int rvk_trial_counts(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                     const double* doppler, const rvk_ransac_params* params,
+                     const int32_t* rng_cluster_index, int32_t* counts);
+
+/* Seed pairs drawn on the device: pairs[2*(c*max_trials+t)+{0,1}] = (i, j)
+ * of draw_seed_pair(seed, key_c, t, n_c) (src/ransac.cpp:256-268). */
+int rvk_seed_pairs(int32_t n_clusters, const int64_t* offsets, const rvk_ransac_params* params,
+                   const int32_t* rng_cluster_index, int32_t* pairs);
+
+/* Per-cluster normalization offsets/scales and the MAD corridor, computed on
+ * the device exactly as normalize_cluster + mad_threshold: norm[4*c+{0..3}] =
+ * (offset_az, offset_dop, scale_az, scale_dop), threshold[c]. */
+int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                           const double* doppler, double threshold_scale, double* norm,
+                           double* threshold);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RVK_GPU_H_ */
