@@ -1,0 +1,317 @@
+"""Python mirror of the reference's hot-path API, over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj:
+
+* ``run_ransac(clusters, params, workers=0)``   include/rvk/ransac.hpp:128-129
+* ``estimate_all(frame, clusters, masks, workers=0)`` include/rvk/velocity.hpp:123-125
+* ``gather_cluster_points(frame, clusters)``    include/rvk/ransac.hpp:133-134
+* ``draw_seed_pair(seed, cluster_id, trial, n)`` include/rvk/ransac.hpp:105
+
+``std::invalid_argument`` maps to ``ValueError``, ``rvk::ClusterTooSmall`` to
+``ClusterTooSmall``; CUDA failures raise ``DeviceError`` (there is no CPU
+fallback). The CSR entry points (``*_csr``) are the zero-copy form used by the
+bench and the parity tests: ``offsets[C+1]`` (int64), ``azimuth[P]``,
+``doppler[P]`` (float64), points of cluster c at ``offsets[c]:offsets[c+1]``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+
+class ClusterTooSmall(RuntimeError):
+    """rvk::ClusterTooSmall (include/rvk/ransac.hpp:47-49)."""
+
+    def __init__(self, msg: str, cluster: int = -1):
+        super().__init__(msg)
+        self.cluster = cluster
+
+
+class DeviceError(RuntimeError):
+    """A CUDA error inside the native library."""
+
+
+@dataclass
+class RansacParams:
+    """rvk::RansacParams (include/rvk/ransac.hpp:19-23)."""
+
+    max_trials: int = 256
+    threshold_scale: float = 1.0
+    rng_seed: int = 0
+
+    def c(self) -> N.RansacParamsC:
+        return N.RansacParamsC(int(self.max_trials), 0, float(self.threshold_scale),
+                               int(self.rng_seed) & (2**64 - 1))
+
+
+@dataclass
+class InlierMask:
+    """rvk::InlierMask (include/rvk/types.hpp:50-55)."""
+
+    cluster_id: int
+    mask: np.ndarray          # bool [n]
+    inlier_count: int
+    winning_trial: int
+
+
+@dataclass
+class VelocityEstimate:
+    """rvk::VelocityEstimate (include/rvk/types.hpp:57-65)."""
+
+    frame_id: int
+    cluster_id: int
+    v_x: float
+    v_y: float
+    heading: Optional[float]
+    inlier_count: int
+    condition_ok: bool
+
+
+@dataclass
+class RadarPoint:
+    """rvk::RadarPoint (include/rvk/types.hpp:27-33)."""
+
+    x: float = 0.0
+    y: float = 0.0
+    z: float = 0.0
+    doppler: float = 0.0
+    azimuth: float = 0.0
+
+
+@dataclass
+class Frame:
+    """rvk::Frame (include/rvk/types.hpp:35-40), struct-of-arrays."""
+
+    frame_id: int = 0
+    azimuth: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    doppler: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+@dataclass
+class Cluster:
+    """rvk::Cluster (include/rvk/types.hpp:43-46)."""
+
+    cluster_id: int
+    point_indices: np.ndarray
+
+
+@dataclass
+class RansacResult:
+    inlier_count: np.ndarray   # int32 [C]
+    winning_trial: np.ndarray  # int32 [C]
+    mask: np.ndarray           # uint8 [P]
+
+
+def _raise(st: int) -> None:
+    lib = N.gpu()
+    msg = (lib.rvk_last_error() or b"").decode()
+    if st == N.RVK_EINVAL:
+        raise ValueError(msg)
+    if st == N.RVK_ECLUSTER_TOO_SMALL:
+        raise ClusterTooSmall(msg, lib.rvk_last_error_cluster())
+    if st == N.RVK_ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def _check(st: int) -> None:
+    if st != N.RVK_OK:
+        _raise(st)
+
+
+def _csr(offsets, azimuth, doppler):
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    azimuth = np.ascontiguousarray(azimuth, dtype=np.float64)
+    doppler = np.ascontiguousarray(doppler, dtype=np.float64)
+    if offsets.ndim != 1 or offsets.size < 1:
+        raise ValueError("offsets must be a 1-D array of n_clusters + 1 entries")
+    if azimuth.shape != doppler.shape or azimuth.size < int(offsets[-1]):
+        raise ValueError("azimuth/doppler must hold offsets[-1] points")
+    return offsets, azimuth, doppler
+
+
+def _opt_i32(a, n):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    if a.size != n:
+        raise ValueError("per-cluster array has the wrong length")
+    return a
+
+
+def clusters_to_csr(clusters: Sequence[np.ndarray]):
+    """list of (n, 2) [azimuth, doppler] arrays (Eigen::ArrayX2d) -> CSR."""
+    sizes = np.array([np.asarray(c).shape[0] for c in clusters], dtype=np.int64)
+    offsets = np.zeros(len(clusters) + 1, dtype=np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    if len(clusters):
+        stacked = np.concatenate([np.asarray(c, dtype=np.float64).reshape(-1, 2)
+                                  for c in clusters]) if offsets[-1] else np.zeros((0, 2))
+    else:
+        stacked = np.zeros((0, 2))
+    return offsets, np.ascontiguousarray(stacked[:, 0]), np.ascontiguousarray(stacked[:, 1])
+
+
+# ------------------------------------------------------------------ CSR API
+
+def run_ransac_csr(offsets, azimuth, doppler, params: RansacParams,
+                   rng_cluster_index=None) -> RansacResult:
+    """rvk_run_ransac: bit-exact run_ransac over a CSR frame."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    cnt = np.zeros(n, np.int32)
+    tr = np.zeros(n, np.int32)
+    mask = np.zeros(azimuth.size, np.uint8)
+    keys = _opt_i32(rng_cluster_index, n)
+    p = params.c()
+    _check(N.gpu().rvk_run_ransac(n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler), C.addressof(p),
+                                  N.ptr(keys), 0, N.ptr(cnt), N.ptr(tr), N.ptr(mask)))
+    return RansacResult(cnt, tr, mask)
+
+
+def ransac_estimate_csr(offsets, azimuth, doppler, params: RansacParams, frame_id: int = 0,
+                        cluster_ids=None, rng_cluster_index=None):
+    """rvk_ransac_estimate: run_ransac + estimate_all in one device pass."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    cnt = np.zeros(n, np.int32)
+    tr = np.zeros(n, np.int32)
+    mask = np.zeros(azimuth.size, np.uint8)
+    est = np.zeros(n, N.ESTIMATE_DTYPE)
+    ids = _opt_i32(cluster_ids, n)
+    keys = _opt_i32(rng_cluster_index, n)
+    p = params.c()
+    _check(N.gpu().rvk_ransac_estimate(frame_id, n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+                                       N.ptr(ids), C.addressof(p), N.ptr(keys), N.ptr(cnt),
+                                       N.ptr(tr), N.ptr(mask), N.ptr(est)))
+    return RansacResult(cnt, tr, mask), est
+
+
+def estimate_all_csr(offsets, azimuth, doppler, mask, frame_id: int = 0, cluster_ids=None):
+    """rvk_estimate_all: LSQ refit + heading for caller masks (uint8 [P])."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    if mask.size != azimuth.size:
+        raise ValueError("estimate_all: mask size does not match cluster size")
+    est = np.zeros(n, N.ESTIMATE_DTYPE)
+    ids = _opt_i32(cluster_ids, n)
+    _check(N.gpu().rvk_estimate_all(frame_id, n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+                                    N.ptr(ids), N.ptr(mask), 0, N.ptr(est)))
+    return est
+
+
+def trial_counts_csr(offsets, azimuth, doppler, params: RansacParams, rng_cluster_index=None):
+    """Exact per-(cluster, trial) counts, [C, max_trials] (src/ransac.cpp:308-319)."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    out = np.zeros(n * params.max_trials, np.int32)
+    keys = _opt_i32(rng_cluster_index, n)
+    p = params.c()
+    _check(N.gpu().rvk_trial_counts(n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+                                    C.addressof(p), N.ptr(keys), N.ptr(out)))
+    return out.reshape(n, params.max_trials)
+
+
+def seed_pairs_csr(offsets, params: RansacParams, rng_cluster_index=None):
+    """Device-drawn seed pairs, [C, max_trials, 2]."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = offsets.size - 1
+    out = np.zeros(2 * n * params.max_trials, np.int32)
+    keys = _opt_i32(rng_cluster_index, n)
+    p = params.c()
+    _check(N.gpu().rvk_seed_pairs(n, N.ptr(offsets), C.addressof(p), N.ptr(keys), N.ptr(out)))
+    return out.reshape(n, params.max_trials, 2)
+
+
+def cluster_thresholds_csr(offsets, azimuth, doppler, threshold_scale: float = 1.0):
+    """(norm[C, 4] = offset_az, offset_dop, scale_az, scale_dop ; threshold[C])."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    norm = np.zeros(4 * n)
+    thr = np.zeros(n)
+    _check(N.gpu().rvk_cluster_thresholds(n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+                                          float(threshold_scale), N.ptr(norm), N.ptr(thr)))
+    return norm.reshape(n, 4), thr
+
+
+def ransac_estimate_device(offsets, azimuth, doppler, params: RansacParams, out, stream=None,
+                           frame_id: int = 0, cluster_ids=None, rng_cluster_index=None):
+    """rvk_ransac_estimate_device on torch CUDA tensors (async on `stream`).
+
+    out: dict with int32 'inlier_count'[C], 'winning_trial'[C], uint8 'mask'[P]
+    and uint8 'est'[C*48] (rvk_estimate records) device tensors.
+    """
+    n = int(offsets.numel()) - 1
+    p = params.c()
+    s = None if stream is None else C.c_void_p(stream.cuda_stream)
+    _check(N.gpu().rvk_ransac_estimate_device(
+        frame_id, n, int(azimuth.numel()), N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+        N.ptr(cluster_ids), C.addressof(p), N.ptr(rng_cluster_index), N.ptr(out["inlier_count"]),
+        N.ptr(out["winning_trial"]), N.ptr(out["mask"]), N.ptr(out["est"]), s))
+
+
+def estimates_from_records(rec: np.ndarray):
+    return [VelocityEstimate(int(r["frame_id"]), int(r["cluster_id"]), float(r["v_x"]),
+                             float(r["v_y"]), float(r["heading"]) if r["has_heading"] else None,
+                             int(r["inlier_count"]), bool(r["condition_ok"])) for r in rec]
+
+
+# ------------------------------------------------------- reference-shaped API
+
+def run_ransac(clusters: Sequence[np.ndarray], params: RansacParams = RansacParams(),
+               workers: int = 0):
+    """rvk::run_ransac (src/ransac.cpp:283-344). clusters: list of (n, 2)
+    [azimuth, doppler] arrays. Returns one InlierMask per cluster, cluster_id
+    = position. `workers` is accepted and ignored (the device grid replaces
+    the thread team)."""
+    del workers
+    offsets, az, dop = clusters_to_csr(clusters)
+    r = run_ransac_csr(offsets, az, dop, params)
+    out = []
+    for c in range(len(clusters)):
+        m = r.mask[offsets[c]:offsets[c + 1]].astype(bool)
+        out.append(InlierMask(c, m, int(r.inlier_count[c]), int(r.winning_trial[c])))
+    return out
+
+
+def gather_cluster_points(frame: Frame, clusters: Sequence[Cluster]):
+    """rvk::gather_cluster_points (src/ransac.cpp:346-360)."""
+    return [np.stack([frame.azimuth[np.asarray(cl.point_indices, dtype=np.int64)],
+                      frame.doppler[np.asarray(cl.point_indices, dtype=np.int64)]], axis=1)
+            for cl in clusters]
+
+
+def estimate_all(frame: Frame, clusters: Sequence[Cluster], masks: Sequence[InlierMask],
+                 workers: int = 0):
+    """rvk::estimate_all (src/velocity.cpp:219-248)."""
+    del workers
+    if len(clusters) != len(masks):
+        raise ValueError("estimate_all: one mask per cluster required")
+    for cl, m in zip(clusters, masks):
+        if len(m.mask) != len(cl.point_indices):
+            raise ValueError("estimate_all: mask size does not match cluster size")
+    pts = gather_cluster_points(frame, clusters)
+    offsets, az, dop = clusters_to_csr(pts)
+    mask = np.concatenate([np.asarray(m.mask, dtype=np.uint8) for m in masks]) if masks else \
+        np.zeros(0, np.uint8)
+    ids = np.array([cl.cluster_id for cl in clusters], dtype=np.int32)
+    rec = estimate_all_csr(offsets, az, dop, mask, frame.frame_id, ids)
+    return estimates_from_records(rec)
+
+
+def draw_seed_pair(seed: int, cluster_id: int, trial: int, n: int):
+    """rvk::draw_seed_pair (src/ransac.cpp:256-268), drawn on the device."""
+    if n < 2:
+        raise ValueError("draw_seed_pair: need at least 2 points")
+    # Build a cluster of n points keyed `cluster_id`; trials 0..trial.
+    offsets = np.array([0, n], np.int64)
+    pairs = seed_pairs_csr(offsets, RansacParams(trial + 1, 1.0, seed),
+                           rng_cluster_index=np.array([cluster_id], np.int32))
+    i, j = pairs[0, trial]
+    return int(i), int(j)

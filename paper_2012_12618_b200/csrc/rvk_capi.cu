@@ -1,0 +1,530 @@
+// Host side of the C-ABI (include/rvk_gpu.h): validation with the
+// reference's order and messages, per-thread device context (stream +
+// grow-only workspace + pinned staging), host<->device marshalling, and the
+// kernel pipeline prep -> score -> select(+refit).
+//
+// There is no CPU fallback anywhere: if CUDA is unavailable every entry
+// point returns RVK_ECUDA with the CUDA error string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/rvk_gpu.h"
+#include "rvk_kernels.cuh"
+
+namespace rvk_gpu {
+
+namespace {
+
+thread_local std::string g_error;
+thread_local int32_t g_error_cluster = -1;
+thread_local int64_t g_launches = 0;
+
+constexpr int kMinClusterSize = 3;  // include/rvk/types.hpp:20
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return status;
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+};
+
+#define RVK_CUDA(call)                                     \
+  do {                                                     \
+    const cudaError_t rvk_e_ = (call);                     \
+    if (rvk_e_ != cudaSuccess) throw CudaError{rvk_e_, #call}; \
+  } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+    if (bytes > cap) {
+      const size_t want = std::max(bytes, cap * 2);
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      RVK_CUDA(cudaMalloc(&p, want));
+      cap = want;
+    }
+    return static_cast<T*>(p);
+  }
+};
+
+// Grow-only pinned host buffer (staging for H2D/D2H).
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      const size_t want = std::max<size_t>(bytes, 1 << 20);
+      RVK_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+      cap = want;
+    }
+    return p;
+  }
+};
+
+struct Context {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  DevBuf in;       // offsets | az | dop | ids | keys | order (one H2D)
+  DevBuf out;      // count | trial | est | mask (one D2H)
+  DevBuf xy64, xy32, thr, norm, upper, aux;
+  HostBuf stage_in, stage_out;
+};
+
+Context& context() {
+  static std::mutex mu;
+  thread_local Context* ctx = nullptr;
+  int dev = 0;
+  RVK_CUDA(cudaGetDevice(&dev));
+  if (ctx == nullptr || ctx->device != dev) {
+    std::lock_guard<std::mutex> lock(mu);
+    ctx = new Context();  // one per (thread, device); lives for the thread
+    ctx->device = dev;
+    RVK_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  }
+  return *ctx;
+}
+
+size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+// Validation in the reference's order (src/ransac.cpp:285-299).
+int validate_params(const rvk_ransac_params* p, const char* who) {
+  if (p == nullptr) return fail(RVK_EINVAL, "%s: params must not be null", who);
+  if (p->max_trials < 1) return fail(RVK_EINVAL, "%s: max_trials must be at least 1", who);
+  if (!(p->threshold_scale > 0.0))
+    return fail(RVK_EINVAL, "%s: threshold_scale must be positive", who);
+  return RVK_OK;
+}
+
+int validate_offsets(int32_t n_clusters, const int64_t* offsets, int min_size, const char* who) {
+  if (n_clusters < 0) return fail(RVK_EINVAL, "%s: negative cluster count", who);
+  if (n_clusters > 0 && offsets == nullptr) return fail(RVK_EINVAL, "%s: offsets is null", who);
+  if (n_clusters > 0 && offsets[0] != 0) return fail(RVK_EINVAL, "%s: offsets[0] must be 0", who);
+  for (int32_t c = 0; c < n_clusters; ++c) {
+    const int64_t n = offsets[c + 1] - offsets[c];
+    if (n < 0) return fail(RVK_EINVAL, "%s: offsets must be non-decreasing", who);
+    if (n > (int64_t{1} << 30)) return fail(RVK_EINVAL, "%s: cluster %d too large", who, c);
+    if (n < min_size) {
+      g_error_cluster = c;
+      return fail(RVK_ECLUSTER_TOO_SMALL, "%s: cluster %d has %lld points, need %d", who, c,
+                  static_cast<long long>(n), min_size);
+    }
+  }
+  return RVK_OK;
+}
+
+// Largest clusters first, so the scoring grid's tail is short (LPT).
+void lpt_order(int32_t n_clusters, const int64_t* offsets, int32_t* order) {
+  std::iota(order, order + n_clusters, 0);
+  std::stable_sort(order, order + n_clusters, [&](int32_t a, int32_t b) {
+    return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
+  });
+}
+
+template <class F>
+int guarded(F&& f) {
+  g_error.clear();
+  g_error_cluster = -1;
+  try {
+    return f();
+  } catch (const CudaError& e) {
+    return fail(RVK_ECUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e.e),
+                cudaGetErrorString(e.e), e.what);
+  } catch (const std::bad_alloc&) {
+    return fail(RVK_ENOMEM, "host allocation failed");
+  }
+}
+
+// Stages the host frame into one pinned buffer, copies it with one H2D and
+// returns the device view (offsets, az, dop, ids, keys, order).
+struct Staged {
+  FrameDev f;
+  int64_t* d_offsets;
+};
+
+FrameDev stage_frame(Context& ctx, int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                     const double* az, const double* dop, const int32_t* ids,
+                     const int32_t* keys, bool want_order, const uint8_t* mask_in,
+                     uint8_t** d_mask_in) {
+  const int64_t P = offsets[n_clusters];
+  const size_t o_off = 0;
+  const size_t o_az = align_up(o_off + sizeof(int64_t) * (n_clusters + 1));
+  const size_t o_dop = align_up(o_az + sizeof(double) * P);
+  const size_t o_ids = align_up(o_dop + sizeof(double) * P);
+  const size_t o_keys = align_up(o_ids + sizeof(int32_t) * n_clusters);
+  const size_t o_ord = align_up(o_keys + sizeof(int32_t) * n_clusters);
+  const size_t o_mask = align_up(o_ord + sizeof(int32_t) * n_clusters);
+  const size_t total = align_up(o_mask + (mask_in ? P : 0));
+  char* h = static_cast<char*>(ctx.stage_in.get(total));
+  char* d = ctx.in.get<char>(total);
+  std::memcpy(h + o_off, offsets, sizeof(int64_t) * (n_clusters + 1));
+  std::memcpy(h + o_az, az, sizeof(double) * P);
+  std::memcpy(h + o_dop, dop, sizeof(double) * P);
+  if (ids) std::memcpy(h + o_ids, ids, sizeof(int32_t) * n_clusters);
+  if (keys) std::memcpy(h + o_keys, keys, sizeof(int32_t) * n_clusters);
+  if (want_order) lpt_order(n_clusters, offsets, reinterpret_cast<int32_t*>(h + o_ord));
+  if (mask_in) std::memcpy(h + o_mask, mask_in, P);
+  RVK_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, ctx.stream));
+  FrameDev f;
+  f.n_clusters = n_clusters;
+  f.n_points = P;
+  f.offsets = reinterpret_cast<const int64_t*>(d + o_off);
+  f.azimuth = reinterpret_cast<const double*>(d + o_az);
+  f.doppler = reinterpret_cast<const double*>(d + o_dop);
+  f.cluster_ids = ids ? reinterpret_cast<const int32_t*>(d + o_ids) : nullptr;
+  f.keys = keys ? reinterpret_cast<const int32_t*>(d + o_keys) : nullptr;
+  f.order = want_order ? reinterpret_cast<const int32_t*>(d + o_ord) : nullptr;
+  f.frame_id = frame_id;
+  if (d_mask_in) *d_mask_in = reinterpret_cast<uint8_t*>(d + o_mask);
+  return f;
+}
+
+Scratch scratch(Context& ctx, int32_t n_clusters, int64_t P, int32_t T) {
+  Scratch s;
+  s.xy64 = ctx.xy64.get<double2>(P);
+  s.xy32 = ctx.xy32.get<float2>(P + 2);
+  s.thr = ctx.thr.get<double>(n_clusters);
+  s.norm = ctx.norm.get<double>(4 * static_cast<size_t>(n_clusters));
+  s.upper = ctx.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
+  return s;
+}
+
+void check_launch() { RVK_CUDA(cudaGetLastError()); }
+
+// Output block: count[C] | trial[C] | est[C] | mask[P], one D2H.
+struct OutLayout {
+  size_t o_cnt, o_tr, o_est, o_mask, total;
+  OutLayout(int32_t C, int64_t P) {
+    o_cnt = 0;
+    o_tr = align_up(sizeof(int32_t) * C);
+    o_est = align_up(o_tr + sizeof(int32_t) * C);
+    o_mask = align_up(o_est + sizeof(rvk_estimate) * C);
+    total = align_up(o_mask + P);
+  }
+};
+
+// ---- optional stage timing (rvk_profile_enable / rvk_profile_read) ----
+struct StageRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+struct Profile {
+  bool on = false;
+  std::vector<StageRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    RVK_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+};
+thread_local Profile g_prof;
+
+template <class F>
+void stage(int id, cudaStream_t st, F&& launch) {
+  if (!g_prof.on) {
+    launch();
+    return;
+  }
+  StageRec r{id, g_prof.ev(), g_prof.ev()};
+  RVK_CUDA(cudaEventRecord(r.a, st));
+  launch();
+  RVK_CUDA(cudaEventRecord(r.b, st));
+  g_prof.recs.push_back(r);
+}
+
+// prep -> score -> select(+refit): the whole device pipeline of one call.
+void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                  const Outputs& o, cudaStream_t st) {
+  stage(0, st, [&] { launch_prep(f, p.threshold_scale, s, st); });
+  stage(1, st, [&] { launch_score(f, p, s, st); });
+  stage(2, st, [&] { launch_select(f, p, s, o, st); });
+  check_launch();
+}
+
+int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                         const double* az, const double* dop, const int32_t* ids,
+                         const rvk_ransac_params* params, const int32_t* keys,
+                         int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                         rvk_estimate* out, bool refit) {
+  int st = validate_params(params, "run_ransac");
+  if (st != RVK_OK) return st;
+  st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
+  if (st != RVK_OK) return st;
+  if (n_clusters == 0) return RVK_OK;
+  if ((az == nullptr || dop == nullptr) && offsets[n_clusters] > 0)
+    return fail(RVK_EINVAL, "run_ransac: null point arrays");
+  Context& ctx = context();
+  const int64_t P = offsets[n_clusters];
+  FrameDev f = stage_frame(ctx, frame_id, n_clusters, offsets, az, dop, ids, keys, true, nullptr,
+                           nullptr);
+  Scratch s = scratch(ctx, n_clusters, P, params->max_trials);
+  const OutLayout L(n_clusters, P);
+  char* dout = ctx.out.get<char>(L.total);
+  Outputs o;
+  o.inlier_count = reinterpret_cast<int32_t*>(dout + L.o_cnt);
+  o.winning_trial = reinterpret_cast<int32_t*>(dout + L.o_tr);
+  o.est = refit ? reinterpret_cast<rvk_estimate*>(dout + L.o_est) : nullptr;
+  o.mask = reinterpret_cast<uint8_t*>(dout + L.o_mask);
+  run_pipeline(f, *params, s, o, ctx.stream);
+  char* h = static_cast<char*>(ctx.stage_out.get(L.total));
+  RVK_CUDA(cudaMemcpyAsync(h, dout, L.total, cudaMemcpyDeviceToHost, ctx.stream));
+  RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (inlier_count) std::memcpy(inlier_count, h + L.o_cnt, sizeof(int32_t) * n_clusters);
+  if (winning_trial) std::memcpy(winning_trial, h + L.o_tr, sizeof(int32_t) * n_clusters);
+  if (mask) std::memcpy(mask, h + L.o_mask, P);
+  if (out && refit) std::memcpy(out, h + L.o_est, sizeof(rvk_estimate) * n_clusters);
+  return RVK_OK;
+}
+
+}  // namespace
+
+void count_launch() { ++g_launches; }
+
+}  // namespace rvk_gpu
+
+using namespace rvk_gpu;
+
+extern "C" {
+
+int32_t rvk_abi_version(void) { return RVK_GPU_ABI_VERSION; }
+const char* rvk_last_error(void) { return g_error.c_str(); }
+int32_t rvk_last_error_cluster(void) { return g_error_cluster; }
+int64_t rvk_kernel_launches(void) { return g_launches; }
+void rvk_reset_kernel_launches(void) { g_launches = 0; }
+
+int rvk_run_ransac(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                   const double* doppler, const rvk_ransac_params* params,
+                   const int32_t* rng_cluster_index, int32_t /*workers*/, int32_t* inlier_count,
+                   int32_t* winning_trial, uint8_t* mask) {
+  return guarded([&]() -> int {
+    return ransac_estimate_host(0, n_clusters, offsets, azimuth, doppler, nullptr, params,
+                                rng_cluster_index, inlier_count, winning_trial, mask, nullptr,
+                                false);
+  });
+}
+
+int rvk_ransac_estimate(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                        const double* azimuth, const double* doppler, const int32_t* cluster_ids,
+                        const rvk_ransac_params* params, const int32_t* rng_cluster_index,
+                        int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                        rvk_estimate* out) {
+  return guarded([&]() -> int {
+    return ransac_estimate_host(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
+                                params, rng_cluster_index, inlier_count, winning_trial, mask, out,
+                                true);
+  });
+}
+
+int rvk_estimate_all(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                     const double* azimuth, const double* doppler, const int32_t* cluster_ids,
+                     const uint8_t* mask, int32_t /*workers*/, rvk_estimate* out) {
+  return guarded([&]() -> int {
+    // estimate_all validates the mask count/size (src/velocity.cpp:222-233);
+    // in the CSR form the mask is P bytes aligned with the points, so only
+    // the structural checks remain.
+    int st = validate_offsets(n_clusters, offsets, 0, "estimate_all");
+    if (st != RVK_OK) return st;
+    if (n_clusters == 0) return RVK_OK;
+    if (mask == nullptr && offsets[n_clusters] > 0)
+      return fail(RVK_EINVAL, "estimate_all: one mask per cluster required");
+    Context& ctx = context();
+    uint8_t* d_mask = nullptr;
+    FrameDev f = stage_frame(ctx, frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
+                             nullptr, false, mask, &d_mask);
+    rvk_estimate* d_est = ctx.out.get<rvk_estimate>(n_clusters);
+    launch_refit(f, d_mask, d_est, ctx.stream);
+    check_launch();
+    void* h = ctx.stage_out.get(sizeof(rvk_estimate) * n_clusters);
+    RVK_CUDA(cudaMemcpyAsync(h, d_est, sizeof(rvk_estimate) * n_clusters, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(out, h, sizeof(rvk_estimate) * n_clusters);
+    return RVK_OK;
+  });
+}
+
+int rvk_ransac_estimate_device(int64_t frame_id, int32_t n_clusters, int64_t n_points,
+                               const int64_t* d_offsets, const double* d_azimuth,
+                               const double* d_doppler, const int32_t* d_cluster_ids,
+                               const rvk_ransac_params* params, const int32_t* d_rng_cluster_index,
+                               int32_t* d_inlier_count, int32_t* d_winning_trial, uint8_t* d_mask,
+                               rvk_estimate* d_out, void* stream) {
+  return guarded([&]() -> int {
+    int st = validate_params(params, "run_ransac");
+    if (st != RVK_OK) return st;
+    if (n_clusters < 0 || n_points < 0) return fail(RVK_EINVAL, "run_ransac: negative sizes");
+    if (n_clusters == 0) return RVK_OK;
+    if (d_mask == nullptr) return fail(RVK_EINVAL, "run_ransac: device mask buffer required");
+    Context& ctx = context();
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    FrameDev f;
+    f.n_clusters = n_clusters;
+    f.n_points = n_points;
+    f.offsets = d_offsets;
+    f.azimuth = d_azimuth;
+    f.doppler = d_doppler;
+    f.cluster_ids = d_cluster_ids;
+    f.keys = d_rng_cluster_index;
+    f.order = nullptr;
+    f.frame_id = frame_id;
+    Scratch sc = scratch(ctx, n_clusters, n_points, params->max_trials);
+    Outputs o;
+    o.inlier_count = d_inlier_count;
+    o.winning_trial = d_winning_trial;
+    o.mask = d_mask;
+    o.est = d_out;
+    run_pipeline(f, *params, sc, o, s);
+    return RVK_OK;
+  });
+}
+
+int rvk_trial_counts(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                     const double* doppler, const rvk_ransac_params* params,
+                     const int32_t* rng_cluster_index, int32_t* counts) {
+  return guarded([&]() -> int {
+    int st = validate_params(params, "run_ransac");
+    if (st != RVK_OK) return st;
+    st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
+    if (st != RVK_OK) return st;
+    if (n_clusters == 0) return RVK_OK;
+    Context& ctx = context();
+    const int64_t P = offsets[n_clusters];
+    FrameDev f = stage_frame(ctx, 0, n_clusters, offsets, azimuth, doppler, nullptr,
+                             rng_cluster_index, false, nullptr, nullptr);
+    Scratch s = scratch(ctx, n_clusters, P, params->max_trials);
+    const size_t nc = static_cast<size_t>(n_clusters) * params->max_trials;
+    int32_t* d_counts = ctx.aux.get<int32_t>(nc);
+    launch_prep(f, params->threshold_scale, s, ctx.stream);
+    launch_exact_counts(f, *params, s, d_counts, ctx.stream);
+    check_launch();
+    void* h = ctx.stage_out.get(sizeof(int32_t) * nc);
+    RVK_CUDA(cudaMemcpyAsync(h, d_counts, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(counts, h, sizeof(int32_t) * nc);
+    return RVK_OK;
+  });
+}
+
+int rvk_seed_pairs(int32_t n_clusters, const int64_t* offsets, const rvk_ransac_params* params,
+                   const int32_t* rng_cluster_index, int32_t* pairs) {
+  return guarded([&]() -> int {
+    int st = validate_params(params, "run_ransac");
+    if (st != RVK_OK) return st;
+    st = validate_offsets(n_clusters, offsets, 2, "draw_seed_pair");
+    if (st != RVK_OK) {
+      if (st == RVK_ECLUSTER_TOO_SMALL) return fail(RVK_EINVAL, "draw_seed_pair: need at least 2 points");
+      return st;
+    }
+    if (n_clusters == 0) return RVK_OK;
+    Context& ctx = context();
+    const size_t nc = static_cast<size_t>(n_clusters) * params->max_trials;
+    const size_t o_keys = align_up(sizeof(int64_t) * (n_clusters + 1));
+    const size_t total = align_up(o_keys + sizeof(int32_t) * n_clusters);
+    char* h = static_cast<char*>(ctx.stage_in.get(total));
+    char* d = ctx.in.get<char>(total);
+    std::memcpy(h, offsets, sizeof(int64_t) * (n_clusters + 1));
+    if (rng_cluster_index) std::memcpy(h + o_keys, rng_cluster_index, sizeof(int32_t) * n_clusters);
+    RVK_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, ctx.stream));
+    FrameDev f;
+    f.n_clusters = n_clusters;
+    f.offsets = reinterpret_cast<const int64_t*>(d);
+    f.keys = rng_cluster_index ? reinterpret_cast<const int32_t*>(d + o_keys) : nullptr;
+    int32_t* d_pairs = ctx.aux.get<int32_t>(2 * nc);
+    launch_seed_pairs(f, *params, d_pairs, ctx.stream);
+    check_launch();
+    void* ho = ctx.stage_out.get(sizeof(int32_t) * 2 * nc);
+    RVK_CUDA(cudaMemcpyAsync(ho, d_pairs, sizeof(int32_t) * 2 * nc, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(pairs, ho, sizeof(int32_t) * 2 * nc);
+    return RVK_OK;
+  });
+}
+
+int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                           const double* doppler, double threshold_scale, double* norm,
+                           double* threshold) {
+  return guarded([&]() -> int {
+    int st = validate_offsets(n_clusters, offsets, 1, "normalize_cluster");
+    if (st != RVK_OK) {
+      if (st == RVK_ECLUSTER_TOO_SMALL) return fail(RVK_EINVAL, "normalize_cluster: empty cluster");
+      return st;
+    }
+    if (n_clusters == 0) return RVK_OK;
+    Context& ctx = context();
+    const int64_t P = offsets[n_clusters];
+    FrameDev f = stage_frame(ctx, 0, n_clusters, offsets, azimuth, doppler, nullptr, nullptr,
+                             false, nullptr, nullptr);
+    Scratch s = scratch(ctx, n_clusters, P, 1);
+    launch_prep(f, threshold_scale, s, ctx.stream);
+    check_launch();
+    const size_t o_thr = align_up(sizeof(double) * 4 * n_clusters);
+    const size_t total = o_thr + sizeof(double) * n_clusters;
+    char* h = static_cast<char*>(ctx.stage_out.get(total));
+    RVK_CUDA(cudaMemcpyAsync(h, s.norm, sizeof(double) * 4 * n_clusters, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    RVK_CUDA(cudaMemcpyAsync(h + o_thr, s.thr, sizeof(double) * n_clusters,
+                             cudaMemcpyDeviceToHost, ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (norm) std::memcpy(norm, h, sizeof(double) * 4 * n_clusters);
+    if (threshold) std::memcpy(threshold, h + o_thr, sizeof(double) * n_clusters);
+    return RVK_OK;
+  });
+}
+
+void rvk_profile_enable(int32_t on) { g_prof.on = on != 0; }
+
+int rvk_profile_read(double* ms, int64_t* launches, int32_t n_stages) {
+  return guarded([&]() -> int {
+    for (int i = 0; i < n_stages; ++i) {
+      if (ms) ms[i] = 0.0;
+      if (launches) launches[i] = 0;
+    }
+    for (const StageRec& r : g_prof.recs) {
+      RVK_CUDA(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      RVK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+      if (r.stage < n_stages) {
+        if (ms) ms[r.stage] += t;
+        if (launches) launches[r.stage] += 1;
+      }
+      g_prof.pool.push_back(r.a);
+      g_prof.pool.push_back(r.b);
+    }
+    g_prof.recs.clear();
+    return RVK_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// Device-side building blocks shared by the sm_100a kernels (rvk_kernels.cu).
+//
+// Exactness contract: every quantity the reference
+// computes in FP64 and that feeds a discrete decision (normalized
+// coordinates, median, MAD threshold, line (m, c, den), point distance) is
+// recomputed here with explicit round-to-nearest intrinsics (__dadd_rn,
+// __dmul_rn, __ddiv_rn, __dsqrt_rn) in the reference's operation order, so no
+// FMA contraction can change a bit. The FP32 fast filter is only ever used
+// with a rigorous guard band; anything inside the band is decided by the
+// exact FP64 sequence.
+#pragma once
+
+#include <cstdint>
+
+namespace rvk_dev {
+
+constexpr double kSeedEpsilon = 1e-12;          // include/rvk/ransac.hpp:17
+constexpr double kRankEpsilon = 1e-8;           // include/rvk/velocity.hpp:18
+constexpr double kZeroVelocityEpsilon = 1e-9;   // include/rvk/velocity.hpp:21
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;  // include/rvk/rng.hpp:58
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+// ---- KeyedRng (include/rvk/rng.hpp:16-67), bit-for-bit ----
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// draw_seed_pair (src/ransac.cpp:256-268): KeyedRng(seed, (u32)cluster,
+// (u32)trial); i = next_below(n); j = next_below(n-1), ++j if j >= i.
+// next_below is the high word of the 64x32 product (rng.hpp:34-38).
+__device__ __forceinline__ void seed_pair(uint64_t seed, uint32_t cluster, uint32_t trial,
+                                          uint32_t n, int& i, int& j) {
+  uint64_t k = mix64(static_cast<uint64_t>(cluster) + kGamma);
+  k = mix64(k ^ static_cast<uint64_t>(trial));
+  uint64_t state = mix64(k ^ seed);
+  state += kGamma;
+  const uint64_t z1 = mix64(state);
+  state += kGamma;
+  const uint64_t z2 = mix64(state);
+  i = static_cast<int>(__umul64hi(z1, static_cast<uint64_t>(n)));
+  j = static_cast<int>(__umul64hi(z2, static_cast<uint64_t>(n - 1)));
+  if (j >= i) ++j;
+}
+
+// Line through the seeds in the normalized plane, exactly as run_trial
+// (src/ransac.cpp:184-190): dx = x2 - x1; |dx| < eps -> degenerate;
+// m = (y2 - y1) / dx; c = y1 - m * x1; den = sqrt(m * m + 1).
+struct Line {
+  double m, c, den;
+  bool degenerate;
+};
+
+__device__ __forceinline__ Line make_line(double x1, double y1, double x2, double y2) {
+  Line L;
+  const double dx = __dsub_rn(x2, x1);
+  L.degenerate = fabs(dx) < kSeedEpsilon;
+  L.m = __ddiv_rn(__dsub_rn(y2, y1), dx);
+  L.c = __dsub_rn(y1, __dmul_rn(L.m, x1));
+  L.den = __dsqrt_rn(__dadd_rn(__dmul_rn(L.m, L.m), 1.0));
+  return L;
+}
+
+// The reference's per-point decision (src/ransac.cpp:201-202):
+// |(-m) * x + y - c| / den <= threshold, all FP64 round-to-nearest.
+__device__ __forceinline__ bool exact_inlier(const Line& L, double x, double y, double thr) {
+  const double r = __dsub_rn(__dadd_rn(__dmul_rn(-L.m, x), y), L.c);
+  return __ddiv_rn(fabs(r), L.den) <= thr;
+}
+
+// FP32 affine form of the same distance, e = A x + B y + C with
+// (A, B, C) = (-m, 1, -c) / den, and two squared corridor bounds:
+//   e^2 <  t2lo  => certainly an inlier of the FP64 test,
+//   e^2 >= t2hi  => certainly an outlier,
+// otherwise the point is decided by exact_inlier(). With x, y in [0, 1]
+// the FP32 evaluation error of e is <= 4u * S, S = |A| + |B| + |C|,
+// u = 2^-24, and the FP64 reference's own error is <= 4 * 2^-53 * S; the
+// band 2^-21 * S (= 8u S) covers both with a factor ~2 margin, and the
+// (1 -/+ 2^-30) factors cover the FP64 rounding of the squared bounds.
+struct FastHyp {
+  float A, B, C;
+  float t2hi;  // e^2 < t2hi: possible inlier (upper-bound count)
+  float t2lo;  // e^2 < t2lo: certain inlier
+};
+
+__device__ __forceinline__ FastHyp make_fast(const Line& L, double thr) {
+  FastHyp h;
+  if (L.degenerate) {  // scores 0 (src/ransac.cpp:185-187): nothing passes
+    h.A = h.B = h.C = 0.f;
+    h.t2hi = -1.f;
+    h.t2lo = -1.f;
+    return h;
+  }
+  const double A = __ddiv_rn(-L.m, L.den);
+  const double B = __ddiv_rn(1.0, L.den);
+  const double C = __ddiv_rn(-L.c, L.den);
+  const double S = fabs(A) + fabs(B) + fabs(C);
+  const double band = S * 0x1p-21;
+  h.A = __double2float_rn(A);
+  h.B = __double2float_rn(B);
+  h.C = __double2float_rn(C);
+  const double hi = (thr + band) * (1.0 + 0x1p-30);
+  h.t2hi = __double2float_ru(hi * hi);
+  if (thr > band) {
+    const double lo = (thr - band) * (1.0 - 0x1p-30);
+    h.t2lo = __double2float_rd(lo * lo);
+  } else {
+    h.t2lo = 0.f;  // e^2 < 0 never holds: no certain inliers
+  }
+  return h;
+}
+
+// Full per-hypothesis state for the exact (verification / mask) passes.
+struct ExactHyp {
+  Line L;
+  FastHyp f;
+  int a, b;
+};
+
+__device__ __forceinline__ ExactHyp make_exact(const double2* __restrict__ xy64, uint64_t seed,
+                                               uint32_t key, uint32_t trial, int n, double thr) {
+  ExactHyp H;
+  seed_pair(seed, key, trial, static_cast<uint32_t>(n), H.a, H.b);
+  const double2 p = xy64[H.a];
+  const double2 q = xy64[H.b];
+  H.L = make_line(p.x, p.y, q.x, q.y);
+  H.f = make_fast(H.L, thr);
+  return H;
+}
+
+// Exact inlier decision of point k for a non-degenerate hypothesis
+// (run_trial, src/ransac.cpp:192-208: seeds counted without evaluation).
+__device__ __forceinline__ bool classify(const ExactHyp& H, int k, float2 p32,
+                                         const double2* __restrict__ xy64, double thr) {
+  if (k == H.a || k == H.b) return true;
+  const float e = __fmaf_rn(H.f.A, p32.x, __fmaf_rn(H.f.B, p32.y, H.f.C));
+  if (__fmaf_rn(e, e, -H.f.t2lo) < 0.f) return true;
+  if (!(__fmaf_rn(e, e, -H.f.t2hi) < 0.f)) return false;
+  const double2 q = xy64[k];
+  return exact_inlier(H.L, q.x, q.y, thr);
+}
+
+// Packs (count, trial) so that a max picks the largest count and, on ties,
+// the lowest trial -- the ascending strict-> scan of src/ransac.cpp:326-334.
+__device__ __forceinline__ unsigned long long pack_best(int count, int trial) {
+  return (static_cast<unsigned long long>(static_cast<uint32_t>(count)) << 32) |
+         static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(trial));
+}
+__device__ __forceinline__ int unpack_count(unsigned long long v) {
+  return static_cast<int>(v >> 32);
+}
+__device__ __forceinline__ int unpack_trial(unsigned long long v) {
+  return static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(v & 0xFFFFFFFFull));
+}
+
+}  // namespace rvk_dev

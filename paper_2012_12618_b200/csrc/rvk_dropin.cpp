@@ -1,0 +1,129 @@
+// C++ drop-in for the reference API: strong definitions of
+//
+//   std::vector<InlierMask> rvk::run_ransac(const std::vector<Eigen::ArrayX2d>&,
+//                                           const RansacParams&, int workers)
+//       -- include/rvk/ransac.hpp:128-129, replaces src/ransac.cpp:283-344
+//   std::vector<VelocityEstimate> rvk::estimate_all(const Frame&,
+//                                                   const std::vector<Cluster>&,
+//                                                   const std::vector<InlierMask>&, int workers)
+//       -- include/rvk/velocity.hpp:123-125, replaces src/velocity.cpp:219-248
+//
+// with the reference's exact signatures, compiled against the reference's
+// public headers (proj/include/rvk) and Eigen. Both marshal into the CSR
+// layout of include/rvk_gpu.h and call the sm_100a pipeline; no CPU
+// arithmetic of the path remains here. Errors are rethrown with the
+// reference's types and messages (std::invalid_argument,
+// rvk::ClusterTooSmall). `workers` is accepted and ignored.
+//
+// Link-time substitution: weaken those two symbols in the
+// reference's ransac.o / velocity.o (objcopy --weaken-symbol) and link this
+// library; every other reference symbol (primitives, sequential baselines,
+// gather, combine_masks) stays the reference's own.
+#include <rvk/ransac.hpp>
+#include <rvk/types.hpp>
+#include <rvk/velocity.hpp>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rvk_gpu.h"
+
+namespace rvk {
+namespace {
+
+[[noreturn]] void rethrow(int status) {
+  const std::string msg = rvk_last_error();
+  if (status == RVK_EINVAL) throw std::invalid_argument(msg);
+  if (status == RVK_ECLUSTER_TOO_SMALL) throw ClusterTooSmall(msg);
+  throw std::runtime_error(msg);
+}
+
+}  // namespace
+
+std::vector<InlierMask> run_ransac(const std::vector<Eigen::ArrayX2d>& clusters,
+                                   const RansacParams& params, int /*workers*/) {
+  const int32_t n = static_cast<int32_t>(clusters.size());
+  std::vector<int64_t> offsets(static_cast<std::size_t>(n) + 1, 0);
+  for (int32_t c = 0; c < n; ++c)
+    offsets[c + 1] = offsets[c] + static_cast<int64_t>(clusters[static_cast<std::size_t>(c)].rows());
+  const int64_t P = offsets[n];
+  // ArrayX2d is column-major: col(0) = azimuth[n], col(1) = doppler[n].
+  std::vector<double> az(static_cast<std::size_t>(P)), dop(static_cast<std::size_t>(P));
+  for (int32_t c = 0; c < n; ++c) {
+    const auto& m = clusters[static_cast<std::size_t>(c)];
+    for (Eigen::Index k = 0; k < m.rows(); ++k) {
+      az[static_cast<std::size_t>(offsets[c] + k)] = m(k, 0);
+      dop[static_cast<std::size_t>(offsets[c] + k)] = m(k, 1);
+    }
+  }
+  rvk_ransac_params p{params.max_trials, 0, params.threshold_scale, params.rng_seed};
+  std::vector<int32_t> count(static_cast<std::size_t>(n)), trial(static_cast<std::size_t>(n));
+  std::vector<uint8_t> mask(static_cast<std::size_t>(P));
+  const int st = rvk_run_ransac(n, offsets.data(), az.data(), dop.data(), &p, nullptr, 0,
+                                count.data(), trial.data(), mask.data());
+  if (st != RVK_OK) rethrow(st);
+  std::vector<InlierMask> out(static_cast<std::size_t>(n));
+  for (int32_t c = 0; c < n; ++c) {
+    InlierMask& im = out[static_cast<std::size_t>(c)];
+    im.cluster_id = c;
+    im.inlier_count = count[static_cast<std::size_t>(c)];
+    im.winning_trial = trial[static_cast<std::size_t>(c)];
+    im.mask = BoolArray::Constant(offsets[c + 1] - offsets[c], false);
+    for (int64_t k = offsets[c]; k < offsets[c + 1]; ++k)
+      im.mask(k - offsets[c]) = mask[static_cast<std::size_t>(k)] != 0;
+  }
+  return out;
+}
+
+std::vector<VelocityEstimate> estimate_all(const Frame& frame, const std::vector<Cluster>& clusters,
+                                           const std::vector<InlierMask>& masks,
+                                           int /*workers*/) {
+  if (clusters.size() != masks.size())  // src/velocity.cpp:222-224
+    throw std::invalid_argument("estimate_all: one mask per cluster required");
+  const int32_t n = static_cast<int32_t>(clusters.size());
+  std::vector<int64_t> offsets(static_cast<std::size_t>(n) + 1, 0);
+  for (int32_t c = 0; c < n; ++c) {
+    const auto& cl = clusters[static_cast<std::size_t>(c)];
+    if (masks[static_cast<std::size_t>(c)].mask.size() !=
+        static_cast<Eigen::Index>(cl.point_indices.size()))  // velocity.cpp:231-233
+      throw std::invalid_argument("estimate_all: mask size does not match cluster size");
+    offsets[c + 1] = offsets[c] + static_cast<int64_t>(cl.point_indices.size());
+  }
+  const int64_t P = offsets[n];
+  std::vector<double> az(static_cast<std::size_t>(P)), dop(static_cast<std::size_t>(P));
+  std::vector<uint8_t> mask(static_cast<std::size_t>(P));
+  std::vector<int32_t> ids(static_cast<std::size_t>(n));
+  for (int32_t c = 0; c < n; ++c) {
+    const auto& cl = clusters[static_cast<std::size_t>(c)];
+    ids[static_cast<std::size_t>(c)] = cl.cluster_id;
+    for (std::size_t k = 0; k < cl.point_indices.size(); ++k) {
+      const RadarPoint& pt = frame.points[static_cast<std::size_t>(cl.point_indices[k])];
+      const std::size_t q = static_cast<std::size_t>(offsets[c]) + k;
+      az[q] = pt.azimuth;
+      dop[q] = pt.doppler;
+      mask[q] = masks[static_cast<std::size_t>(c)].mask(static_cast<Eigen::Index>(k)) ? 1 : 0;
+    }
+  }
+  std::vector<rvk_estimate> est(static_cast<std::size_t>(n));
+  const int st = rvk_estimate_all(frame.frame_id, n, offsets.data(), az.data(), dop.data(),
+                                  ids.data(), mask.data(), 0, est.data());
+  if (st != RVK_OK) rethrow(st);
+  std::vector<VelocityEstimate> out(static_cast<std::size_t>(n));
+  for (int32_t c = 0; c < n; ++c) {
+    const rvk_estimate& e = est[static_cast<std::size_t>(c)];
+    VelocityEstimate& v = out[static_cast<std::size_t>(c)];
+    v.frame_id = e.frame_id;
+    v.cluster_id = e.cluster_id;
+    v.v_x = e.v_x;
+    v.v_y = e.v_y;
+    v.heading = e.has_heading ? std::optional<double>(e.heading) : std::nullopt;
+    v.inlier_count = e.inlier_count;
+    v.condition_ok = e.condition_ok != 0;
+  }
+  return out;
+}
+
+}  // namespace rvk

@@ -1,0 +1,586 @@
+// sm_100a kernels of the per-cluster velocity-profile estimator.
+//
+//   prep_kernel    normalize_cluster + median + mad_threshold
+//                  (src/ransac.cpp:214-239, include/rvk/ransac.hpp:53-84)
+//   score_kernel   the hot loop: every (cluster, trial) line hypothesis
+//                  against every point of its cluster (run_trial,
+//                  src/ransac.cpp:177-210, scheduled as in :303-319), FP32
+//                  packed FFMA2 with a guard band -> UPPER-BOUND counts
+//   select_kernel  exact argmax (max count, lowest trial; :321-334): the
+//                  best upper bound is verified exactly, then every trial
+//                  whose upper bound reaches that exact count is verified
+//                  too; winner mask rebuilt exactly (:335-341); then the
+//                  least-squares refit + heading of estimate_cluster_velocity
+//                  (src/velocity.cpp:26-90) on the winning inliers.
+//   refit_kernel   estimate_all on caller-provided masks (velocity.cpp:92-121)
+//
+// Why the argmax stays exact: upper[t] >= exact[t] for every trial (the FP32
+// band only ever admits extra points). If E0 is the exact count of the
+// lowest-index trial with the largest upper bound, any trial t with
+// upper[t] < E0 has exact[t] < E0 and cannot win or tie, so verifying the
+// trials with upper[t] >= E0 decides the reference's winner exactly.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+
+#include "rvk_device.cuh"
+#include "rvk_kernels.cuh"
+
+namespace rvk_gpu {
+
+using namespace rvk_dev;
+
+namespace {
+
+constexpr int kPrepThreads = 256;
+constexpr int kSelectThreads = 256;
+constexpr int kScoreThreads = 128;
+constexpr int kHypPerThread = 4;  // two FFMA2 pairs
+constexpr int kHypPerTile = kScoreThreads * kHypPerThread;
+constexpr int kChunk = 4096;      // points staged per shared-memory chunk
+constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
+
+// ---------------------------------------------------------------- helpers
+
+template <class T, class Op>
+__device__ __forceinline__ T warp_reduce(T v, Op op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reduction; every thread gets the result. `red` holds >= 32 T.
+template <class T, class Op>
+__device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_reduce(v, op);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T r = red[0];
+  for (int w = 1; w < nw; ++w) r = op(r, red[w]);
+  return r;
+}
+
+struct MinOp {
+  __device__ double operator()(double a, double b) const { return b < a ? b : a; }
+};
+struct MaxOp {
+  __device__ double operator()(double a, double b) const { return b > a ? b : a; }
+};
+struct SumI {
+  __device__ int operator()(int a, int b) const { return a + b; }
+};
+struct SumD {
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+struct MaxU64 {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
+    return a > b ? a : b;
+  }
+};
+struct MinI {
+  __device__ int operator()(int a, int b) const { return b < a ? b : a; }
+};
+
+// k-th smallest (0-based) normalized doppler of the block's cluster, exact:
+// MSD radix select over the IEEE bit patterns (non-negative doubles order
+// like their bit patterns). hist: 256 counters in shared memory.
+// xy is written earlier in the same kernel: no __restrict__ (no .nc loads).
+__device__ double block_select_y(const double2* xy, int n, int k,
+                                 unsigned int* hist, unsigned long long* sh_prefix,
+                                 int* sh_k) {
+  unsigned long long prefix = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long key = __double_as_longlong(xy[i].y);
+      if (((key ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: find the bucket holding rank k
+      const int lane = threadIdx.x;
+      unsigned int local[8];
+      unsigned int sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        local[q] = hist[lane * 8 + q];
+        sum += local[q];
+      }
+      unsigned int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned int excl = incl - sum;
+      const unsigned int kk = static_cast<unsigned int>(k);
+      const bool mine = kk >= excl && kk < incl;
+      if (mine) {
+        unsigned int cum = excl;
+        int digit = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (kk >= cum && kk < cum + local[q]) {
+            digit = lane * 8 + q;
+            *sh_k = static_cast<int>(kk - cum);
+          }
+          cum += local[q];
+        }
+        *sh_prefix = prefix | (static_cast<unsigned long long>(digit) << shift);
+      }
+    }
+    __syncthreads();
+    prefix = *sh_prefix;
+    k = *sh_k;
+    __syncthreads();
+  }
+  return __longlong_as_double(static_cast<long long>(prefix));
+}
+
+// ------------------------------------------------------------- prep kernel
+
+__global__ void __launch_bounds__(kPrepThreads)
+prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+            const double* __restrict__ az, const double* __restrict__ dop, double scale,
+            double2* xy64, float2* __restrict__ xy32, double* __restrict__ thr,
+            double* __restrict__ norm) {
+  __shared__ double red[32];
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long sh_prefix;
+  __shared__ int sh_k;
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+
+  // normalize_cluster (src/ransac.cpp:214-232): per-axis min/max, exact.
+  double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double a = az[b + k], d = dop[b + k];
+    lo0 = a < lo0 ? a : lo0;
+    hi0 = a > hi0 ? a : hi0;
+    lo1 = d < lo1 ? d : lo1;
+    hi1 = d > hi1 ? d : hi1;
+  }
+  lo0 = block_reduce(lo0, MinOp(), red);
+  hi0 = block_reduce(hi0, MaxOp(), red);
+  lo1 = block_reduce(lo1, MinOp(), red);
+  hi1 = block_reduce(hi1, MaxOp(), red);
+  const double s0 = __dsub_rn(hi0, lo0);
+  const double s1 = __dsub_rn(hi1, lo1);
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
+    const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
+    xy64[b + k] = make_double2(x, y);
+    xy32[b + k] = make_float2(__double2float_rn(x), __double2float_rn(y));
+  }
+  if (threadIdx.x == 0 && norm != nullptr) {
+    norm[4 * c + 0] = lo0;
+    norm[4 * c + 1] = lo1;
+    norm[4 * c + 2] = s0;
+    norm[4 * c + 3] = s1;
+  }
+  __syncthreads();
+
+  // median (include/rvk/ransac.hpp:53-70): middle element, or the mean of
+  // the middle pair for even n, of the sorted normalized dopplers.
+  const double2* cxy = xy64 + b;
+  double med;
+  if (n & 1) {
+    med = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+  } else {
+    const double lo = block_select_y(cxy, n, n / 2 - 1, hist, &sh_prefix, &sh_k);
+    const double hi = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+    med = __ddiv_rn(__dadd_rn(lo, hi), 2.0);
+  }
+
+  // mean_abs_deviation (ransac.hpp:74-84): the sum is order-sensitive, so it
+  // runs sequentially in index order, exactly as the reference.
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {
+      const double d0 = fabs(__dsub_rn(cxy[k].y, med));
+      const double d1 = fabs(__dsub_rn(cxy[k + 1].y, med));
+      const double d2 = fabs(__dsub_rn(cxy[k + 2].y, med));
+      const double d3 = fabs(__dsub_rn(cxy[k + 3].y, med));
+      acc = __dadd_rn(acc, d0);
+      acc = __dadd_rn(acc, d1);
+      acc = __dadd_rn(acc, d2);
+      acc = __dadd_rn(acc, d3);
+    }
+    for (; k < n; ++k) acc = __dadd_rn(acc, fabs(__dsub_rn(cxy[k].y, med)));
+    // mad_threshold (src/ransac.cpp:234-239)
+    thr[c] = __dmul_rn(scale, __ddiv_rn(acc, static_cast<double>(n)));
+  }
+}
+
+// ------------------------------------------------------------ score kernel
+
+// One CTA = one tile of kHypPerTile trials of one cluster. Each thread owns
+// kHypPerThread hypotheses as two FFMA2 pairs; the cluster's FP32 points are
+// staged in shared memory and read as float4 (two points) broadcasts.
+// Per point and hypothesis pair: 3 FFMA2 (e = A x + (B y + C); g = e^2 - t2)
+// and the sign bit of g accumulated into an integer count.
+__global__ void __launch_bounds__(kScoreThreads)
+score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy64,
+             const float2* __restrict__ xy32, const double* __restrict__ thr,
+             const int32_t* __restrict__ keys, const int32_t* __restrict__ order, int T,
+             int tiles_per_cluster, uint64_t seed, int32_t* __restrict__ upper) {
+  __shared__ float4 pts[kChunk / 2];
+  const int tile = blockIdx.x;
+  const int ci = tile / tiles_per_cluster;
+  const int tb = tile - ci * tiles_per_cluster;
+  const int c = order ? order[ci] : ci;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double th = thr[c];
+
+  float2 A[2], B[2], Cc[2], T2[2];
+#pragma unroll
+  for (int q = 0; q < kHypPerThread; ++q) {
+    const int t = tb * kHypPerTile + q * kScoreThreads + threadIdx.x;
+    FastHyp f;
+    if (t < T) {
+      f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th).f;
+    } else {
+      f.A = f.B = f.C = 0.f;
+      f.t2hi = -1.f;
+    }
+    const int pr = q >> 1;
+    if (q & 1) {
+      A[pr].y = f.A; B[pr].y = f.B; Cc[pr].y = f.C; T2[pr].y = -f.t2hi;
+    } else {
+      A[pr].x = f.A; B[pr].x = f.B; Cc[pr].x = f.C; T2[pr].x = -f.t2hi;
+    }
+  }
+
+  uint32_t cnt[kHypPerThread] = {0, 0, 0, 0};
+  const float4* src = reinterpret_cast<const float4*>(xy32 + b);
+  const bool aligned = (b & 1) == 0;
+  for (int c0 = 0; c0 < n; c0 += kChunk) {
+    const int m = min(kChunk, n - c0);
+    const int m2 = (m + 1) >> 1;
+    __syncthreads();
+    if (aligned && (c0 & 1) == 0) {
+      for (int i = threadIdx.x; i < m2; i += blockDim.x) {
+        float4 v = (2 * i + 1 < m) ? src[(c0 >> 1) + i]
+                                   : make_float4(xy32[b + c0 + 2 * i].x,
+                                                 xy32[b + c0 + 2 * i].y, 0.f, kPadY);
+        pts[i] = v;
+      }
+    } else {
+      for (int i = threadIdx.x; i < m2; i += blockDim.x) {
+        const float2 p0 = xy32[b + c0 + 2 * i];
+        const float2 p1 = (2 * i + 1 < m) ? xy32[b + c0 + 2 * i + 1] : make_float2(0.f, kPadY);
+        pts[i] = make_float4(p0.x, p0.y, p1.x, p1.y);
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int i = 0; i < m2; ++i) {
+      const float4 v = pts[i];
+      const float2 x0 = make_float2(v.x, v.x), y0 = make_float2(v.y, v.y);
+      const float2 x1 = make_float2(v.z, v.z), y1 = make_float2(v.w, v.w);
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        float2 e = __ffma2_rn(A[pr], x0, __ffma2_rn(B[pr], y0, Cc[pr]));
+        float2 g = __ffma2_rn(e, e, T2[pr]);
+        cnt[2 * pr] += __float_as_uint(g.x) >> 31;
+        cnt[2 * pr + 1] += __float_as_uint(g.y) >> 31;
+        e = __ffma2_rn(A[pr], x1, __ffma2_rn(B[pr], y1, Cc[pr]));
+        g = __ffma2_rn(e, e, T2[pr]);
+        cnt[2 * pr] += __float_as_uint(g.x) >> 31;
+        cnt[2 * pr + 1] += __float_as_uint(g.y) >> 31;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kHypPerThread; ++q) {
+    const int t = tb * kHypPerTile + q * kScoreThreads + threadIdx.x;
+    if (t < T) upper[static_cast<int64_t>(c) * T + t] = static_cast<int32_t>(cnt[q]);
+  }
+}
+
+// ----------------------------------------------------------- select kernel
+
+__device__ int warp_exact_count(const ExactHyp& H, int n, const float2* __restrict__ p32,
+                                const double2* __restrict__ p64, double th) {
+  if (H.L.degenerate) return 0;
+  int cnt = 0;
+  for (int k = threadIdx.x & 31; k < n; k += 32) cnt += classify(H, k, p32[k], p64, th) ? 1 : 0;
+  return warp_reduce(cnt, SumI());
+}
+
+// LSQ refit + heading of one cluster (estimate_cluster_velocity,
+// src/velocity.cpp:26-90; solve_velocity / min_norm_fallback,
+// include/rvk/velocity.hpp:46-105; heading_angle velocity.cpp:19-24).
+// Reductions use a fixed tree, so results are deterministic; they differ
+// from Eigen's reduction order only in the last bits (tolerance-checked).
+// `mask` may have been written earlier in the same kernel: no __restrict__.
+__device__ void block_refit(int n, const double* __restrict__ az, const double* __restrict__ dop,
+                            const uint8_t* mask, int64_t frame_id, int cluster_id,
+                            rvk_estimate* __restrict__ out, double* red) {
+  __shared__ int redi[32];
+  double g00 = 0, g01 = 0, g11 = 0, b0 = 0, b1 = 0, ds = 0;
+  int nin = 0, first = INT_MAX;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    if (!mask[k]) continue;
+    double s, c;
+    sincos(az[k], &s, &c);
+    const double d = dop[k];
+    g00 += c * c;
+    g01 += c * s;
+    g11 += s * s;
+    b0 += c * d;
+    b1 += s * d;
+    ds += d;
+    ++nin;
+    first = k < first ? k : first;
+  }
+  nin = block_reduce(nin, SumI(), redi);
+  first = block_reduce(first, MinI(), redi);
+  g00 = block_reduce(g00, SumD(), red);
+  g01 = block_reduce(g01, SumD(), red);
+  g11 = block_reduce(g11, SumD(), red);
+  b0 = block_reduce(b0, SumD(), red);
+  b1 = block_reduce(b1, SumD(), red);
+  ds = block_reduce(ds, SumD(), red);
+  if (threadIdx.x != 0) return;
+  rvk_estimate e;
+  e.frame_id = frame_id;
+  e.cluster_id = cluster_id;
+  e.inlier_count = nin;
+  e.heading = 0.0;
+  e.has_heading = 0;
+  if (nin == 0) {  // velocity.cpp:56-62
+    e.v_x = 0.0;
+    e.v_y = 0.0;
+    e.condition_ok = 0;
+    *out = e;
+    return;
+  }
+  if (nin == 1) {  // velocity.cpp:63-67
+    double s, c;
+    sincos(az[first], &s, &c);
+    e.v_x = dop[first] * c;
+    e.v_y = dop[first] * s;
+    e.condition_ok = 0;
+  } else {
+    const double det = g00 * g11 - g01 * g01;
+    const double half_trace = (g00 + g11) / 2.0;
+    if (det >= kRankEpsilon * half_trace * half_trace) {  // velocity.hpp:64
+      e.v_x = (g11 * b0 - g01 * b1) / det;
+      e.v_y = (g00 * b1 - g01 * b0) / det;
+      e.condition_ok = 1;
+    } else {  // min_norm_fallback, velocity.hpp:79-105
+      const double half_sum = (g00 + g11) / 2.0;
+      const double half_diff = (g00 - g11) / 2.0;
+      const double lambda = half_sum + sqrt(half_diff * half_diff + g01 * g01);
+      double u0, u1;
+      if (g01 != 0.0) {
+        u0 = g01;
+        u1 = lambda - g00;
+      } else if (g00 >= g11) {
+        u0 = 1.0;
+        u1 = 0.0;
+      } else {
+        u0 = 0.0;
+        u1 = 1.0;
+      }
+      const double nr = sqrt(u0 * u0 + u1 * u1);
+      if (nr > 0.0) {
+        u0 /= nr;
+        u1 /= nr;
+      }
+      double s0, c0;
+      sincos(az[first], &s0, &c0);
+      if (u0 * c0 + u1 * s0 < 0.0) {
+        u0 = -u0;
+        u1 = -u1;
+      }
+      const double mean = ds / nin;
+      e.v_x = mean * u0;
+      e.v_y = mean * u1;
+      e.condition_ok = 0;
+    }
+  }
+  if (!(fabs(e.v_x) < kZeroVelocityEpsilon && fabs(e.v_y) < kZeroVelocityEpsilon)) {
+    const double h = atan2(e.v_y, e.v_x);
+    e.heading = h == -kPi ? kPi : h;  // to_half_open_angle, types.hpp:74-77
+    e.has_heading = 1;
+  }
+  *out = e;
+}
+
+__global__ void __launch_bounds__(kSelectThreads)
+select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
+              const double* __restrict__ dop, const int32_t* __restrict__ keys,
+              const int32_t* __restrict__ cluster_ids, int64_t frame_id,
+              const double2* __restrict__ xy64, const float2* __restrict__ xy32,
+              const double* __restrict__ thr, const int32_t* __restrict__ upper, int T,
+              uint64_t seed, int32_t* __restrict__ out_count, int32_t* __restrict__ out_trial,
+              uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
+  __shared__ unsigned long long redu[32];
+  __shared__ int redi[32];
+  __shared__ double redd[32];
+  __shared__ unsigned long long best;
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double th = thr[c];
+  const float2* p32 = xy32 + b;
+  const double2* p64 = xy64 + b;
+  const int32_t* U = upper + static_cast<int64_t>(c) * T;
+
+  // 1. trial with the largest upper bound (lowest index on ties).
+  unsigned long long v = 0;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) v = MaxU64()(v, pack_best(U[t], t));
+  v = block_reduce(v, MaxU64(), redu);
+  const int t0 = unpack_trial(v);
+
+  // 2. its exact count.
+  const ExactHyp H0 = make_exact(p64, seed, key, static_cast<uint32_t>(t0), n, th);
+  int e0 = 0;
+  if (!H0.L.degenerate)
+    for (int k = threadIdx.x; k < n; k += blockDim.x) e0 += classify(H0, k, p32[k], p64, th);
+  e0 = block_reduce(e0, SumI(), redi);
+  if (threadIdx.x == 0) best = pack_best(e0, t0);
+  __syncthreads();
+
+  // 3. verify every other trial that could reach e0 (warp per candidate).
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < T; t += nw) {
+    if (t == t0 || U[t] < e0) continue;
+    const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, th);
+    const int e = warp_exact_count(H, n, p32, p64, th);
+    if ((threadIdx.x & 31) == 0) atomicMax(&best, pack_best(e, t));
+  }
+  __syncthreads();
+  const int win = unpack_trial(best);
+  const int win_count = unpack_count(best);
+
+  // 4. winner mask (evaluate_trial, src/ransac.cpp:274-281).
+  const ExactHyp W = make_exact(p64, seed, key, static_cast<uint32_t>(win), n, th);
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    mask[b + k] = (!W.L.degenerate && classify(W, k, p32[k], p64, th)) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    if (out_count) out_count[c] = win_count;
+    if (out_trial) out_trial[c] = win;
+  }
+  if (est == nullptr) return;
+  __syncthreads();  // mask visible to the whole block
+
+  // 5. LSQ refit on the winning inliers.
+  block_refit(n, az + b, dop + b, mask + b, frame_id, cluster_ids ? cluster_ids[c] : c, est + c,
+              redd);
+}
+
+__global__ void __launch_bounds__(kSelectThreads)
+refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
+             const double* __restrict__ dop, const int32_t* __restrict__ cluster_ids,
+             int64_t frame_id, const uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
+  __shared__ double redd[32];
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  block_refit(n, az + b, dop + b, mask + b, frame_id, cluster_ids ? cluster_ids[c] : c, est + c,
+              redd);
+}
+
+__global__ void __launch_bounds__(kSelectThreads)
+exact_counts_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ keys,
+                    const double2* __restrict__ xy64, const float2* __restrict__ xy32,
+                    const double* __restrict__ thr, int T, uint64_t seed,
+                    int32_t* __restrict__ counts) {
+  const int c = blockIdx.x;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double th = thr[c];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < T; t += nw) {
+    const ExactHyp H = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th);
+    const int e = warp_exact_count(H, n, xy32 + b, xy64 + b, th);
+    if ((threadIdx.x & 31) == 0) counts[static_cast<int64_t>(c) * T + t] = e;
+  }
+}
+
+__global__ void seed_pairs_kernel(const int64_t* __restrict__ offsets,
+                                  const int32_t* __restrict__ keys, int32_t n_clusters, int T,
+                                  uint64_t seed, int32_t* __restrict__ pairs) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(n_clusters) * T) return;
+  const int c = static_cast<int>(idx / T), t = static_cast<int>(idx % T);
+  const int n = static_cast<int>(offsets[c + 1] - offsets[c]);
+  int i, j;
+  seed_pair(seed, keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c),
+            static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+  pairs[2 * idx] = i;
+  pairs[2 * idx + 1] = j;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+
+void launch_prep(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  prep_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(f.n_clusters, f.offsets, f.azimuth,
+                                                      f.doppler, scale, s.xy64, s.xy32, s.thr,
+                                                      s.norm);
+  count_launch();
+}
+
+void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                  cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  const int tpc = (p.max_trials + kHypPerTile - 1) / kHypPerTile;
+  const int64_t grid = static_cast<int64_t>(f.n_clusters) * tpc;
+  score_kernel<<<static_cast<unsigned>(grid), kScoreThreads, 0, st>>>(
+      f.offsets, s.xy64, s.xy32, s.thr, f.keys, f.order, p.max_trials, tpc, p.rng_seed, s.upper);
+  count_launch();
+}
+
+void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                   const Outputs& o, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  select_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
+      f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.thr,
+      s.upper, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial, o.mask, o.est);
+  count_launch();
+}
+
+void launch_refit(const FrameDev& f, const uint8_t* mask, rvk_estimate* est, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  refit_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(f.offsets, f.azimuth, f.doppler,
+                                                        f.cluster_ids, f.frame_id, mask, est);
+  count_launch();
+}
+
+void launch_exact_counts(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                         int32_t* counts, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  exact_counts_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
+      f.offsets, f.keys, s.xy64, s.xy32, s.thr, p.max_trials, p.rng_seed, counts);
+  count_launch();
+}
+
+void launch_seed_pairs(const FrameDev& f, const rvk_ransac_params& p, int32_t* pairs,
+                       cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(f.n_clusters) * p.max_trials;
+  if (total == 0) return;
+  seed_pairs_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      f.offsets, f.keys, f.n_clusters, p.max_trials, p.rng_seed, pairs);
+  count_launch();
+}
+
+}  // namespace rvk_gpu

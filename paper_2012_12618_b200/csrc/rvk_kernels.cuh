@@ -1,0 +1,60 @@
+// Host-side launchers for the sm_100a kernels in rvk_kernels.cu.
+// All launchers are asynchronous on `stream` and count their launches in
+// the calling thread's counter (rvk_kernel_launches()).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/rvk_gpu.h"
+
+namespace rvk_gpu {
+
+struct FrameDev {
+  int32_t n_clusters = 0;
+  int64_t n_points = 0;
+  const int64_t* offsets = nullptr;   // [C+1]
+  const double* azimuth = nullptr;    // [P]
+  const double* doppler = nullptr;    // [P]
+  const int32_t* keys = nullptr;      // [C] RNG cluster key or null (positional)
+  const int32_t* cluster_ids = nullptr;  // [C] or null (positional)
+  const int32_t* order = nullptr;     // [C] scoring order (largest first) or null
+  int64_t frame_id = 0;
+};
+
+struct Scratch {
+  double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
+  float2* xy32 = nullptr;    // [P] normalized (x, y), FP32
+  double* thr = nullptr;     // [C]
+  double* norm = nullptr;    // [4C] (offset_az, offset_dop, scale_az, scale_dop)
+  int32_t* upper = nullptr;  // [C*T] fast-pass upper-bound counts
+};
+
+struct Outputs {
+  int32_t* inlier_count = nullptr;   // [C]
+  int32_t* winning_trial = nullptr;  // [C]
+  uint8_t* mask = nullptr;           // [P] (required by the select kernel)
+  rvk_estimate* est = nullptr;       // [C] or null (no refit)
+};
+
+void count_launch();
+
+// normalize_cluster + median + mad_threshold per cluster.
+void launch_prep(const FrameDev& f, double threshold_scale, const Scratch& s, cudaStream_t st);
+// Fast FP32 scoring: upper-bound inlier counts for every (cluster, trial).
+void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                  cudaStream_t st);
+// Exact argmax (verifying every candidate that could win), winner mask,
+// optional LSQ refit + heading.
+void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                   const Outputs& o, cudaStream_t st);
+// estimate_all on caller masks.
+void launch_refit(const FrameDev& f, const uint8_t* mask, rvk_estimate* est, cudaStream_t st);
+// Exact count of every (cluster, trial).
+void launch_exact_counts(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                         int32_t* counts, cudaStream_t st);
+void launch_seed_pairs(const FrameDev& f, const rvk_ransac_params& p, int32_t* pairs,
+                       cudaStream_t st);
+
+}  // namespace rvk_gpu

@@ -1,0 +1,118 @@
+"""Shared fixtures.
+
+Markers: ``gpu`` -- needs a CUDA device (run on the B200 box with
+``pytest -m gpu``); everything else runs on CPU.
+
+The CPU checkers (oracle/) and the native libraries are (re)built on first
+use if missing or stale: the C oracle always; the reference build only where
+/root/reference exists (this container) -- on the GPU box the prebuilt
+oracle/_ref files arrive with the repo snapshot.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+_built = False
+
+
+def _ensure_built():
+    global _built
+    if _built:
+        return
+    from oracle import binding
+    binding.build(reference=True)
+    from paper_2012_12618_b200 import build as pkg_build
+    pkg_build.build()
+    _built = True
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    _ensure_built()
+    from oracle.binding import Oracle
+    return Oracle()
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The unmodified reference build, or skip where it was never built."""
+    _ensure_built()
+    from oracle.binding import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref/librvk_ref.so not built (no /root/reference here)")
+    return Reference()
+
+
+@pytest.fixture(scope="session")
+def golden_cases():
+    data = np.load(os.path.join(GOLDEN, "cases.npz"))
+    names = [str(n) for n in data["names"]]
+    out = []
+    for n in names:
+        pre = n + "/"
+        T, scale, _ = data[pre + "params"]
+        out.append(dict(
+            name=n, offsets=data[pre + "offsets"], az=data[pre + "az"], dop=data[pre + "dop"],
+            max_trials=int(T), threshold_scale=float(scale), seed=int(data[pre + "seed"][0]),
+            inlier_count=data[pre + "inlier_count"], winning_trial=data[pre + "winning_trial"],
+            mask=data[pre + "mask"], trial_counts=data[pre + "trial_counts"],
+            norm=data[pre + "norm"], threshold=data[pre + "threshold"],
+            normalized=data[pre + "normalized"], estimates=data[pre + "estimates"],
+            frame_id=names.index(n)))
+    return out
+
+
+@pytest.fixture(scope="session")
+def golden_rng():
+    return dict(np.load(os.path.join(GOLDEN, "rng.npz")))
+
+
+@pytest.fixture(scope="session")
+def golden_scene():
+    d = np.load(os.path.join(GOLDEN, "scene.npz"))
+    return [dict(seed=int(d[f"{i}/seed"][0]), objects=d[f"{i}/objects"], x=d[f"{i}/x"],
+                 y=d[f"{i}/y"], doppler=d[f"{i}/doppler"], azimuth=d[f"{i}/azimuth"],
+                 outlier=d[f"{i}/outlier"]) for i in range(int(d["n"][0]))]
+
+
+@pytest.fixture(scope="session")
+def gpu_lib():
+    """The CUDA library on a real device (the GPU tests' entry point)."""
+    _ensure_built()
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2012_12618_b200 import _native
+    return _native.gpu()
+
+
+def assert_estimates_close(got, want, rel=1e-4, heading_tol=1e-3, label=""):
+    """Tolerance of the north_star: v_x, v_y, speed within 1e-4 relative
+    (absolute floor 1e-9 m/s), heading within 1e-3 rad; discrete fields exact."""
+    assert got.shape == want.shape
+    for f in ("frame_id", "cluster_id", "inlier_count", "condition_ok", "has_heading"):
+        np.testing.assert_array_equal(got[f], want[f], err_msg=f"{label} field {f}")
+    for f in ("v_x", "v_y"):
+        np.testing.assert_allclose(got[f], want[f], rtol=rel, atol=1e-9, err_msg=f"{label} {f}")
+    sp_g = np.hypot(got["v_x"], got["v_y"])
+    sp_w = np.hypot(want["v_x"], want["v_y"])
+    np.testing.assert_allclose(sp_g, sp_w, rtol=rel, atol=1e-9, err_msg=f"{label} speed")
+    h = want["has_heading"] == 1
+    dh = np.abs(np.remainder(got["heading"][h] - want["heading"][h] + np.pi, 2 * np.pi) - np.pi)
+    assert (dh <= heading_tol).all(), f"{label} heading off by {dh.max()}"

@@ -1,0 +1,271 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the oracle and the
+reference's golden vectors.
+
+Bar (BASELINE.json north_star): seed pairs, thresholds, per-trial counts,
+inlier counts, winning trials and masks bit-exact; v_x, v_y, speed within
+1e-4 relative and heading within 1e-3 rad, condition_ok / heading presence
+exact (assert_estimates_close).
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2012_12618_b200 as rvk
+from paper_2012_12618_b200 import workloads as W
+from conftest import ROOT, assert_estimates_close
+from oracle.binding import make_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _params(g):
+    return rvk.RansacParams(g["max_trials"], g["threshold_scale"], g["seed"])
+
+
+def _oracle_params(p):
+    return make_params(p.max_trials, p.threshold_scale, p.rng_seed)
+
+
+def test_native_library_is_the_cuda_one(gpu_lib):
+    assert gpu_lib.rvk_abi_version() == 1
+    gpu_lib.rvk_reset_kernel_launches()
+    off = np.array([0, 5], np.int64)
+    rvk.run_ransac_csr(off, np.linspace(0, 1, 5), np.linspace(1, 2, 5), rvk.RansacParams(8))
+    assert gpu_lib.rvk_kernel_launches() == 3  # prep, score, select
+
+
+def test_seed_pairs_vs_oracle(gpu_lib, oracle):
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        k = int(rng.integers(1, 8))
+        sizes = rng.choice([2, 3, 5, 64, 100, 2048, 70000], size=k)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        keys = rng.integers(0, 10000, size=k).astype(np.int32)
+        p = rvk.RansacParams(int(rng.integers(1, 300)), 1.0, int(rng.integers(0, 2**63)) * 2 + 1)
+        got = rvk.seed_pairs_csr(off, p, rng_cluster_index=keys)
+        for c in range(k):
+            for t in range(0, p.max_trials, 7):
+                assert tuple(got[c, t]) == oracle.seed_pair(p.rng_seed, int(keys[c]), t,
+                                                            int(sizes[c]))
+
+
+def test_seed_pairs_golden(gpu_lib, golden_rng):
+    ins, outs = golden_rng["seed_pair_in"], golden_rng["seed_pair_out"]
+    for (s, c, t, n), want in list(zip(ins, outs))[:300]:
+        got = rvk.draw_seed_pair(int(s), int(c), int(t), int(n))
+        assert got == tuple(int(v) for v in want)
+
+
+def test_thresholds_golden(gpu_lib, golden_cases):
+    for g in golden_cases:
+        norm, thr = rvk.cluster_thresholds_csr(g["offsets"], g["az"], g["dop"],
+                                               g["threshold_scale"])
+        np.testing.assert_array_equal(norm, g["norm"], err_msg=g["name"])
+        np.testing.assert_array_equal(thr, g["threshold"], err_msg=g["name"])
+
+
+def test_trial_counts_golden(gpu_lib, golden_cases):
+    for g in golden_cases:
+        got = rvk.trial_counts_csr(g["offsets"], g["az"], g["dop"], _params(g))
+        np.testing.assert_array_equal(got, g["trial_counts"], err_msg=g["name"])
+
+
+def test_ransac_golden(gpu_lib, golden_cases):
+    for g in golden_cases:
+        r = rvk.run_ransac_csr(g["offsets"], g["az"], g["dop"], _params(g))
+        np.testing.assert_array_equal(r.inlier_count, g["inlier_count"], err_msg=g["name"])
+        np.testing.assert_array_equal(r.winning_trial, g["winning_trial"], err_msg=g["name"])
+        np.testing.assert_array_equal(r.mask, g["mask"], err_msg=g["name"])
+
+
+def test_ransac_estimate_golden(gpu_lib, golden_cases):
+    for g in golden_cases:
+        n = g["offsets"].size - 1
+        r, est = rvk.ransac_estimate_csr(g["offsets"], g["az"], g["dop"], _params(g),
+                                         frame_id=g["frame_id"],
+                                         cluster_ids=np.arange(n, dtype=np.int32) + 100)
+        np.testing.assert_array_equal(r.mask, g["mask"], err_msg=g["name"])
+        assert_estimates_close(est, g["estimates"], label=g["name"])
+        # estimate_all on the reference's masks too
+        est2 = rvk.estimate_all_csr(g["offsets"], g["az"], g["dop"], g["mask"],
+                                    frame_id=g["frame_id"],
+                                    cluster_ids=np.arange(n, dtype=np.int32) + 100)
+        assert_estimates_close(est2, g["estimates"], label=g["name"] + "/estimate_all")
+
+
+def test_c3_thousand_random_frames(gpu_lib, oracle):
+    """Acceptance C3 (acceptance_test.cpp:257-330) against the GPU: 1000
+    frames, 1-4 clusters x 5-40 points, T in [16, 96], random 64-bit seed."""
+    rng = np.random.default_rng(303)
+    for f in range(1000):
+        off, az, dop = W.random_clusters(rng, int(rng.integers(1, 5)))
+        p = rvk.RansacParams(int(rng.integers(16, 97)), 1.0, int(rng.integers(0, 2**63)))
+        r, est = rvk.ransac_estimate_csr(off, az, dop, p, frame_id=f)
+        o = oracle.sequential_ransac(off, az, dop, _oracle_params(p))
+        np.testing.assert_array_equal(r.mask, o.mask, err_msg=f"frame {f}")
+        np.testing.assert_array_equal(r.winning_trial, o.winning_trial, err_msg=f"frame {f}")
+        np.testing.assert_array_equal(r.inlier_count, o.inlier_count, err_msg=f"frame {f}")
+        oe = oracle.estimate_all(off, az, dop, o.mask, frame_id=f)
+        assert_estimates_close(est, oe, label=f"frame {f}")
+
+
+@pytest.mark.parametrize("scale", [1.0, 0.25, 1e-3, 3.0])
+def test_radar_frames_all_trial_counts(gpu_lib, oracle, scale):
+    """Per-trial counts exact for every trial (not only the verified ones)."""
+    w = W.automotive(seed=5, n_clusters=12, max_trials=96, lo_pts=16, hi_pts=400)
+    p = rvk.RansacParams(96, scale, 99)
+    got = rvk.trial_counts_csr(w.offsets, w.azimuth, w.doppler, p)
+    want = oracle.trial_counts(w.offsets, w.azimuth, w.doppler, _oracle_params(p))
+    np.testing.assert_array_equal(got, want)
+    r = rvk.run_ransac_csr(w.offsets, w.azimuth, w.doppler, p)
+    o = oracle.sequential_ransac(w.offsets, w.azimuth, w.doppler, _oracle_params(p))
+    np.testing.assert_array_equal(r.mask, o.mask)
+    np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
+
+
+def test_config1_full(gpu_lib, oracle):
+    w = W.single_frame()
+    p = rvk.RansacParams(w.max_trials, w.threshold_scale, w.rng_seed)
+    r, est = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+    o, oe = oracle.ransac_estimate_range(w.offsets, w.azimuth, w.doppler, _oracle_params(p), 0,
+                                         w.n_clusters)
+    np.testing.assert_array_equal(r.mask, o.mask)
+    np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
+    np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
+    assert_estimates_close(est, oe)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_full_size_configs_sampled(gpu_lib, oracle, cfg):
+    """Full-size frames on the GPU; the oracle checks a bounded sample of
+    clusters (the largest ones and a spread of others) bit-exactly."""
+    w = W.CONFIGS[cfg]()
+    p = rvk.RansacParams(w.max_trials, w.threshold_scale, w.rng_seed)
+    r, est = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+    sizes = np.diff(w.offsets)
+    budget = 1.5e8  # oracle evals
+    order = np.argsort(-sizes, kind="stable")
+    picks = list(order[:2]) + list(range(0, w.n_clusters, max(1, w.n_clusters // 12)))
+    done = 0
+    for c in sorted(set(int(c) for c in picks)):
+        if done + sizes[c] * w.max_trials > budget:
+            continue
+        done += sizes[c] * w.max_trials
+        o, oe = oracle.ransac_estimate_range(w.offsets, w.azimuth, w.doppler,
+                                             _oracle_params(p), c, c + 1)
+        sl = slice(w.offsets[c], w.offsets[c + 1])
+        np.testing.assert_array_equal(r.mask[sl], o.mask[sl], err_msg=f"cfg {cfg} cluster {c}")
+        assert r.winning_trial[c] == o.winning_trial[c]
+        assert r.inlier_count[c] == o.inlier_count[c]
+        assert_estimates_close(est[c:c + 1], oe[c:c + 1], label=f"cfg {cfg} cluster {c}")
+    # size-independent properties over every cluster
+    per = np.add.reduceat(r.mask.astype(np.int64), w.offsets[:-1])
+    np.testing.assert_array_equal(per, r.inlier_count)
+    np.testing.assert_array_equal(est["inlier_count"], r.inlier_count)
+    assert (r.winning_trial >= 0).all() and (r.winning_trial < w.max_trials).all()
+    pairs = rvk.seed_pairs_csr(w.offsets, p)
+    idx = np.arange(w.n_clusters)
+    a = pairs[idx, r.winning_trial, 0] + w.offsets[:-1]
+    b = pairs[idx, r.winning_trial, 1] + w.offsets[:-1]
+    assert r.mask[a].all() and r.mask[b].all()  # the winner contains its seeds
+
+
+def test_batch_composition_invariance(gpu_lib):
+    """Splitting a frame into batches with frame-local RNG keys gives
+    byte-identical results (the reference's worker-count invariance)."""
+    w = W.imaging(n_clusters=600, total=120_000)
+    p = rvk.RansacParams(256, 1.0, 12345)
+    full, est = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+    h = w.n_clusters // 3
+    for lo, hi in [(0, h), (h, w.n_clusters)]:
+        off = w.offsets[lo:hi + 1] - w.offsets[lo]
+        sl = slice(w.offsets[lo], w.offsets[hi])
+        r, e = rvk.ransac_estimate_csr(off, w.azimuth[sl], w.doppler[sl], p,
+                                       rng_cluster_index=np.arange(lo, hi, dtype=np.int32))
+        np.testing.assert_array_equal(r.mask, full.mask[sl])
+        np.testing.assert_array_equal(r.winning_trial, full.winning_trial[lo:hi])
+        for f in ("v_x", "v_y", "heading"):
+            np.testing.assert_array_equal(e[f], est[f][lo:hi])
+
+
+def test_edge_cases(gpu_lib, oracle):
+    rng = np.random.default_rng(11)
+    cases = []
+    # huge cluster (> shared-memory chunk), odd sizes, odd base offsets
+    cases.append([rng.uniform(-1, 1, (9001, 2)) * [1, 10]])
+    cases.append([rng.uniform(-1, 1, (3, 2)), rng.uniform(-1, 1, (4, 2)),
+                  rng.uniform(-1, 1, (4097, 2))])
+    # zero spread in azimuth (all degenerate), in doppler (zero MAD)
+    cases.append([np.stack([np.full(20, 0.3), rng.uniform(-5, 5, 20)], 1)])
+    cases.append([np.stack([rng.uniform(-1, 1, 20), np.full(20, 2.0)], 1)])
+    # duplicates + quantized ties
+    q = np.round(rng.uniform(-1, 1, (200, 2)) * 4) / 4
+    cases.append([q, q[:50].copy()])
+    for cl in cases:
+        off, az, dop = rvk.clusters_to_csr(cl)
+        for T, scale in [(1, 1.0), (513, 1.0), (64, 1e-6), (300, 0.25)]:
+            p = rvk.RansacParams(T, scale, 77)
+            r = rvk.run_ransac_csr(off, az, dop, p)
+            o = oracle.sequential_ransac(off, az, dop, _oracle_params(p))
+            np.testing.assert_array_equal(r.mask, o.mask)
+            np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
+            np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
+
+
+def test_errors_and_reference_shaped_api(gpu_lib, oracle):
+    with pytest.raises(rvk.ClusterTooSmall, match="cluster 0 has 2 points"):
+        rvk.run_ransac([np.zeros((2, 2))])
+    masks = rvk.run_ransac([np.array([[0.0, 1.0], [0.1, 1.2], [0.2, 1.4], [0.3, 1.6],
+                                      [0.4, 1.8]])], rvk.RansacParams(32))
+    assert masks[0].inlier_count == 5 and masks[0].winning_trial == 0 and masks[0].mask.all()
+    assert rvk.run_ransac([], rvk.RansacParams()) == []
+
+
+def test_device_api_matches_host_api(gpu_lib):
+    import torch
+    w = W.automotive(seed=3, n_clusters=50)
+    p = rvk.RansacParams(w.max_trials, 1.0, 5)
+    r, est = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+    dev = torch.device("cuda")
+    off = torch.from_numpy(w.offsets).to(dev)
+    az = torch.from_numpy(w.azimuth).to(dev)
+    dp = torch.from_numpy(w.doppler).to(dev)
+    out = {"inlier_count": torch.zeros(w.n_clusters, dtype=torch.int32, device=dev),
+           "winning_trial": torch.zeros(w.n_clusters, dtype=torch.int32, device=dev),
+           "mask": torch.zeros(w.n_points, dtype=torch.uint8, device=dev),
+           "est": torch.zeros(w.n_clusters * 48, dtype=torch.uint8, device=dev)}
+    s = torch.cuda.current_stream()
+    rvk.ransac_estimate_device(off, az, dp, p, out, stream=s)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["mask"].cpu().numpy(), r.mask)
+    np.testing.assert_array_equal(out["winning_trial"].cpu().numpy(), r.winning_trial)
+    e = out["est"].cpu().numpy().view(est.dtype)
+    for f in ("v_x", "v_y", "heading", "inlier_count"):
+        np.testing.assert_array_equal(e[f], est[f])
+
+
+def _run_binary(name, extra=()):
+    path = os.path.join(ROOT, "oracle", "_ref", name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (needs /root/reference at build time)")
+    out = subprocess.run([path, *extra], capture_output=True, text=True, timeout=900)
+    return out.returncode, out.stdout + out.stderr
+
+
+def test_reference_unit_suites_against_dropin(gpu_lib):
+    """The reference's own gtest suites (test_ransac, test_baseline,
+    test_velocity, ...) linked against the GPU drop-in."""
+    code, log = _run_binary("rvk_dropin_tests")
+    assert code == 0, log[-4000:]
+
+
+def test_reference_acceptance_against_dropin(gpu_lib):
+    """Acceptance C1, C2, C3 (1000 frames), C5-C7 of the reference against the
+    GPU drop-in. C4 (CPU thread-scaling trend) is about the CPU engine and is
+    excluded."""
+    code, log = _run_binary("rvk_dropin_acceptance", ["--gtest_filter=-C4ScalingTrend"])
+    assert code == 0, log[-4000:]
+    for crit in ("C1", "C2", "C3", "C5", "C6", "C7"):
+        assert f"[ACCEPTANCE] {crit}" in log and ": PASS" in log
