@@ -207,7 +207,7 @@ Scratch scratch(Context& ctx, int32_t n_clusters, int64_t P, int32_t T) {
   Scratch s;
   s.xy64 = ctx.xy64.get<double2>(P);
   s.xy32 = ctx.xy32.get<float2>(P + 2);
-  s.thr = ctx.thr.get<double>(n_clusters);
+  s.stat = ctx.thr.get<double4>(n_clusters);
   s.norm = ctx.norm.get<double>(4 * static_cast<size_t>(n_clusters));
   s.upper = ctx.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
   return s;
@@ -425,6 +425,7 @@ int rvk_trial_counts(int32_t n_clusters, const int64_t* offsets, const double* a
     const size_t nc = static_cast<size_t>(n_clusters) * params->max_trials;
     int32_t* d_counts = ctx.aux.get<int32_t>(nc);
     launch_prep(f, params->threshold_scale, s, ctx.stream);
+    launch_mad_exact(f, params->threshold_scale, s, ctx.stream);
     launch_exact_counts(f, *params, s, d_counts, ctx.stream);
     check_launch();
     void* h = ctx.stage_out.get(sizeof(int32_t) * nc);
@@ -488,17 +489,20 @@ int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const dou
                              false, nullptr, nullptr);
     Scratch s = scratch(ctx, n_clusters, P, 1);
     launch_prep(f, threshold_scale, s, ctx.stream);
+    launch_mad_exact(f, threshold_scale, s, ctx.stream);
     check_launch();
-    const size_t o_thr = align_up(sizeof(double) * 4 * n_clusters);
-    const size_t total = o_thr + sizeof(double) * n_clusters;
+    const size_t o_st = align_up(sizeof(double) * 4 * n_clusters);
+    const size_t total = o_st + sizeof(double4) * n_clusters;
     char* h = static_cast<char*>(ctx.stage_out.get(total));
     RVK_CUDA(cudaMemcpyAsync(h, s.norm, sizeof(double) * 4 * n_clusters, cudaMemcpyDeviceToHost,
                              ctx.stream));
-    RVK_CUDA(cudaMemcpyAsync(h + o_thr, s.thr, sizeof(double) * n_clusters,
+    RVK_CUDA(cudaMemcpyAsync(h + o_st, s.stat, sizeof(double4) * n_clusters,
                              cudaMemcpyDeviceToHost, ctx.stream));
     RVK_CUDA(cudaStreamSynchronize(ctx.stream));
     if (norm) std::memcpy(norm, h, sizeof(double) * 4 * n_clusters);
-    if (threshold) std::memcpy(threshold, h + o_thr, sizeof(double) * n_clusters);
+    const double4* stv = reinterpret_cast<const double4*>(h + o_st);
+    if (threshold)
+      for (int32_t c = 0; c < n_clusters; ++c) threshold[c] = stv[c].w;
     return RVK_OK;
   });
 }

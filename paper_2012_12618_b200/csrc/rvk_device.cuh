@@ -69,11 +69,17 @@ __device__ __forceinline__ bool exact_inlier(const Line& L, double x, double y, 
   return __ddiv_rn(fabs(r), L.den) <= thr;
 }
 
+// The corridor half-width is known as an interval [thr_lo, thr_hi] that
+// contains the reference's FP64 threshold exactly: the prep kernel sums the
+// MAD deviations in parallel and bounds the difference to the reference's
+// left-to-right sum (see prep_kernel); thr_lo == thr_hi once the exact
+// sequential sum has been taken (exact_threshold()).
+
 // FP32 affine form of the same distance, e = A x + B y + C with
 // (A, B, C) = (-m, 1, -c) / den, and two squared corridor bounds:
 //   e^2 <  t2lo  => certainly an inlier of the FP64 test,
 //   e^2 >= t2hi  => certainly an outlier,
-// otherwise the point is decided by exact_inlier(). With x, y in [0, 1]
+// otherwise the point is decided by exact_decide(). With x, y in [0, 1]
 // the FP32 evaluation error of e is <= 4u * S, S = |A| + |B| + |C|,
 // u = 2^-24, and the FP64 reference's own error is <= 4 * 2^-53 * S; the
 // band 2^-21 * S (= 8u S) covers both with a factor ~2 margin, and the
@@ -84,7 +90,7 @@ struct FastHyp {
   float t2lo;  // e^2 < t2lo: certain inlier
 };
 
-__device__ __forceinline__ FastHyp make_fast(const Line& L, double thr) {
+__device__ __forceinline__ FastHyp make_fast(const Line& L, double thr_lo, double thr_hi) {
   FastHyp h;
   if (L.degenerate) {  // scores 0 (src/ransac.cpp:185-187): nothing passes
     h.A = h.B = h.C = 0.f;
@@ -100,10 +106,10 @@ __device__ __forceinline__ FastHyp make_fast(const Line& L, double thr) {
   h.A = __double2float_rn(A);
   h.B = __double2float_rn(B);
   h.C = __double2float_rn(C);
-  const double hi = (thr + band) * (1.0 + 0x1p-30);
+  const double hi = (thr_hi + band) * (1.0 + 0x1p-30);
   h.t2hi = __double2float_ru(hi * hi);
-  if (thr > band) {
-    const double lo = (thr - band) * (1.0 - 0x1p-30);
+  if (thr_lo > band) {
+    const double lo = (thr_lo - band) * (1.0 - 0x1p-30);
     h.t2lo = __double2float_rd(lo * lo);
   } else {
     h.t2lo = 0.f;  // e^2 < 0 never holds: no certain inliers
@@ -119,26 +125,55 @@ struct ExactHyp {
 };
 
 __device__ __forceinline__ ExactHyp make_exact(const double2* __restrict__ xy64, uint64_t seed,
-                                               uint32_t key, uint32_t trial, int n, double thr) {
+                                               uint32_t key, uint32_t trial, int n,
+                                               double thr_lo, double thr_hi) {
   ExactHyp H;
   seed_pair(seed, key, trial, static_cast<uint32_t>(n), H.a, H.b);
   const double2 p = xy64[H.a];
   const double2 q = xy64[H.b];
   H.L = make_line(p.x, p.y, q.x, q.y);
-  H.f = make_fast(H.L, thr);
+  H.f = make_fast(H.L, thr_lo, thr_hi);
   return H;
 }
 
+enum Decision : int { kOut = 0, kIn = 1, kUndecided = 2 };
+
 // Exact inlier decision of point k for a non-degenerate hypothesis
 // (run_trial, src/ransac.cpp:192-208: seeds counted without evaluation).
-__device__ __forceinline__ bool classify(const ExactHyp& H, int k, float2 p32,
-                                         const double2* __restrict__ xy64, double thr) {
-  if (k == H.a || k == H.b) return true;
+// kUndecided only when the FP64 distance falls inside [thr_lo, thr_hi],
+// i.e. the threshold's last bits matter and the exact sequential MAD sum is
+// needed.
+__device__ __forceinline__ int classify(const ExactHyp& H, int k, float2 p32,
+                                        const double2* __restrict__ xy64, double thr_lo,
+                                        double thr_hi) {
+  if (k == H.a || k == H.b) return kIn;
   const float e = __fmaf_rn(H.f.A, p32.x, __fmaf_rn(H.f.B, p32.y, H.f.C));
-  if (__fmaf_rn(e, e, -H.f.t2lo) < 0.f) return true;
-  if (!(__fmaf_rn(e, e, -H.f.t2hi) < 0.f)) return false;
+  if (__fmaf_rn(e, e, -H.f.t2lo) < 0.f) return kIn;
+  if (!(__fmaf_rn(e, e, -H.f.t2hi) < 0.f)) return kOut;
   const double2 q = xy64[k];
-  return exact_inlier(H.L, q.x, q.y, thr);
+  const double r = __dsub_rn(__dadd_rn(__dmul_rn(-H.L.m, q.x), q.y), H.L.c);
+  const double d = __ddiv_rn(fabs(r), H.L.den);
+  if (d <= thr_lo) return kIn;
+  if (d > thr_hi) return kOut;
+  return kUndecided;
+}
+
+// The reference's threshold bit for bit: mean_abs_deviation's left-to-right
+// sum (include/rvk/ransac.hpp:74-84) then mad_threshold's scale
+// (src/ransac.cpp:234-239). One thread; n dependent FP64 adds.
+__device__ __forceinline__ double exact_threshold(const double2* xy64, int n, double med,
+                                                  double scale) {
+  double acc = 0.0;
+  int k = 0;
+  for (; k + 8 <= n; k += 8) {
+    double d[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = fabs(__dsub_rn(xy64[k + q].y, med));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = __dadd_rn(acc, d[q]);
+  }
+  for (; k < n; ++k) acc = __dadd_rn(acc, fabs(__dsub_rn(xy64[k].y, med)));
+  return __dmul_rn(scale, __ddiv_rn(acc, static_cast<double>(n)));
 }
 
 // Packs (count, trial) so that a max picks the largest count and, on ties,

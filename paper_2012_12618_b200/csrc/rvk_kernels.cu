@@ -26,6 +26,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <math_constants.h>
+
 #include "rvk_device.cuh"
 #include "rvk_kernels.cuh"
 
@@ -42,6 +44,7 @@ constexpr int kHypPerThread = 4;  // two FFMA2 pairs
 constexpr int kHypPerTile = kScoreThreads * kHypPerThread;
 constexpr int kChunk = 4096;      // points staged per shared-memory chunk
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
+constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
 // ---------------------------------------------------------------- helpers
 
@@ -146,12 +149,50 @@ __device__ double block_select_y(const double2* xy, int n, int k,
 
 // ------------------------------------------------------------- prep kernel
 
+// Ascending bitonic sort of N (power of two, <= kSortCap) doubles in shared
+// memory by the whole block.
+__device__ void block_bitonic_sort(double* s, int N) {
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double a = s[i], b = s[ixj];
+          const bool asc = (i & k) == 0;
+          if ((a > b) == asc) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Per cluster (one CTA): normalize_cluster (src/ransac.cpp:214-232), the
+// median of the normalized dopplers (ransac.hpp:53-70, exact: bitonic sort in
+// shared memory, or radix select over global memory for huge clusters), and
+// the MAD corridor as a guaranteed interval.
+//
+// The reference sums |y_i - med| left to right (ransac.hpp:78-83), n
+// dependent FP64 adds; that order cannot be parallelized bit-exactly. Here
+// the deviations (identical doubles) are summed in a tree; for non-negative
+// terms any summation order is within gamma_{n-1} * S of the exact sum S, so
+// the reference's sum lies within 2 gamma_{n-1} S_tree of ours, and after the
+// division by n and the scale multiply (a few more roundings) the reference's
+// threshold lies in thr_mid * (1 -/+ (4n + 16) 2^-53). Every consumer decides
+// with that interval and takes the exact sequential sum only when a distance
+// lands inside it (exact_threshold(); practically never).
+//
+// stat[c] = (thr_lo, thr_hi, median, thr_exact or NaN).
 __global__ void __launch_bounds__(kPrepThreads)
 prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
             const double* __restrict__ az, const double* __restrict__ dop, double scale,
-            double2* xy64, float2* __restrict__ xy32, double* __restrict__ thr,
+            double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
             double* __restrict__ norm) {
   __shared__ double red[32];
+  __shared__ double sy[kSortCap];
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long sh_prefix;
   __shared__ int sh_k;
@@ -159,7 +200,6 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
 
-  // normalize_cluster (src/ransac.cpp:214-232): per-axis min/max, exact.
   double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double a = az[b + k], d = dop[b + k];
@@ -174,12 +214,18 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   hi1 = block_reduce(hi1, MaxOp(), red);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
+  const bool in_smem = n <= kSortCap;
+  int N = 1;
+  while (N < n) N <<= 1;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
     xy32[b + k] = make_float2(__double2float_rn(x), __double2float_rn(y));
+    if (in_smem) sy[k] = y;
   }
+  if (in_smem)
+    for (int k = n + threadIdx.x; k < N; k += blockDim.x) sy[k] = CUDART_INF;
   if (threadIdx.x == 0 && norm != nullptr) {
     norm[4 * c + 0] = lo0;
     norm[4 * c + 1] = lo1;
@@ -188,37 +234,50 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   }
   __syncthreads();
 
-  // median (include/rvk/ransac.hpp:53-70): middle element, or the mean of
-  // the middle pair for even n, of the sorted normalized dopplers.
-  const double2* cxy = xy64 + b;
   double med;
-  if (n & 1) {
-    med = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+  if (in_smem) {
+    block_bitonic_sort(sy, N);
+    med = (n & 1) ? sy[n / 2] : __ddiv_rn(__dadd_rn(sy[n / 2 - 1], sy[n / 2]), 2.0);
   } else {
-    const double lo = block_select_y(cxy, n, n / 2 - 1, hist, &sh_prefix, &sh_k);
-    const double hi = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
-    med = __ddiv_rn(__dadd_rn(lo, hi), 2.0);
+    const double2* cxy = xy64 + b;
+    if (n & 1) {
+      med = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+    } else {
+      const double lo = block_select_y(cxy, n, n / 2 - 1, hist, &sh_prefix, &sh_k);
+      const double hi = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+      med = __ddiv_rn(__dadd_rn(lo, hi), 2.0);
+    }
   }
 
-  // mean_abs_deviation (ransac.hpp:74-84): the sum is order-sensitive, so it
-  // runs sequentially in index order, exactly as the reference.
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    int k = 0;
-    for (; k + 4 <= n; k += 4) {
-      const double d0 = fabs(__dsub_rn(cxy[k].y, med));
-      const double d1 = fabs(__dsub_rn(cxy[k + 1].y, med));
-      const double d2 = fabs(__dsub_rn(cxy[k + 2].y, med));
-      const double d3 = fabs(__dsub_rn(cxy[k + 3].y, med));
-      acc = __dadd_rn(acc, d0);
-      acc = __dadd_rn(acc, d1);
-      acc = __dadd_rn(acc, d2);
-      acc = __dadd_rn(acc, d3);
-    }
-    for (; k < n; ++k) acc = __dadd_rn(acc, fabs(__dsub_rn(cxy[k].y, med)));
-    // mad_threshold (src/ransac.cpp:234-239)
-    thr[c] = __dmul_rn(scale, __ddiv_rn(acc, static_cast<double>(n)));
+  double part = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const double y = in_smem ? sy[k] : xy64[b + k].y;
+    part += fabs(__dsub_rn(y, med));
   }
+  const double S = block_reduce(part, SumD(), red);
+  if (threadIdx.x == 0) {
+    const double mid = scale * (S / n);
+    const double delta = (4.0 * n + 16.0) * 0x1p-53;
+    stat[c] = make_double4(mid * (1.0 - delta), mid * (1.0 + delta), med, CUDART_NAN);
+  }
+}
+
+// The exact reference threshold (left-to-right MAD sum), one warp per
+// cluster: used where the threshold itself is an output
+// (rvk_cluster_thresholds) and by the all-trials exact counter.
+__global__ void mad_exact_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                                 const double2* __restrict__ xy64, double scale,
+                                 double4* __restrict__ stat) {
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n_clusters || (threadIdx.x & 31) != 0) return;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  double4 st = stat[c];
+  const double t = exact_threshold(xy64 + b, n, st.z, scale);
+  st.x = t;
+  st.y = t;
+  st.w = t;
+  stat[c] = st;
 }
 
 // ------------------------------------------------------------ score kernel
@@ -230,7 +289,7 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 // and the sign bit of g accumulated into an integer count.
 __global__ void __launch_bounds__(kScoreThreads)
 score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy64,
-             const float2* __restrict__ xy32, const double* __restrict__ thr,
+             const float2* __restrict__ xy32, const double4* __restrict__ stat,
              const int32_t* __restrict__ keys, const int32_t* __restrict__ order, int T,
              int tiles_per_cluster, uint64_t seed, int32_t* __restrict__ upper) {
   __shared__ float4 pts[kChunk / 2];
@@ -241,7 +300,7 @@ score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-  const double th = thr[c];
+  const double4 st = stat[c];
 
   float2 A[2], B[2], Cc[2], T2[2];
 #pragma unroll
@@ -249,7 +308,7 @@ score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy
     const int t = tb * kHypPerTile + q * kScoreThreads + threadIdx.x;
     FastHyp f;
     if (t < T) {
-      f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th).f;
+      f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, st.x, st.y).f;
     } else {
       f.A = f.B = f.C = 0.f;
       f.t2hi = -1.f;
@@ -311,11 +370,20 @@ score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy
 
 // ----------------------------------------------------------- select kernel
 
+// Exact count of one hypothesis by one warp; sets *undecided when some
+// point's FP64 distance fell inside the threshold interval.
 __device__ int warp_exact_count(const ExactHyp& H, int n, const float2* __restrict__ p32,
-                                const double2* __restrict__ p64, double th) {
+                                const double2* __restrict__ p64, double thr_lo, double thr_hi,
+                                bool* undecided) {
   if (H.L.degenerate) return 0;
   int cnt = 0;
-  for (int k = threadIdx.x & 31; k < n; k += 32) cnt += classify(H, k, p32[k], p64, th) ? 1 : 0;
+  bool und = false;
+  for (int k = threadIdx.x & 31; k < n; k += 32) {
+    const int d = classify(H, k, p32[k], p64, thr_lo, thr_hi);
+    cnt += d == kIn;
+    und |= d == kUndecided;
+  }
+  *undecided = __any_sync(0xffffffffu, und);
   return warp_reduce(cnt, SumI());
 }
 
@@ -420,58 +488,121 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
   *out = e;
 }
 
+// Exact winner per cluster (one CTA). With U = the fast pass's upper bounds
+// (exact[t] <= U[t]), t0 = the lowest trial with the largest U and
+// E0 = exact[t0], a trial t can only beat or tie-win against t0 if
+// U[t] > E0, or U[t] == E0 and t < t0 (ties go to the lowest trial,
+// src/ransac.cpp:326-334). Only those are verified; when U[t0] == E0 there
+// are none. Then the winner's mask (evaluate_trial, :274-281) and the LSQ
+// refit on its inliers.
 __global__ void __launch_bounds__(kSelectThreads)
 select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
               const double* __restrict__ dop, const int32_t* __restrict__ keys,
               const int32_t* __restrict__ cluster_ids, int64_t frame_id,
               const double2* __restrict__ xy64, const float2* __restrict__ xy32,
-              const double* __restrict__ thr, const int32_t* __restrict__ upper, int T,
-              uint64_t seed, int32_t* __restrict__ out_count, int32_t* __restrict__ out_trial,
-              uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
+              const double4* __restrict__ stat, double scale, const int32_t* __restrict__ upper,
+              int T, uint64_t seed, int32_t* __restrict__ out_count,
+              int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
+              rvk_estimate* __restrict__ est) {
   __shared__ unsigned long long redu[32];
   __shared__ int redi[32];
   __shared__ double redd[32];
   __shared__ unsigned long long best;
+  __shared__ double sh_thr;
+  __shared__ int sh_need_exact;
   const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-  const double th = thr[c];
+  const double4 st = stat[c];
+  double thr_lo = st.x, thr_hi = st.y;
   const float2* p32 = xy32 + b;
   const double2* p64 = xy64 + b;
   const int32_t* U = upper + static_cast<int64_t>(c) * T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+
+  // Switches the whole block to the exact sequential threshold (rare).
+  auto go_exact = [&]() {
+    if (threadIdx.x == 0) sh_thr = exact_threshold(p64, n, st.z, scale);
+    __syncthreads();
+    thr_lo = thr_hi = sh_thr;
+  };
 
   // 1. trial with the largest upper bound (lowest index on ties).
   unsigned long long v = 0;
   for (int t = threadIdx.x; t < T; t += blockDim.x) v = MaxU64()(v, pack_best(U[t], t));
   v = block_reduce(v, MaxU64(), redu);
   const int t0 = unpack_trial(v);
+  const int u0 = unpack_count(v);
 
   // 2. its exact count.
-  const ExactHyp H0 = make_exact(p64, seed, key, static_cast<uint32_t>(t0), n, th);
   int e0 = 0;
-  if (!H0.L.degenerate)
-    for (int k = threadIdx.x; k < n; k += blockDim.x) e0 += classify(H0, k, p32[k], p64, th);
-  e0 = block_reduce(e0, SumI(), redi);
-  if (threadIdx.x == 0) best = pack_best(e0, t0);
+  for (int pass = 0; pass < 2; ++pass) {
+    const ExactHyp H0 = make_exact(p64, seed, key, static_cast<uint32_t>(t0), n, thr_lo, thr_hi);
+    int cnt = 0;
+    bool und = false;
+    if (!H0.L.degenerate)
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int d = classify(H0, k, p32[k], p64, thr_lo, thr_hi);
+        cnt += d == kIn;
+        und |= d == kUndecided;
+      }
+    if (__syncthreads_or(und)) {
+      go_exact();
+      continue;
+    }
+    e0 = block_reduce(cnt, SumI(), redi);
+    break;
+  }
+  if (threadIdx.x == 0) {
+    best = pack_best(e0, t0);
+    sh_need_exact = 0;
+  }
   __syncthreads();
 
-  // 3. verify every other trial that could reach e0 (warp per candidate).
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int t = warp; t < T; t += nw) {
-    if (t == t0 || U[t] < e0) continue;
-    const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, th);
-    const int e = warp_exact_count(H, n, p32, p64, th);
-    if ((threadIdx.x & 31) == 0) atomicMax(&best, pack_best(e, t));
+  // 3. verify the trials that could still win (none when u0 == e0).
+  if (u0 > e0) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int t = warp; t < T; t += nw) {
+        const int u = U[t];
+        if (t == t0 || u < e0 || (u == e0 && t > t0)) continue;
+        const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
+        bool und;
+        const int e = warp_exact_count(H, n, p32, p64, thr_lo, thr_hi, &und);
+        if (und) {
+          if (lane == 0) sh_need_exact = 1;
+        } else if (lane == 0) {
+          atomicMax(&best, pack_best(e, t));
+        }
+      }
+      if (__syncthreads_or(sh_need_exact) && pass == 0) {
+        go_exact();  // redo every candidate with the exact threshold
+        if (threadIdx.x == 0) sh_need_exact = 0;
+        __syncthreads();
+        continue;
+      }
+      break;
+    }
   }
   __syncthreads();
   const int win = unpack_trial(best);
   const int win_count = unpack_count(best);
 
   // 4. winner mask (evaluate_trial, src/ransac.cpp:274-281).
-  const ExactHyp W = make_exact(p64, seed, key, static_cast<uint32_t>(win), n, th);
-  for (int k = threadIdx.x; k < n; k += blockDim.x)
-    mask[b + k] = (!W.L.degenerate && classify(W, k, p32[k], p64, th)) ? 1 : 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const ExactHyp W = make_exact(p64, seed, key, static_cast<uint32_t>(win), n, thr_lo, thr_hi);
+    bool und = false;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int d = W.L.degenerate ? kOut : classify(W, k, p32[k], p64, thr_lo, thr_hi);
+      und |= d == kUndecided;
+      mask[b + k] = d == kIn ? 1 : 0;
+    }
+    if (__syncthreads_or(und)) {
+      go_exact();
+      continue;
+    }
+    break;
+  }
   if (threadIdx.x == 0) {
     if (out_count) out_count[c] = win_count;
     if (out_trial) out_trial[c] = win;
@@ -496,20 +627,23 @@ refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
               redd);
 }
 
+// Exact count of every (cluster, trial) (warp per trial). Requires the exact
+// threshold in stat (mad_exact_kernel ran), so nothing is ever undecided.
 __global__ void __launch_bounds__(kSelectThreads)
 exact_counts_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ keys,
                     const double2* __restrict__ xy64, const float2* __restrict__ xy32,
-                    const double* __restrict__ thr, int T, uint64_t seed,
+                    const double4* __restrict__ stat, int T, uint64_t seed,
                     int32_t* __restrict__ counts) {
   const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-  const double th = thr[c];
+  const double th = stat[c].w;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int t = warp; t < T; t += nw) {
-    const ExactHyp H = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th);
-    const int e = warp_exact_count(H, n, xy32 + b, xy64 + b, th);
+    const ExactHyp H = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th, th);
+    bool und;
+    const int e = warp_exact_count(H, n, xy32 + b, xy64 + b, th, th, &und);
     if ((threadIdx.x & 31) == 0) counts[static_cast<int64_t>(c) * T + t] = e;
   }
 }
@@ -535,8 +669,15 @@ __global__ void seed_pairs_kernel(const int64_t* __restrict__ offsets,
 void launch_prep(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
   if (f.n_clusters == 0) return;
   prep_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(f.n_clusters, f.offsets, f.azimuth,
-                                                      f.doppler, scale, s.xy64, s.xy32, s.thr,
+                                                      f.doppler, scale, s.xy64, s.xy32, s.stat,
                                                       s.norm);
+  count_launch();
+}
+
+void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  mad_exact_kernel<<<(f.n_clusters + 7) / 8, 256, 0, st>>>(f.n_clusters, f.offsets, s.xy64,
+                                                           scale, s.stat);
   count_launch();
 }
 
@@ -546,7 +687,7 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   const int tpc = (p.max_trials + kHypPerTile - 1) / kHypPerTile;
   const int64_t grid = static_cast<int64_t>(f.n_clusters) * tpc;
   score_kernel<<<static_cast<unsigned>(grid), kScoreThreads, 0, st>>>(
-      f.offsets, s.xy64, s.xy32, s.thr, f.keys, f.order, p.max_trials, tpc, p.rng_seed, s.upper);
+      f.offsets, s.xy64, s.xy32, s.stat, f.keys, f.order, p.max_trials, tpc, p.rng_seed, s.upper);
   count_launch();
 }
 
@@ -554,8 +695,9 @@ void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch&
                    const Outputs& o, cudaStream_t st) {
   if (f.n_clusters == 0) return;
   select_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
-      f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.thr,
-      s.upper, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial, o.mask, o.est);
+      f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
+      p.threshold_scale, s.upper, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial,
+      o.mask, o.est);
   count_launch();
 }
 
@@ -570,7 +712,7 @@ void launch_exact_counts(const FrameDev& f, const rvk_ransac_params& p, const Sc
                          int32_t* counts, cudaStream_t st) {
   if (f.n_clusters == 0) return;
   exact_counts_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
-      f.offsets, f.keys, s.xy64, s.xy32, s.thr, p.max_trials, p.rng_seed, counts);
+      f.offsets, f.keys, s.xy64, s.xy32, s.stat, p.max_trials, p.rng_seed, counts);
   count_launch();
 }
 

@@ -26,7 +26,7 @@ struct FrameDev {
 struct Scratch {
   double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
   float2* xy32 = nullptr;    // [P] normalized (x, y), FP32
-  double* thr = nullptr;     // [C]
+  double4* stat = nullptr;   // [C] (thr_lo, thr_hi, median, thr_exact|NaN)
   double* norm = nullptr;    // [4C] (offset_az, offset_dop, scale_az, scale_dop)
   int32_t* upper = nullptr;  // [C*T] fast-pass upper-bound counts
 };
@@ -42,6 +42,9 @@ void count_launch();
 
 // normalize_cluster + median + mad_threshold per cluster.
 void launch_prep(const FrameDev& f, double threshold_scale, const Scratch& s, cudaStream_t st);
+// Exact (left-to-right) MAD threshold into stat[c].w (and .x = .y).
+void launch_mad_exact(const FrameDev& f, double threshold_scale, const Scratch& s,
+                      cudaStream_t st);
 // Fast FP32 scoring: upper-bound inlier counts for every (cluster, trial).
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);
