@@ -354,9 +354,9 @@ def main():
         torch.cuda.synchronize()
     launches = lib.rvk_kernel_launches()
     lib.rvk_profile_enable(0)
-    stage_ms = (C.c_double * 3)()
-    stage_n = (C.c_int64 * 3)()
-    lib.rvk_profile_read(stage_ms, stage_n, 3)
+    stage_ms = (C.c_double * 4)()
+    stage_n = (C.c_int64 * 4)()
+    lib.rvk_profile_read(stage_ms, stage_n, 4)
     elapsed = ev[0].elapsed_time(ev[-1]) / 1e3
     per_step = [ev[j].elapsed_time(ev[j + 1]) for j in range(args.steps)]
     if world > 1:
@@ -371,8 +371,8 @@ def main():
         evals_all, clusters_all = float(evals), float(clusters)
 
     # ---- roofline of the dominant kernel (score_kernel)
-    score_ms = stage_ms[1] / max(1, stage_n[1])
-    evals_per_launch = evals / max(1, stage_n[1])
+    score_ms = stage_ms[2] / max(1, stage_n[2])
+    evals_per_launch = evals / max(1, stage_n[2])
     achieved = evals_per_launch * FLOP_PER_EVAL / (score_ms / 1e3) / 1e12
     clk = clk.summary()
     sm_max = clk.get("sm_max_mhz") or 1965
@@ -394,10 +394,11 @@ def main():
                 "nominal_peak": nominal,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals_per_launch,
                 "avg_launch_ms": score_ms, "traffic": traffic,
-                "share_of_step": stage_ms[1] / total_ms if total_ms else None,
+                "share_of_step": stage_ms[2] / total_ms if total_ms else None,
                 "stage_ms_per_step": {"prep": stage_ms[0] / args.steps,
-                                      "score": stage_ms[1] / args.steps,
-                                      "select_refit": stage_ms[2] / args.steps}}
+                                      "hyp_setup": stage_ms[1] / args.steps,
+                                      "score": stage_ms[2] / args.steps,
+                                      "select_refit": stage_ms[3] / args.steps}}
 
     result = None
     if rank == 0:

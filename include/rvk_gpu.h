@@ -155,8 +155,8 @@ int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const dou
                            double* threshold);
 
 /* Stage timing for benchmarking/profiling. When enabled, CUDA events bracket
- * every pipeline stage launch on its stream (0 = prep, 1 = score, 2 =
- * select+refit); rvk_profile_read waits for them, returns the accumulated
+ * every pipeline stage launch on its stream (0 = prep, 1 = hypothesis
+ * setup + tile plan, 2 = score, 3 = select+refit); rvk_profile_read waits for them, returns the accumulated
  * device milliseconds and launch counts per stage, and clears the record. */
 void rvk_profile_enable(int32_t on);
 int rvk_profile_read(double* ms, int64_t* launches, int32_t n_stages);

@@ -91,7 +91,7 @@ struct Context {
   cudaStream_t stream = nullptr;
   DevBuf in;       // offsets | az | dop | ids | keys | order (one H2D)
   DevBuf out;      // count | trial | est | mask (one D2H)
-  DevBuf xy64, xy32, thr, norm, upper, aux;
+  DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, aux;
   HostBuf stage_in, stage_out;
 };
 
@@ -210,6 +210,8 @@ Scratch scratch(Context& ctx, int32_t n_clusters, int64_t P, int32_t T) {
   s.stat = ctx.thr.get<double4>(n_clusters);
   s.norm = ctx.norm.get<double>(4 * static_cast<size_t>(n_clusters));
   s.upper = ctx.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
+  s.hyp = ctx.hyp.get<float4>(static_cast<size_t>(n_clusters) * std::max(T, 1));
+  s.tile_start = ctx.tiles.get<int32_t>(static_cast<size_t>(n_clusters) + 1);
   return s;
 }
 
@@ -262,12 +264,13 @@ void stage(int id, cudaStream_t st, F&& launch) {
   g_prof.recs.push_back(r);
 }
 
-// prep -> score -> select(+refit): the whole device pipeline of one call.
+// prep -> hyps -> score -> select(+refit): the whole device pipeline of one call.
 void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   const Outputs& o, cudaStream_t st) {
   stage(0, st, [&] { launch_prep(f, p.threshold_scale, s, st); });
-  stage(1, st, [&] { launch_score(f, p, s, st); });
-  stage(2, st, [&] { launch_select(f, p, s, o, st); });
+  stage(1, st, [&] { launch_hyps(f, p, s, st); });
+  stage(2, st, [&] { launch_score(f, p, s, st); });
+  stage(3, st, [&] { launch_select(f, p, s, o, st); });
   check_launch();
 }
 

@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
 
 #include <math_constants.h>
@@ -40,9 +41,9 @@ namespace {
 constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
 constexpr int kScoreThreads = 128;
-constexpr int kHypPerThread = 4;  // two FFMA2 pairs
-constexpr int kHypPerTile = kScoreThreads * kHypPerThread;
-constexpr int kChunk = 4096;      // points staged per shared-memory chunk
+constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
+constexpr int kPT = 256;          // points per scoring task (one chunk)
+constexpr int kMaxTileChunks = kScoreThreads / kNH + 1;  // chunks a tile can touch (G >= 8)
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
 constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
@@ -149,25 +150,68 @@ __device__ double block_select_y(const double2* xy, int n, int k,
 
 // ------------------------------------------------------------- prep kernel
 
-// Ascending bitonic sort of N (power of two, <= kSortCap) doubles in shared
-// memory by the whole block.
-__device__ void block_bitonic_sort(double* s, int N) {
-  for (int k = 2; k <= N; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const double a = s[i], b = s[ixj];
-          const bool asc = (i & k) == 0;
-          if ((a > b) == asc) {
-            s[i] = b;
-            s[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
+// k-th smallest (0-based) of n non-negative doubles given as bit patterns in
+// shared memory: MSD radix select with 11-bit digits (6 passes), exact.
+// hist: 2048 counters; sh: 2 ints of scratch.
+__device__ unsigned long long block_radix_select(const unsigned long long* keys, int n, int k,
+                                                 unsigned int* hist, int* sh) {
+  unsigned long long prefix = 0, mask = 0;
+  const int nt = blockDim.x;
+#pragma unroll 1
+  for (int pass = 0; pass < 6; ++pass) {
+    const int shift = pass < 5 ? 53 - 11 * pass : 0;
+    const int bits = pass < 5 ? 11 : 9;
+    const unsigned int nb = 1u << bits;
+    for (int i = threadIdx.x; i < (int)nb; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += nt) {
+      const unsigned long long key = keys[i];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1u);
     }
+    __syncthreads();
+    // Block-wide search for the bucket holding rank k: thread j owns bins
+    // [j*per, (j+1)*per).
+    const int per = (nb + nt - 1) / nt;
+    unsigned int local = 0;
+    for (int q = 0; q < per; ++q) {
+      const int bin = threadIdx.x * per + q;
+      if (bin < (int)nb) local += hist[bin];
+    }
+    // exclusive scan of `local` across the block
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    __shared__ unsigned int wsum[32];
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    unsigned int base = 0;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    const unsigned int excl = base + incl - local;
+    const unsigned int kk = static_cast<unsigned int>(k);
+    if (kk >= excl && kk < excl + local) {
+      unsigned int cum = excl;
+      for (int q = 0; q < per; ++q) {
+        const int bin = threadIdx.x * per + q;
+        const unsigned int h = bin < (int)nb ? hist[bin] : 0u;
+        if (kk < cum + h) {
+          sh[0] = bin;
+          sh[1] = static_cast<int>(kk - cum);
+          break;
+        }
+        cum += h;
+      }
+    }
+    __syncthreads();
+    prefix |= static_cast<unsigned long long>(sh[0]) << shift;
+    mask |= static_cast<unsigned long long>(nb - 1) << shift;
+    k = sh[1];
+    __syncthreads();
   }
+  return prefix;
 }
 
 // Per cluster (one CTA): normalize_cluster (src/ransac.cpp:214-232), the
@@ -192,10 +236,11 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
             double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
             double* __restrict__ norm) {
   __shared__ double red[32];
-  __shared__ double sy[kSortCap];
-  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long sy[kSortCap];  // normalized dopplers (bit patterns)
+  __shared__ unsigned int hist[2048];
   __shared__ unsigned long long sh_prefix;
   __shared__ int sh_k;
+  __shared__ int sh2[2];
   const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
@@ -215,17 +260,13 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   const bool in_smem = n <= kSortCap;
-  int N = 1;
-  while (N < n) N <<= 1;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
     xy32[b + k] = make_float2(__double2float_rn(x), __double2float_rn(y));
-    if (in_smem) sy[k] = y;
+    if (in_smem) sy[k] = static_cast<unsigned long long>(__double_as_longlong(y));
   }
-  if (in_smem)
-    for (int k = n + threadIdx.x; k < N; k += blockDim.x) sy[k] = CUDART_INF;
   if (threadIdx.x == 0 && norm != nullptr) {
     norm[4 * c + 0] = lo0;
     norm[4 * c + 1] = lo1;
@@ -236,8 +277,31 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 
   double med;
   if (in_smem) {
-    block_bitonic_sort(sy, N);
-    med = (n & 1) ? sy[n / 2] : __ddiv_rn(__dadd_rn(sy[n / 2 - 1], sy[n / 2]), 2.0);
+    // k-th order statistics (median of the sorted copy, ransac.hpp:60-69).
+    const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
+    const unsigned long long v0 = block_radix_select(sy, n, k0, hist, sh2);
+    const double d0 = __longlong_as_double(static_cast<long long>(v0));
+    if (n & 1) {
+      med = d0;
+    } else {
+      // next order statistic: v0 again if more than k0+1 keys are <= v0,
+      // else the smallest key above v0.
+      int le = 0;
+      double above = CUDART_INF;
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const unsigned long long key = sy[k];
+        if (key <= v0) {
+          ++le;
+        } else {
+          const double y = __longlong_as_double(static_cast<long long>(key));
+          above = y < above ? y : above;
+        }
+      }
+      le = block_reduce(le, SumI(), reinterpret_cast<int*>(hist));
+      above = block_reduce(above, MinOp(), red);
+      const double d1 = le >= n / 2 + 1 ? d0 : above;
+      med = __ddiv_rn(__dadd_rn(d0, d1), 2.0);
+    }
   } else {
     const double2* cxy = xy64 + b;
     if (n & 1) {
@@ -251,7 +315,8 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 
   double part = 0.0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const double y = in_smem ? sy[k] : xy64[b + k].y;
+    const double y = in_smem ? __longlong_as_double(static_cast<long long>(sy[k]))
+                             : xy64[b + k].y;
     part += fabs(__dsub_rn(y, med));
   }
   const double S = block_reduce(part, SumD(), red);
@@ -282,90 +347,148 @@ __global__ void mad_exact_kernel(int32_t n_clusters, const int64_t* __restrict__
 
 // ------------------------------------------------------------ score kernel
 
-// One CTA = one tile of kHypPerTile trials of one cluster. Each thread owns
-// kHypPerThread hypotheses as two FFMA2 pairs; the cluster's FP32 points are
-// staged in shared memory and read as float4 (two points) broadcasts.
-// Per point and hypothesis pair: 3 FFMA2 (e = A x + (B y + C); g = e^2 - t2)
-// and the sign bit of g accumulated into an integer count.
-__global__ void __launch_bounds__(kScoreThreads)
-score_kernel(const int64_t* __restrict__ offsets, const double2* __restrict__ xy64,
-             const float2* __restrict__ xy32, const double4* __restrict__ stat,
-             const int32_t* __restrict__ keys, const int32_t* __restrict__ order, int T,
-             int tiles_per_cluster, uint64_t seed, int32_t* __restrict__ upper) {
-  __shared__ float4 pts[kChunk / 2];
-  const int tile = blockIdx.x;
-  const int ci = tile / tiles_per_cluster;
-  const int tb = tile - ci * tiles_per_cluster;
-  const int c = order ? order[ci] : ci;
+// One thread per (cluster, trial): seed pair (KeyedRng), exact FP64 line,
+// FP32 coefficients and corridor bound -> hyp[c*T + t] = (A, B, C, -t2hi);
+// also zeroes the upper-bound counters the scoring tiles accumulate into.
+__global__ void hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                           const double2* __restrict__ xy64, const double4* __restrict__ stat,
+                           const int32_t* __restrict__ keys, int T, uint64_t seed,
+                           float4* __restrict__ hyp, int32_t* __restrict__ upper) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(n_clusters) * T) return;
+  const int c = static_cast<int>(idx / T), t = static_cast<int>(idx - static_cast<int64_t>(c) * T);
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double4 st = stat[c];
+  const FastHyp f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, st.x, st.y).f;
+  hyp[idx] = make_float4(f.A, f.B, f.C, -f.t2hi);
+  upper[idx] = 0;
+}
 
-  float2 A[2], B[2], Cc[2], T2[2];
-#pragma unroll
-  for (int q = 0; q < kHypPerThread; ++q) {
-    const int t = tb * kHypPerTile + q * kScoreThreads + threadIdx.x;
-    FastHyp f;
-    if (t < T) {
-      f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, st.x, st.y).f;
-    } else {
-      f.A = f.B = f.C = 0.f;
-      f.t2hi = -1.f;
+// Tile plan: a scoring task = (cluster, group of kNH trials, chunk of kPT
+// points); a tile = 128 consecutive tasks of one cluster (groups fastest), so
+// every tile costs about the same (<= 8 x 256 x 128 evaluations) whatever the
+// cluster sizes. tile_start[c] = exclusive prefix of tiles per cluster.
+__device__ __forceinline__ int score_groups(int T) { return max((T + kNH - 1) / kNH, kNH); }
+
+__global__ void tile_plan_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets, int T,
+                                 int32_t* __restrict__ tile_start) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int G = score_groups(T);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n_clusters; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    int tiles = 0;
+    if (c < n_clusters) {
+      const int n = static_cast<int>(offsets[c + 1] - offsets[c]);
+      const long long tasks = static_cast<long long>(G) * ((n + kPT - 1) / kPT);
+      tiles = static_cast<int>((tasks + kScoreThreads - 1) / kScoreThreads);
     }
-    const int pr = q >> 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = tiles;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = carry;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    if (c < n_clusters) tile_start[c] = off + incl - tiles;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = off + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_start[n_clusters] = carry;
+}
+
+// The hot loop. Each thread scores kNH = 8 hypotheses (four FFMA2 pairs)
+// against the kPT points of its chunk, staged in shared memory and read as
+// float4 broadcasts (two points). Per point and pair: 3 FFMA2
+// (e = A x + (B y + C); g = e^2 - t2hi) and the sign bit of g added to the
+// count (LEA.HI). Counts are upper bounds (guard band, see make_fast) and
+// accumulate over chunks with integer atomics (order-free, deterministic).
+__global__ void __launch_bounds__(kScoreThreads)
+score_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+             const float2* __restrict__ xy32, const float4* __restrict__ hyp,
+             const int32_t* __restrict__ tile_start, int T, int32_t* __restrict__ upper) {
+  __shared__ float4 pts[kMaxTileChunks * kPT / 2];
+  const int tile = blockIdx.x;
+  if (tile >= tile_start[n_clusters]) return;
+  // cluster owning this tile: last c with tile_start[c] <= tile
+  int lo = 0, hi = n_clusters - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  const int c = lo;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const int G = score_groups(T);
+  const int nch = (n + kPT - 1) / kPT;
+  const long long tasks = static_cast<long long>(G) * nch;
+  const long long task0 = static_cast<long long>(tile - tile_start[c]) * kScoreThreads;
+  const int k_first = static_cast<int>(task0 / G);
+  const int k_last = static_cast<int>(min(task0 + kScoreThreads - 1, tasks - 1) / G);
+
+  // stage chunks [k_first, k_last] (padded to even counts per chunk)
+  const int p_first = k_first * kPT;
+  const int p_end = min(n, (k_last + 1) * kPT);
+  for (int i = threadIdx.x; i < (k_last - k_first + 1) * (kPT / 2); i += blockDim.x) {
+    const int p = p_first + 2 * i;
+    const float2 p0 = p < p_end ? xy32[b + p] : make_float2(0.f, kPadY);
+    const float2 p1 = p + 1 < p_end ? xy32[b + p + 1] : make_float2(0.f, kPadY);
+    pts[i] = make_float4(p0.x, p0.y, p1.x, p1.y);
+  }
+  const long long task = task0 + threadIdx.x;
+  const bool valid = task < tasks;
+  const int g = valid ? static_cast<int>(task % G) : 0;
+  const int k = valid ? static_cast<int>(task / G) : k_first;
+  const int t0 = g * kNH;
+  float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
+  const float4* hp = hyp + static_cast<int64_t>(c) * T;
+#pragma unroll
+  for (int q = 0; q < kNH; ++q) {
+    float4 h = make_float4(0.f, 0.f, 0.f, 1.f);  // inert: e^2 + 1 > 0
+    if (valid && t0 + q < T) h = hp[t0 + q];
     if (q & 1) {
-      A[pr].y = f.A; B[pr].y = f.B; Cc[pr].y = f.C; T2[pr].y = -f.t2hi;
+      A[q >> 1].y = h.x; B[q >> 1].y = h.y; Cc[q >> 1].y = h.z; T2[q >> 1].y = h.w;
     } else {
-      A[pr].x = f.A; B[pr].x = f.B; Cc[pr].x = f.C; T2[pr].x = -f.t2hi;
+      A[q >> 1].x = h.x; B[q >> 1].x = h.y; Cc[q >> 1].x = h.z; T2[q >> 1].x = h.w;
     }
   }
-
-  uint32_t cnt[kHypPerThread] = {0, 0, 0, 0};
-  const float4* src = reinterpret_cast<const float4*>(xy32 + b);
-  const bool aligned = (b & 1) == 0;
-  for (int c0 = 0; c0 < n; c0 += kChunk) {
-    const int m = min(kChunk, n - c0);
-    const int m2 = (m + 1) >> 1;
-    __syncthreads();
-    if (aligned && (c0 & 1) == 0) {
-      for (int i = threadIdx.x; i < m2; i += blockDim.x) {
-        float4 v = (2 * i + 1 < m) ? src[(c0 >> 1) + i]
-                                   : make_float4(xy32[b + c0 + 2 * i].x,
-                                                 xy32[b + c0 + 2 * i].y, 0.f, kPadY);
-        pts[i] = v;
-      }
-    } else {
-      for (int i = threadIdx.x; i < m2; i += blockDim.x) {
-        const float2 p0 = xy32[b + c0 + 2 * i];
-        const float2 p1 = (2 * i + 1 < m) ? xy32[b + c0 + 2 * i + 1] : make_float2(0.f, kPadY);
-        pts[i] = make_float4(p0.x, p0.y, p1.x, p1.y);
-      }
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int i = 0; i < m2; ++i) {
-      const float4 v = pts[i];
-      const float2 x0 = make_float2(v.x, v.x), y0 = make_float2(v.y, v.y);
-      const float2 x1 = make_float2(v.z, v.z), y1 = make_float2(v.w, v.w);
+  __syncthreads();
+  uint32_t cnt[kNH];
 #pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {
-        float2 e = __ffma2_rn(A[pr], x0, __ffma2_rn(B[pr], y0, Cc[pr]));
-        float2 g = __ffma2_rn(e, e, T2[pr]);
-        cnt[2 * pr] += __float_as_uint(g.x) >> 31;
-        cnt[2 * pr + 1] += __float_as_uint(g.y) >> 31;
-        e = __ffma2_rn(A[pr], x1, __ffma2_rn(B[pr], y1, Cc[pr]));
-        g = __ffma2_rn(e, e, T2[pr]);
-        cnt[2 * pr] += __float_as_uint(g.x) >> 31;
-        cnt[2 * pr + 1] += __float_as_uint(g.y) >> 31;
-      }
+  for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+  const float4* cp = pts + (k - k_first) * (kPT / 2);
+  const int m2 = (min(kPT, n - k * kPT) + 1) >> 1;
+#pragma unroll 2
+  for (int i = 0; i < m2; ++i) {
+    const float4 v = cp[i];
+#pragma unroll
+    for (int pr = 0; pr < kNH / 2; ++pr) {
+      float2 e = __ffma2_rn(A[pr], make_float2(v.x, v.x),
+                            __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
+      float2 gg = __ffma2_rn(e, e, T2[pr]);
+      cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
+      cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
+      e = __ffma2_rn(A[pr], make_float2(v.z, v.z),
+                     __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
+      gg = __ffma2_rn(e, e, T2[pr]);
+      cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
+      cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
     }
   }
+  if (!valid) return;
+  int32_t* up = upper + static_cast<int64_t>(c) * T + t0;
 #pragma unroll
-  for (int q = 0; q < kHypPerThread; ++q) {
-    const int t = tb * kHypPerTile + q * kScoreThreads + threadIdx.x;
-    if (t < T) upper[static_cast<int64_t>(c) * T + t] = static_cast<int32_t>(cnt[q]);
-  }
+  for (int q = 0; q < kNH; ++q)
+    if (t0 + q < T && cnt[q]) atomicAdd(&up[q], static_cast<int32_t>(cnt[q]));
 }
 
 // ----------------------------------------------------------- select kernel
@@ -681,13 +804,27 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
   count_launch();
 }
 
+void launch_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                 cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  const int T = p.max_trials;
+  const int64_t total = static_cast<int64_t>(f.n_clusters) * T;
+  hyp_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+      f.n_clusters, f.offsets, s.xy64, s.stat, f.keys, T, p.rng_seed, s.hyp, s.upper);
+  count_launch();
+  tile_plan_kernel<<<1, 1024, 0, st>>>(f.n_clusters, f.offsets, T, s.tile_start);
+  count_launch();
+}
+
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const int tpc = (p.max_trials + kHypPerTile - 1) / kHypPerTile;
-  const int64_t grid = static_cast<int64_t>(f.n_clusters) * tpc;
-  score_kernel<<<static_cast<unsigned>(grid), kScoreThreads, 0, st>>>(
-      f.offsets, s.xy64, s.xy32, s.stat, f.keys, f.order, p.max_trials, tpc, p.rng_seed, s.upper);
+  const int T = p.max_trials;
+  // grid bound: sum_c ceil(G * nch_c / 128) <= G * (P / kPT + C) / 128 + C
+  const int64_t G = std::max<int64_t>((T + kNH - 1) / kNH, kNH);
+  const int64_t bound = (G * (f.n_points / kPT + f.n_clusters)) / kScoreThreads + f.n_clusters + 1;
+  score_kernel<<<static_cast<unsigned>(bound), kScoreThreads, 0, st>>>(
+      f.n_clusters, f.offsets, s.xy32, s.hyp, s.tile_start, T, s.upper);
   count_launch();
 }
 

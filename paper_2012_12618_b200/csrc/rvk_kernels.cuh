@@ -29,6 +29,8 @@ struct Scratch {
   double4* stat = nullptr;   // [C] (thr_lo, thr_hi, median, thr_exact|NaN)
   double* norm = nullptr;    // [4C] (offset_az, offset_dop, scale_az, scale_dop)
   int32_t* upper = nullptr;  // [C*T] fast-pass upper-bound counts
+  float4* hyp = nullptr;     // [C*T] (A, B, C, -t2hi) per hypothesis
+  int32_t* tile_start = nullptr;  // [C+1] scoring tile plan
 };
 
 struct Outputs {
@@ -45,6 +47,9 @@ void launch_prep(const FrameDev& f, double threshold_scale, const Scratch& s, cu
 // Exact (left-to-right) MAD threshold into stat[c].w (and .x = .y).
 void launch_mad_exact(const FrameDev& f, double threshold_scale, const Scratch& s,
                       cudaStream_t st);
+// Hypothesis setup (seed pairs, FP64 lines, FP32 coefficients) + tile plan.
+void launch_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                 cudaStream_t st);
 // Fast FP32 scoring: upper-bound inlier counts for every (cluster, trial).
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);

@@ -42,6 +42,15 @@ __device__ __forceinline__ float u01(uint32_t x) { return (hsh(x) >> 8) * (1.0f 
 //    3 = FFMA2 affine + integer compare on |e| bits (LEA) + LEA.HI
 //    4 = FFMA2 affine + FSETP/compare-add (compiler's choice)
 //    5 = FFMA2 affine; pair 0 FP compare, pair 1 integer compare (mixed)
+//    6 = FFMA2 affine + FSET (|e| < t -> 0/-1) + IADD3 counting two at a time
+//    7 = FFMA2 affine + FFMA2 compare, last pair integer compare (f = 1/NP)
+//    8 = FFMA2 affine + FSET/IADD3, last pair integer compare
+__device__ __forceinline__ uint32_t fset_lt(float a, float b) {
+  uint32_t r;
+  asm("set.lt.u32.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 template <int V, int NH>
 __global__ void __launch_bounds__(kThreads) score_mb(int n, int reps, uint32_t* out) {
   __shared__ float4 pts[kPts / 2];
@@ -51,6 +60,7 @@ __global__ void __launch_bounds__(kThreads) score_mb(int n, int reps, uint32_t* 
   }
   constexpr int NP = NH / 2;
   float2 A[NP], B[NP], Cc[NP], T2[NP];
+  float Tl[NP];
   uint32_t K[NH];
 #pragma unroll
   for (int q = 0; q < NP; ++q) {
@@ -60,6 +70,7 @@ __global__ void __launch_bounds__(kThreads) score_mb(int n, int reps, uint32_t* 
     Cc[q] = make_float2(-0.4f * u01(s + 4), -0.4f * u01(s + 5));
     const float t = 0.05f + 0.1f * u01(s + 6);
     T2[q] = make_float2(-t * t, -t * t);
+    Tl[q] = t;
     K[2 * q] = (__float_as_uint(t) << 1) + 1u;
     K[2 * q + 1] = K[2 * q];
   }
@@ -86,7 +97,17 @@ __global__ void __launch_bounds__(kThreads) score_mb(int n, int reps, uint32_t* 
             const float2 e = __ffma2_rn(A[q], make_float2(x, x),
                                         __ffma2_rn(B[q], make_float2(y, y), Cc[q]));
             const bool fp = (V == 0 || V == 1 || (V == 5 && (q & 1) == 0));
-            if (V == 0 || (V == 5 && fp)) {
+            const bool last = (q == NP - 1);
+            if (V == 6 || (V == 8 && !last)) {
+              cnt[2 * q] -= fset_lt(fabsf(e.x), Tl[q]) + fset_lt(fabsf(e.y), Tl[q]);
+            } else if (V == 7 && !last) {
+              const float2 g = __ffma2_rn(e, e, T2[q]);
+              cnt[2 * q] += __float_as_uint(g.x) >> 31;
+              cnt[2 * q + 1] += __float_as_uint(g.y) >> 31;
+            } else if ((V == 7 || V == 8) && last) {
+              cnt[2 * q] += ((__float_as_uint(e.x) << 1) - K[2 * q]) >> 31;
+              cnt[2 * q + 1] += ((__float_as_uint(e.y) << 1) - K[2 * q + 1]) >> 31;
+            } else if (V == 0 || (V == 5 && fp)) {
               const float2 g = __ffma2_rn(e, e, T2[q]);
               cnt[2 * q] += __float_as_uint(g.x) >> 31;
               cnt[2 * q + 1] += __float_as_uint(g.y) >> 31;
@@ -203,7 +224,18 @@ int main() {
   const double alu = double(pb) * 256 * iters * 16 / (ms_a * 1e-3);
   printf("{\"sms\": %d, \"ffma_imm_tflops\": %.2f, \"ffma_3reg_tflops\": %.2f, "
          "\"alu_xor_shr_add_gops\": %.1f}\n", sms, peak / 1e12, peak3 / 1e12, alu / 1e9);
-  for (int waves : {4, 8}) {
+  for (int waves : {6}) {
+    const int blocks = sms * waves;
+    run<0, 8>("ffma2_all", blocks, peak, d_u);
+    run<0, 16>("ffma2_all", blocks, peak, d_u);
+    run<6, 8>("ffma2_aff_fset_iadd3", blocks, peak, d_u);
+    run<6, 16>("ffma2_aff_fset_iadd3", blocks, peak, d_u);
+    run<7, 8>("ffma2_cmp_last_int", blocks, peak, d_u);
+    run<7, 16>("ffma2_cmp_last_int", blocks, peak, d_u);
+    run<8, 8>("fset_last_int", blocks, peak, d_u);
+    run<8, 16>("fset_last_int", blocks, peak, d_u);
+  }
+  for (int waves : {4}) {
     const int blocks = sms * waves;
     run<0, 4>("ffma2_all", blocks, peak, d_u);
     run<0, 8>("ffma2_all", blocks, peak, d_u);
