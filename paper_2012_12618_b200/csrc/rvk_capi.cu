@@ -14,6 +14,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rvk_gpu.h"
@@ -86,13 +87,21 @@ struct HostBuf {
   }
 };
 
+// Device scratch of one stream's in-flight pipeline.
+struct Workspace {
+  DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, aux;
+};
+
 struct Context {
   int device = -1;
   cudaStream_t stream = nullptr;
   DevBuf in;       // offsets | az | dop | ids | keys | order (one H2D)
   DevBuf out;      // count | trial | est | mask (one D2H)
-  DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, aux;
   HostBuf stage_in, stage_out;
+  // Scratch per stream, so calls on different streams (device API) may be
+  // in flight concurrently; the host API uses `stream`.
+  std::unordered_map<cudaStream_t, Workspace> ws;
+  Workspace& workspace(cudaStream_t s) { return ws[s]; }
 };
 
 Context& context() {
@@ -203,15 +212,15 @@ FrameDev stage_frame(Context& ctx, int64_t frame_id, int32_t n_clusters, const i
   return f;
 }
 
-Scratch scratch(Context& ctx, int32_t n_clusters, int64_t P, int32_t T) {
+Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   Scratch s;
-  s.xy64 = ctx.xy64.get<double2>(P);
-  s.xy32 = ctx.xy32.get<float2>(P + 2);
-  s.stat = ctx.thr.get<double4>(n_clusters);
-  s.norm = ctx.norm.get<double>(4 * static_cast<size_t>(n_clusters));
-  s.upper = ctx.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
-  s.hyp = ctx.hyp.get<float4>(static_cast<size_t>(n_clusters) * std::max(T, 1));
-  s.tile_start = ctx.tiles.get<int32_t>(static_cast<size_t>(n_clusters) + 1);
+  s.xy64 = w.xy64.get<double2>(P);
+  s.xy32 = w.xy32.get<float2>(P + 2);
+  s.stat = w.thr.get<double4>(n_clusters);
+  s.norm = w.norm.get<double>(4 * static_cast<size_t>(n_clusters));
+  s.upper = w.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
+  s.hyp = w.hyp.get<float4>(static_cast<size_t>(n_clusters) * std::max(T, 1));
+  s.tile_start = w.tiles.get<int32_t>(static_cast<size_t>(n_clusters) + 1);
   return s;
 }
 
@@ -290,7 +299,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   const int64_t P = offsets[n_clusters];
   FrameDev f = stage_frame(ctx, frame_id, n_clusters, offsets, az, dop, ids, keys, true, nullptr,
                            nullptr);
-  Scratch s = scratch(ctx, n_clusters, P, params->max_trials);
+  Scratch s = scratch(ctx.workspace(ctx.stream), n_clusters, P, params->max_trials);
   const OutLayout L(n_clusters, P);
   char* dout = ctx.out.get<char>(L.total);
   Outputs o;
@@ -400,7 +409,7 @@ int rvk_ransac_estimate_device(int64_t frame_id, int32_t n_clusters, int64_t n_p
     f.keys = d_rng_cluster_index;
     f.order = nullptr;
     f.frame_id = frame_id;
-    Scratch sc = scratch(ctx, n_clusters, n_points, params->max_trials);
+    Scratch sc = scratch(ctx.workspace(s), n_clusters, n_points, params->max_trials);
     Outputs o;
     o.inlier_count = d_inlier_count;
     o.winning_trial = d_winning_trial;
@@ -424,9 +433,9 @@ int rvk_trial_counts(int32_t n_clusters, const int64_t* offsets, const double* a
     const int64_t P = offsets[n_clusters];
     FrameDev f = stage_frame(ctx, 0, n_clusters, offsets, azimuth, doppler, nullptr,
                              rng_cluster_index, false, nullptr, nullptr);
-    Scratch s = scratch(ctx, n_clusters, P, params->max_trials);
+    Scratch s = scratch(ctx.workspace(ctx.stream), n_clusters, P, params->max_trials);
     const size_t nc = static_cast<size_t>(n_clusters) * params->max_trials;
-    int32_t* d_counts = ctx.aux.get<int32_t>(nc);
+    int32_t* d_counts = ctx.workspace(ctx.stream).aux.get<int32_t>(nc);
     launch_prep(f, params->threshold_scale, s, ctx.stream);
     launch_mad_exact(f, params->threshold_scale, s, ctx.stream);
     launch_exact_counts(f, *params, s, d_counts, ctx.stream);
@@ -464,7 +473,7 @@ int rvk_seed_pairs(int32_t n_clusters, const int64_t* offsets, const rvk_ransac_
     f.n_clusters = n_clusters;
     f.offsets = reinterpret_cast<const int64_t*>(d);
     f.keys = rng_cluster_index ? reinterpret_cast<const int32_t*>(d + o_keys) : nullptr;
-    int32_t* d_pairs = ctx.aux.get<int32_t>(2 * nc);
+    int32_t* d_pairs = ctx.workspace(ctx.stream).aux.get<int32_t>(2 * nc);
     launch_seed_pairs(f, *params, d_pairs, ctx.stream);
     check_launch();
     void* ho = ctx.stage_out.get(sizeof(int32_t) * 2 * nc);
@@ -490,7 +499,7 @@ int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const dou
     const int64_t P = offsets[n_clusters];
     FrameDev f = stage_frame(ctx, 0, n_clusters, offsets, azimuth, doppler, nullptr, nullptr,
                              false, nullptr, nullptr);
-    Scratch s = scratch(ctx, n_clusters, P, 1);
+    Scratch s = scratch(ctx.workspace(ctx.stream), n_clusters, P, 1);
     launch_prep(f, threshold_scale, s, ctx.stream);
     launch_mad_exact(f, threshold_scale, s, ctx.stream);
     check_launch();

@@ -90,17 +90,15 @@ struct FastHyp {
   float t2lo;  // e^2 < t2lo: certain inlier
 };
 
-__device__ __forceinline__ FastHyp make_fast(const Line& L, double thr_lo, double thr_hi) {
+// Coefficients from (m, c) and r ~= 1/den. r may carry a few FP64 ulps of
+// error (rsqrt in the setup kernel): that perturbs A, B, C by ~1e-16
+// relative, far inside the band's factor-2 margin.
+__device__ __forceinline__ FastHyp fast_coeffs(double m, double c, double r, double thr_lo,
+                                               double thr_hi) {
   FastHyp h;
-  if (L.degenerate) {  // scores 0 (src/ransac.cpp:185-187): nothing passes
-    h.A = h.B = h.C = 0.f;
-    h.t2hi = -1.f;
-    h.t2lo = -1.f;
-    return h;
-  }
-  const double A = __ddiv_rn(-L.m, L.den);
-  const double B = __ddiv_rn(1.0, L.den);
-  const double C = __ddiv_rn(-L.c, L.den);
+  const double A = -m * r;
+  const double B = r;
+  const double C = -c * r;
   const double S = fabs(A) + fabs(B) + fabs(C);
   const double band = S * 0x1p-21;
   h.A = __double2float_rn(A);
@@ -115,6 +113,31 @@ __device__ __forceinline__ FastHyp make_fast(const Line& L, double thr_lo, doubl
     h.t2lo = 0.f;  // e^2 < 0 never holds: no certain inliers
   }
   return h;
+}
+
+__device__ __forceinline__ FastHyp inert_fast() {
+  FastHyp h;  // degenerate seeds score 0 (src/ransac.cpp:185-187): nothing passes
+  h.A = h.B = h.C = 0.f;
+  h.t2hi = -1.f;
+  h.t2lo = -1.f;
+  return h;
+}
+
+__device__ __forceinline__ FastHyp make_fast(const Line& L, double thr_lo, double thr_hi) {
+  if (L.degenerate) return inert_fast();
+  return fast_coeffs(L.m, L.c, __ddiv_rn(1.0, L.den), thr_lo, thr_hi);
+}
+
+// Fast-pass hypothesis straight from the seeds: the exact FP64 slope and
+// intercept (same operations as make_line) but 1/den by rsqrt instead of a
+// correctly rounded sqrt + divide; used where only the FP32 filter is needed.
+__device__ __forceinline__ FastHyp make_fast_from_seeds(double x1, double y1, double x2,
+                                                        double y2, double thr_lo, double thr_hi) {
+  const double dx = __dsub_rn(x2, x1);
+  if (fabs(dx) < kSeedEpsilon) return inert_fast();
+  const double m = __ddiv_rn(__dsub_rn(y2, y1), dx);
+  const double c = __dsub_rn(y1, __dmul_rn(m, x1));
+  return fast_coeffs(m, c, rsqrt(__dadd_rn(__dmul_rn(m, m), 1.0)), thr_lo, thr_hi);
 }
 
 // Full per-hypothesis state for the exact (verification / mask) passes.

@@ -104,7 +104,8 @@ __device__ double block_select_y(const double2* xy, int n, int k,
     __syncthreads();
     const unsigned long long hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const unsigned long long key = __double_as_longlong(xy[i].y);
+      const unsigned long long key =
+          static_cast<unsigned long long>(__double_as_longlong(xy[i].y)) & ~(1ull << 63);
       if (((key ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
@@ -214,6 +215,15 @@ __device__ unsigned long long block_radix_select(const unsigned long long* keys,
   return prefix;
 }
 
+__device__ double first_zero(double v, const double* __restrict__ a, int n, double* red) {
+  if (v != 0.0) return v;
+  int first = INT_MAX;
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    if (a[k] == 0.0) first = k < first ? k : first;
+  first = block_reduce(first, MinI(), reinterpret_cast<int*>(red));
+  return a[first];
+}
+
 // Per cluster (one CTA): normalize_cluster (src/ransac.cpp:214-232), the
 // median of the normalized dopplers (ransac.hpp:53-70, exact: bitonic sort in
 // shared memory, or radix select over global memory for huge clusters), and
@@ -253,10 +263,38 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     lo1 = d < lo1 ? d : lo1;
     hi1 = d > hi1 ? d : hi1;
   }
-  lo0 = block_reduce(lo0, MinOp(), red);
-  hi0 = block_reduce(hi0, MaxOp(), red);
-  lo1 = block_reduce(lo1, MinOp(), red);
-  hi1 = block_reduce(hi1, MaxOp(), red);
+  {  // one fused block reduction of (min az, -max az, min dop, -max dop)
+    double4 v = make_double4(lo0, -hi0, lo1, -hi1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v.x = fmin(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+      v.y = fmin(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+      v.z = fmin(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
+      v.w = fmin(v.w, __shfl_xor_sync(0xffffffffu, v.w, o));
+    }
+    __shared__ double4 red4[32];
+    if ((threadIdx.x & 31) == 0) red4[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = red4[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      const double4 u = red4[w];
+      v.x = fmin(v.x, u.x);
+      v.y = fmin(v.y, u.y);
+      v.z = fmin(v.z, u.z);
+      v.w = fmin(v.w, u.w);
+    }
+    lo0 = v.x;
+    hi0 = -v.y;
+    lo1 = v.z;
+    hi1 = -v.w;
+  }
+  // Eigen's minCoeff/maxCoeff keep the FIRST extreme in index order; values
+  // that compare equal differ in bits only for +-0, so an extreme equal to
+  // zero takes the bits of its first occurrence (block-uniform branch).
+  lo0 = first_zero(lo0, az + b, n, red);
+  hi0 = first_zero(hi0, az + b, n, red);
+  lo1 = first_zero(lo1, dop + b, n, red);
+  hi1 = first_zero(hi1, dop + b, n, red);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   const bool in_smem = n <= kSortCap;
@@ -265,7 +303,9 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
     xy32[b + k] = make_float2(__double2float_rn(x), __double2float_rn(y));
-    if (in_smem) sy[k] = static_cast<unsigned long long>(__double_as_longlong(y));
+    // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
+    // std::sort's operator< treats them; every other value is >= +0)
+    if (in_smem) sy[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
   }
   if (threadIdx.x == 0 && norm != nullptr) {
     norm[4 * c + 0] = lo0;
@@ -361,7 +401,11 @@ __global__ void hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offse
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double4 st = stat[c];
-  const FastHyp f = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, st.x, st.y).f;
+  int i, j;
+  seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+  const double2 p = xy64[b + i];
+  const double2 q = xy64[b + j];
+  const FastHyp f = make_fast_from_seeds(p.x, p.y, q.x, q.y, st.x, st.y);
   hyp[idx] = make_float4(f.A, f.B, f.C, -f.t2hi);
   upper[idx] = 0;
 }
