@@ -392,7 +392,7 @@ def main():
     f_off, f_az, f_dop, f_keys = batch(frames[:1])
     one = {"offsets": torch.from_numpy(f_off).to(dev), "az": torch.from_numpy(f_az).to(dev),
            "dop": torch.from_numpy(f_dop).to(dev), "keys": torch.from_numpy(f_keys).to(dev)}
-    lat = []
+    frame_lat = []
     for j in range(33):
         a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -404,7 +404,7 @@ def main():
         b_.record(stream)
         b_.synchronize()
         if j >= 3:
-            lat.append(a.elapsed_time(b_))
+            frame_lat.append(a.elapsed_time(b_))
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
@@ -489,7 +489,7 @@ def main():
         h2d = (C_ + 1) * 8 + 2 * P_ * 8 + 2 * C_ * 4  # offsets, az, dop, keys, LPT order
         d2h = C_ * 4 * 2 + C_ * 48 + P_               # counts, trials, estimates, mask
         e2e = {"value": e2e_evals / e2e_t * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "p50_frame_latency_ms": statistics.median(lat),
+               "d2h_bytes_per_step": d2h, "p50_step_latency_ms": statistics.median(lat),
                "api": "rvk_ransac_estimate (host buffers, pinned)",
                "note": "rank-0 e2e rate x n_gpus" if world > 1 else "single rank"}
 
@@ -510,7 +510,7 @@ def main():
             "config": cfg,
             "clusters_per_sec": clusters_all / elapsed,
             "p50_step_latency_ms": statistics.median(per_step),
-            "p50_frame_latency_ms": statistics.median(lat),
+            "p50_frame_latency_ms": statistics.median(frame_lat),
             "p50_frame_latency_note": "one frame per call, device-resident inputs, CUDA events",
             "streams": S,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

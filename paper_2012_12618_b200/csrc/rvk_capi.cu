@@ -102,6 +102,15 @@ struct Context {
   // in flight concurrently; the host API uses `stream`.
   std::unordered_map<cudaStream_t, Workspace> ws;
   Workspace& workspace(cudaStream_t s) { return ws[s]; }
+  // two internal streams for the chunked host pipeline
+  cudaStream_t pipe[2] = {nullptr, nullptr};
+  cudaEvent_t pipe_ev[1] = {nullptr};
+  void ensure_pipe() {
+    if (pipe[0]) return;
+    RVK_CUDA(cudaStreamCreateWithFlags(&pipe[0], cudaStreamNonBlocking));
+    RVK_CUDA(cudaStreamCreateWithFlags(&pipe[1], cudaStreamNonBlocking));
+    RVK_CUDA(cudaEventCreateWithFlags(&pipe_ev[0], cudaEventDisableTiming));
+  }
 };
 
 Context& context() {
@@ -283,6 +292,26 @@ void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   check_launch();
 }
 
+bool is_pinned(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();  // clear: pageable pointers may report an error on old drivers
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host API: the frame is split into up to kPipeMax cluster-aligned chunks of
+// >= kPipeChunk points; chunk i runs H2D -> prep -> hyps -> score -> select
+// -> D2H on internal stream i % 2, so the copies of one chunk overlap the
+// kernels of the other. Pinned caller buffers are copied directly (no host
+// staging memcpy); pageable ones go through the context's pinned staging.
+// RNG keys stay frame-positional, so the result does not depend on the
+// chunking.
+constexpr int64_t kPipeChunk = 1 << 17;
+constexpr int kPipeMax = 8;
+
 int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
                          const double* az, const double* dop, const int32_t* ids,
                          const rvk_ransac_params* params, const int32_t* keys,
@@ -296,25 +325,99 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   if ((az == nullptr || dop == nullptr) && offsets[n_clusters] > 0)
     return fail(RVK_EINVAL, "run_ransac: null point arrays");
   Context& ctx = context();
+  ctx.ensure_pipe();
   const int64_t P = offsets[n_clusters];
-  FrameDev f = stage_frame(ctx, frame_id, n_clusters, offsets, az, dop, ids, keys, true, nullptr,
-                           nullptr);
-  Scratch s = scratch(ctx.workspace(ctx.stream), n_clusters, P, params->max_trials);
+
+  // chunk boundaries (cluster-aligned)
+  int K = static_cast<int>(std::min<int64_t>(kPipeMax, std::max<int64_t>(1, P / kPipeChunk)));
+  std::vector<int32_t> cut(1, 0);
+  for (int i = 1; i < K; ++i) {
+    const int64_t target = P * i / K;
+    int32_t c = cut.back();
+    while (c < n_clusters && offsets[c] < target) ++c;
+    if (c > cut.back() && c < n_clusters) cut.push_back(c);
+  }
+  cut.push_back(n_clusters);
+  K = static_cast<int>(cut.size()) - 1;
+
+  const bool pin_in = is_pinned(az) && is_pinned(dop);
+  const bool pin_mask = is_pinned(mask);
+
+  // device input block: [offsets (rebased per chunk) | keys | ids] + az | dop
+  const size_t o_keys = align_up(sizeof(int64_t) * (n_clusters + K));
+  const size_t o_ids = align_up(o_keys + sizeof(int32_t) * n_clusters);
+  const size_t o_az = align_up(o_ids + sizeof(int32_t) * n_clusters);
+  const size_t o_dop = align_up(o_az + sizeof(double) * P);
+  const size_t in_total = align_up(o_dop + sizeof(double) * P);
+  const size_t small = o_az;
+  char* h = static_cast<char*>(ctx.stage_in.get(pin_in ? small : in_total));
+  char* d = ctx.in.get<char>(in_total);
+  int64_t* h_off = reinterpret_cast<int64_t*>(h);
+  int32_t* h_keys = reinterpret_cast<int32_t*>(h + o_keys);
+  int32_t* h_ids = reinterpret_cast<int32_t*>(h + o_ids);
+  for (int i = 0; i < K; ++i)  // chunk i's offsets start at slot cut[i] + i
+    for (int32_t c = cut[i]; c <= cut[i + 1]; ++c) h_off[c + i] = offsets[c] - offsets[cut[i]];
+  for (int32_t c = 0; c < n_clusters; ++c) h_keys[c] = keys ? keys[c] : c;
+  if (ids) std::memcpy(h_ids, ids, sizeof(int32_t) * n_clusters);
+  if (!pin_in) {
+    std::memcpy(h + o_az, az, sizeof(double) * P);
+    std::memcpy(h + o_dop, dop, sizeof(double) * P);
+  }
+  const double* src_az = pin_in ? az : reinterpret_cast<const double*>(h + o_az);
+  const double* src_dop = pin_in ? dop : reinterpret_cast<const double*>(h + o_dop);
+
   const OutLayout L(n_clusters, P);
   char* dout = ctx.out.get<char>(L.total);
-  Outputs o;
-  o.inlier_count = reinterpret_cast<int32_t*>(dout + L.o_cnt);
-  o.winning_trial = reinterpret_cast<int32_t*>(dout + L.o_tr);
-  o.est = refit ? reinterpret_cast<rvk_estimate*>(dout + L.o_est) : nullptr;
-  o.mask = reinterpret_cast<uint8_t*>(dout + L.o_mask);
-  run_pipeline(f, *params, s, o, ctx.stream);
-  char* h = static_cast<char*>(ctx.stage_out.get(L.total));
-  RVK_CUDA(cudaMemcpyAsync(h, dout, L.total, cudaMemcpyDeviceToHost, ctx.stream));
-  RVK_CUDA(cudaStreamSynchronize(ctx.stream));
-  if (inlier_count) std::memcpy(inlier_count, h + L.o_cnt, sizeof(int32_t) * n_clusters);
-  if (winning_trial) std::memcpy(winning_trial, h + L.o_tr, sizeof(int32_t) * n_clusters);
-  if (mask) std::memcpy(mask, h + L.o_mask, P);
-  if (out && refit) std::memcpy(out, h + L.o_est, sizeof(rvk_estimate) * n_clusters);
+  char* hout = static_cast<char*>(ctx.stage_out.get(L.total));
+  cudaStream_t s0 = ctx.pipe[0];
+  RVK_CUDA(cudaMemcpyAsync(d, h, small, cudaMemcpyHostToDevice, s0));  // small arrays, once
+  RVK_CUDA(cudaEventRecord(ctx.pipe_ev[0], s0));
+  RVK_CUDA(cudaStreamWaitEvent(ctx.pipe[1], ctx.pipe_ev[0], 0));
+  for (int i = 0; i < K; ++i) {
+    cudaStream_t sc = ctx.pipe[i & 1];
+    const int32_t c0 = cut[i], nc = cut[i + 1] - cut[i];
+    const int64_t p0 = offsets[c0], np = offsets[cut[i + 1]] - p0;
+    char* daz = d + o_az + sizeof(double) * p0;
+    char* ddop = d + o_dop + sizeof(double) * p0;
+    RVK_CUDA(cudaMemcpyAsync(daz, src_az + p0, sizeof(double) * np, cudaMemcpyHostToDevice, sc));
+    RVK_CUDA(cudaMemcpyAsync(ddop, src_dop + p0, sizeof(double) * np, cudaMemcpyHostToDevice, sc));
+    FrameDev f;
+    f.n_clusters = nc;
+    f.n_points = np;
+    f.offsets = reinterpret_cast<const int64_t*>(d) + c0 + i;
+    f.azimuth = reinterpret_cast<const double*>(daz);
+    f.doppler = reinterpret_cast<const double*>(ddop);
+    f.keys = reinterpret_cast<const int32_t*>(d + o_keys) + c0;
+    f.cluster_ids = ids ? reinterpret_cast<const int32_t*>(d + o_ids) + c0 : nullptr;
+    f.frame_id = frame_id;
+    Scratch s = scratch(ctx.workspace(sc), nc, np, params->max_trials);
+    Outputs o;
+    o.inlier_count = reinterpret_cast<int32_t*>(dout + L.o_cnt) + c0;
+    o.winning_trial = reinterpret_cast<int32_t*>(dout + L.o_tr) + c0;
+    o.est = refit ? reinterpret_cast<rvk_estimate*>(dout + L.o_est) + c0 : nullptr;
+    o.mask = reinterpret_cast<uint8_t*>(dout + L.o_mask) + p0;
+    run_pipeline(f, *params, s, o, sc);
+    // per-chunk results back
+    if (mask) {
+      uint8_t* dst = pin_mask ? mask + p0 : reinterpret_cast<uint8_t*>(hout + L.o_mask) + p0;
+      RVK_CUDA(cudaMemcpyAsync(dst, o.mask, np, cudaMemcpyDeviceToHost, sc));
+    }
+    if (inlier_count)
+      RVK_CUDA(cudaMemcpyAsync(reinterpret_cast<int32_t*>(hout + L.o_cnt) + c0, o.inlier_count,
+                               sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, sc));
+    if (winning_trial)
+      RVK_CUDA(cudaMemcpyAsync(reinterpret_cast<int32_t*>(hout + L.o_tr) + c0, o.winning_trial,
+                               sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, sc));
+    if (out && refit)
+      RVK_CUDA(cudaMemcpyAsync(reinterpret_cast<rvk_estimate*>(hout + L.o_est) + c0, o.est,
+                               sizeof(rvk_estimate) * nc, cudaMemcpyDeviceToHost, sc));
+  }
+  RVK_CUDA(cudaStreamSynchronize(ctx.pipe[0]));
+  RVK_CUDA(cudaStreamSynchronize(ctx.pipe[1]));
+  if (inlier_count) std::memcpy(inlier_count, hout + L.o_cnt, sizeof(int32_t) * n_clusters);
+  if (winning_trial) std::memcpy(winning_trial, hout + L.o_tr, sizeof(int32_t) * n_clusters);
+  if (mask && !pin_mask) std::memcpy(mask, hout + L.o_mask, P);
+  if (out && refit) std::memcpy(out, hout + L.o_est, sizeof(rvk_estimate) * n_clusters);
   return RVK_OK;
 }
 
