@@ -8,18 +8,18 @@
  * /root/reference/proj) with plain pointers and sizes:
  *
  *   rvk_run_ransac     <- rvk::run_ransac      include/rvk/ransac.hpp:128-129
- *                                               (impl src/ransac.cpp:283-344)
+ *                                               (impl src/ransac.cpp:138-199)
  *   rvk_estimate_all   <- rvk::estimate_all    include/rvk/velocity.hpp:123-125
- *                                               (impl src/velocity.cpp:219-248)
+ *                                               (impl src/velocity.cpp:92-121)
  *   rvk_ransac_estimate   run_ransac followed by estimate_all on the same
  *                         clusters (the pipeline of tools/rvk_main.cpp:134-144
- *                         and src/bench.cpp:615-627), masks never leave HBM.
+ *                         and src/bench.cpp:132-143), masks never leave HBM.
  *   rvk_trial_counts   <- per-(cluster, trial) count_trial_inliers
- *                         (src/ransac.cpp:270-272) as scored inside run_ransac
- *                         (src/ransac.cpp:309-319); exact for every trial.
- *   rvk_seed_pairs     <- rvk::draw_seed_pair  src/ransac.cpp:256-268
+ *                         (src/ransac.cpp:125-127) as scored inside run_ransac
+ *                         (src/ransac.cpp:164-174); exact for every trial.
+ *   rvk_seed_pairs     <- rvk::draw_seed_pair  src/ransac.cpp:111-123
  *   rvk_cluster_thresholds <- normalize_cluster + mad_threshold
- *                         (src/ransac.cpp:214-239, ransac.hpp:53-84)
+ *                         (src/ransac.cpp:69-94, ransac.hpp:53-84)
  *
  * The C++ layer paper_2012_12618_b200/csrc/rvk_dropin.cpp re-exports the
  * reference's own C++ signatures on top of these, so unchanged callers link
@@ -30,7 +30,7 @@
  *                            points [offsets[c], offsets[c+1]).
  *   azimuth[P], doppler[P]   float64, P = offsets[n_clusters]; the points of
  *                            each cluster in the order gather_cluster_points
- *                            produces (src/ransac.cpp:346-360): this is exactly
+ *                            produces (src/ransac.cpp:201-215): this is exactly
  *                            Eigen::ArrayX2d's column-major [az(n) | dop(n)]
  *                            split into two SoA arrays.
  *   mask[P]                  uint8 0/1, aligned with the points (InlierMask::mask).
@@ -42,9 +42,9 @@
  * Errors: every entry point returns an rvk_status. The message is available
  * from rvk_last_error() (thread-local). Validation order and messages follow
  * the reference so the C++ layer can rethrow the same exception types:
- *   RVK_EINVAL              -> std::invalid_argument   (ransac.cpp:285-290,
- *                                                        velocity.cpp:222-224,231-233)
- *   RVK_ECLUSTER_TOO_SMALL  -> rvk::ClusterTooSmall     (ransac.cpp:295-299);
+ *   RVK_EINVAL              -> std::invalid_argument   (ransac.cpp:140-145,
+ *                                                        velocity.cpp:95-97,231-233)
+ *   RVK_ECLUSTER_TOO_SMALL  -> rvk::ClusterTooSmall     (ransac.cpp:150-154);
  *                              rvk_last_error_cluster() = offending cluster.
  *   RVK_ECUDA / RVK_ENOMEM  -> std::runtime_error (no CPU fallback exists).
  *
@@ -103,9 +103,9 @@ int32_t rvk_last_error_cluster(void);
 int64_t rvk_kernel_launches(void);
 void rvk_reset_kernel_launches(void);
 
-/* rvk::run_ransac (src/ransac.cpp:283-344).
+/* rvk::run_ransac (src/ransac.cpp:138-199).
  *   rng_cluster_index: optional [n_clusters] RNG key per cluster; NULL means
- *   the positional index c, as in the reference (ransac.cpp:314). Batched
+ *   the positional index c, as in the reference (ransac.cpp:169). Batched
  *   multi-frame calls pass the frame-local index.
  *   Outputs (caller-allocated): inlier_count[C], winning_trial[C], mask[P]. */
 int rvk_run_ransac(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
@@ -113,7 +113,7 @@ int rvk_run_ransac(int32_t n_clusters, const int64_t* offsets, const double* azi
                    const int32_t* rng_cluster_index, int32_t workers, int32_t* inlier_count,
                    int32_t* winning_trial, uint8_t* mask);
 
-/* rvk::estimate_all (src/velocity.cpp:219-248) over CSR-gathered clusters.
+/* rvk::estimate_all (src/velocity.cpp:92-121) over CSR-gathered clusters.
  *   cluster_ids[C] = Cluster::cluster_id (copied to the estimates). */
 int rvk_estimate_all(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
                      const double* azimuth, const double* doppler, const int32_t* cluster_ids,
@@ -137,13 +137,13 @@ int rvk_ransac_estimate_device(int64_t frame_id, int32_t n_clusters, int64_t n_p
                                rvk_estimate* d_out, void* stream);
 
 /* Exact per-(cluster, trial) inlier counts, counts[c * max_trials + t]
- * (the `counts` vector of src/ransac.cpp:308-319). */
+ * (the `counts` vector of src/ransac.cpp:163-174). */
 int rvk_trial_counts(int32_t n_clusters, const int64_t* offsets, const double* azimuth,
                      const double* doppler, const rvk_ransac_params* params,
                      const int32_t* rng_cluster_index, int32_t* counts);
 
 /* Seed pairs drawn on the device: pairs[2*(c*max_trials+t)+{0,1}] = (i, j)
- * of draw_seed_pair(seed, key_c, t, n_c) (src/ransac.cpp:256-268). */
+ * of draw_seed_pair(seed, key_c, t, n_c) (src/ransac.cpp:111-123). */
 int rvk_seed_pairs(int32_t n_clusters, const int64_t* offsets, const rvk_ransac_params* params,
                    const int32_t* rng_cluster_index, int32_t* pairs);
 

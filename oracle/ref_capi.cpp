@@ -9,12 +9,12 @@
 //
 // Every function here only converts CSR arrays <-> the reference's Eigen /
 // std::vector types and calls the reference:
-//   rvk::run_ransac         src/ransac.cpp:283-344
+//   rvk::run_ransac         src/ransac.cpp:138-199
 //   rvk::sequential_ransac  src/baseline.cpp:11-51
-//   rvk::estimate_all       src/velocity.cpp:219-248
+//   rvk::estimate_all       src/velocity.cpp:92-121
 //   rvk::sequential_lsq     src/baseline.cpp:53-79
 //   rvk::draw_seed_pair / normalize_cluster / mad_threshold /
-//   count_trial_inliers     src/ransac.cpp:214-272
+//   count_trial_inliers     src/ransac.cpp:69-127
 //   rvk::generate_frame     src/scene.cpp:105-189 (workload synthesis)
 #include <rvk/baseline.hpp>
 #include <rvk/ransac.hpp>
@@ -126,7 +126,7 @@ int guarded(F&& f) {
     return RVK_OK;
   } catch (const rvk::ClusterTooSmall& e) {
     g_error = e.what();
-    // "run_ransac: cluster <c> has ..." (src/ransac.cpp:296)
+    // "run_ransac: cluster <c> has ..." (src/ransac.cpp:151)
     const std::string s = e.what();
     const auto p = s.find("cluster ");
     if (p != std::string::npos) g_error_cluster = std::atoi(s.c_str() + p + 8);

@@ -70,7 +70,7 @@ uint64_t rvk_or_rng_u64(uint64_t seed, uint64_t hi, uint64_t lo, int32_t k) {
   return v;
 }
 
-/* ---- draw_seed_pair, src/ransac.cpp:256-268 ---- */
+/* ---- draw_seed_pair, src/ransac.cpp:111-123 ---- */
 int rvk_or_seed_pair(uint64_t seed, int32_t cluster, int32_t trial, int32_t n, int32_t* i,
                      int32_t* j) {
   if (n < 2) {
@@ -113,7 +113,7 @@ static double mean_abs_deviation(const double* v, int64_t n, int64_t stride) { /
   return acc / (double)n;
 }
 
-/* normalize_cluster (src/ransac.cpp:214-232) + mad_threshold (:234-239). */
+/* normalize_cluster (src/ransac.cpp:69-87) + mad_threshold (:234-239). */
 double rvk_or_prepare_cluster(int64_t n, const double* az, const double* dop, double scale,
                               double* xy, double* norm4) {
   const double* axis_src[2] = {az, dop};
@@ -134,7 +134,7 @@ double rvk_or_prepare_cluster(int64_t n, const double* az, const double* dop, do
   return scale * mean_abs_deviation(xy + 1, n, 2);
 }
 
-/* run_trial, src/ransac.cpp:177-210 (count_trial_inliers / evaluate_trial). */
+/* run_trial, src/ransac.cpp:32-65 (count_trial_inliers / evaluate_trial). */
 int32_t rvk_or_run_trial(int64_t n, const double* xy, int32_t a, int32_t b, double thr,
                          uint8_t* mask) {
   const double x1 = xy[2 * a], y1 = xy[2 * a + 1];
@@ -162,7 +162,7 @@ int32_t rvk_or_run_trial(int64_t n, const double* xy, int32_t a, int32_t b, doub
 
 static int validate(int32_t n_clusters, const int64_t* offsets, const rvk_ransac_params* p,
                     const char* who) {
-  /* src/ransac.cpp:285-299 / src/baseline.cpp:13-27 */
+  /* src/ransac.cpp:140-154 / src/baseline.cpp:13-27 */
   if (p->max_trials < 1) {
     snprintf(g_err, sizeof g_err, "%s: max_trials must be at least 1", who);
     return RVK_EINVAL;

@@ -207,7 +207,7 @@ def estimate_all_csr(offsets, azimuth, doppler, mask, frame_id: int = 0, cluster
 
 
 def trial_counts_csr(offsets, azimuth, doppler, params: RansacParams, rng_cluster_index=None):
-    """Exact per-(cluster, trial) counts, [C, max_trials] (src/ransac.cpp:308-319)."""
+    """Exact per-(cluster, trial) counts, [C, max_trials] (src/ransac.cpp:163-174)."""
     offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
     n = offsets.size - 1
     out = np.zeros(n * params.max_trials, np.int32)
@@ -266,7 +266,7 @@ def estimates_from_records(rec: np.ndarray):
 
 def run_ransac(clusters: Sequence[np.ndarray], params: RansacParams = RansacParams(),
                workers: int = 0):
-    """rvk::run_ransac (src/ransac.cpp:283-344). clusters: list of (n, 2)
+    """rvk::run_ransac (src/ransac.cpp:138-199). clusters: list of (n, 2)
     [azimuth, doppler] arrays. Returns one InlierMask per cluster, cluster_id
     = position. `workers` is accepted and ignored (the device grid replaces
     the thread team)."""
@@ -281,7 +281,7 @@ def run_ransac(clusters: Sequence[np.ndarray], params: RansacParams = RansacPara
 
 
 def gather_cluster_points(frame: Frame, clusters: Sequence[Cluster]):
-    """rvk::gather_cluster_points (src/ransac.cpp:346-360)."""
+    """rvk::gather_cluster_points (src/ransac.cpp:201-215)."""
     return [np.stack([frame.azimuth[np.asarray(cl.point_indices, dtype=np.int64)],
                       frame.doppler[np.asarray(cl.point_indices, dtype=np.int64)]], axis=1)
             for cl in clusters]
@@ -289,7 +289,7 @@ def gather_cluster_points(frame: Frame, clusters: Sequence[Cluster]):
 
 def estimate_all(frame: Frame, clusters: Sequence[Cluster], masks: Sequence[InlierMask],
                  workers: int = 0):
-    """rvk::estimate_all (src/velocity.cpp:219-248)."""
+    """rvk::estimate_all (src/velocity.cpp:92-121)."""
     del workers
     if len(clusters) != len(masks):
         raise ValueError("estimate_all: one mask per cluster required")
@@ -306,7 +306,7 @@ def estimate_all(frame: Frame, clusters: Sequence[Cluster], masks: Sequence[Inli
 
 
 def draw_seed_pair(seed: int, cluster_id: int, trial: int, n: int):
-    """rvk::draw_seed_pair (src/ransac.cpp:256-268), drawn on the device."""
+    """rvk::draw_seed_pair (src/ransac.cpp:111-123), drawn on the device."""
     if n < 2:
         raise ValueError("draw_seed_pair: need at least 2 points")
     # Build a cluster of n points keyed `cluster_id`; trials 0..trial.

@@ -129,7 +129,7 @@ Context& context() {
 
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 
-// Validation in the reference's order (src/ransac.cpp:285-299).
+// Validation in the reference's order (src/ransac.cpp:140-154).
 int validate_params(const rvk_ransac_params* p, const char* who) {
   if (p == nullptr) return fail(RVK_EINVAL, "%s: params must not be null", who);
   if (p->max_trials < 1) return fail(RVK_EINVAL, "%s: max_trials must be at least 1", who);
@@ -357,8 +357,10 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   int32_t* h_ids = reinterpret_cast<int32_t*>(h + o_ids);
   for (int i = 0; i < K; ++i)  // chunk i's offsets start at slot cut[i] + i
     for (int32_t c = cut[i]; c <= cut[i + 1]; ++c) h_off[c + i] = offsets[c] - offsets[cut[i]];
+  // RNG keys and cluster ids default to the frame-positional index: chunk
+  // kernels see chunk-local indices, so both are always passed explicitly.
   for (int32_t c = 0; c < n_clusters; ++c) h_keys[c] = keys ? keys[c] : c;
-  if (ids) std::memcpy(h_ids, ids, sizeof(int32_t) * n_clusters);
+  for (int32_t c = 0; c < n_clusters; ++c) h_ids[c] = ids ? ids[c] : c;
   if (!pin_in) {
     std::memcpy(h + o_az, az, sizeof(double) * P);
     std::memcpy(h + o_dop, dop, sizeof(double) * P);
@@ -388,7 +390,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
     f.azimuth = reinterpret_cast<const double*>(daz);
     f.doppler = reinterpret_cast<const double*>(ddop);
     f.keys = reinterpret_cast<const int32_t*>(d + o_keys) + c0;
-    f.cluster_ids = ids ? reinterpret_cast<const int32_t*>(d + o_ids) + c0 : nullptr;
+    f.cluster_ids = reinterpret_cast<const int32_t*>(d + o_ids) + c0;
     f.frame_id = frame_id;
     Scratch s = scratch(ctx.workspace(sc), nc, np, params->max_trials);
     Outputs o;
@@ -464,7 +466,7 @@ int rvk_estimate_all(int64_t frame_id, int32_t n_clusters, const int64_t* offset
                      const double* azimuth, const double* doppler, const int32_t* cluster_ids,
                      const uint8_t* mask, int32_t /*workers*/, rvk_estimate* out) {
   return guarded([&]() -> int {
-    // estimate_all validates the mask count/size (src/velocity.cpp:222-233);
+    // estimate_all validates the mask count/size (src/velocity.cpp:95-106);
     // in the CSR form the mask is P bytes aligned with the points, so only
     // the structural checks remain.
     int st = validate_offsets(n_clusters, offsets, 0, "estimate_all");

@@ -27,7 +27,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// draw_seed_pair (src/ransac.cpp:256-268): KeyedRng(seed, (u32)cluster,
+// draw_seed_pair (src/ransac.cpp:111-123): KeyedRng(seed, (u32)cluster,
 // (u32)trial); i = next_below(n); j = next_below(n-1), ++j if j >= i.
 // next_below is the high word of the 64x32 product (rng.hpp:34-38).
 __device__ __forceinline__ void seed_pair(uint64_t seed, uint32_t cluster, uint32_t trial,
@@ -45,7 +45,7 @@ __device__ __forceinline__ void seed_pair(uint64_t seed, uint32_t cluster, uint3
 }
 
 // Line through the seeds in the normalized plane, exactly as run_trial
-// (src/ransac.cpp:184-190): dx = x2 - x1; |dx| < eps -> degenerate;
+// (src/ransac.cpp:39-45): dx = x2 - x1; |dx| < eps -> degenerate;
 // m = (y2 - y1) / dx; c = y1 - m * x1; den = sqrt(m * m + 1).
 struct Line {
   double m, c, den;
@@ -62,7 +62,7 @@ __device__ __forceinline__ Line make_line(double x1, double y1, double x2, doubl
   return L;
 }
 
-// The reference's per-point decision (src/ransac.cpp:201-202):
+// The reference's per-point decision (src/ransac.cpp:56-57):
 // |(-m) * x + y - c| / den <= threshold, all FP64 round-to-nearest.
 __device__ __forceinline__ bool exact_inlier(const Line& L, double x, double y, double thr) {
   const double r = __dsub_rn(__dadd_rn(__dmul_rn(-L.m, x), y), L.c);
@@ -116,7 +116,7 @@ __device__ __forceinline__ FastHyp fast_coeffs(double m, double c, double r, dou
 }
 
 __device__ __forceinline__ FastHyp inert_fast() {
-  FastHyp h;  // degenerate seeds score 0 (src/ransac.cpp:185-187): nothing passes
+  FastHyp h;  // degenerate seeds score 0 (src/ransac.cpp:40-42): nothing passes
   h.A = h.B = h.C = 0.f;
   h.t2hi = -1.f;
   h.t2lo = -1.f;
@@ -162,7 +162,7 @@ __device__ __forceinline__ ExactHyp make_exact(const double2* __restrict__ xy64,
 enum Decision : int { kOut = 0, kIn = 1, kUndecided = 2 };
 
 // Exact inlier decision of point k for a non-degenerate hypothesis
-// (run_trial, src/ransac.cpp:192-208: seeds counted without evaluation).
+// (run_trial, src/ransac.cpp:47-63: seeds counted without evaluation).
 // kUndecided only when the FP64 distance falls inside [thr_lo, thr_hi],
 // i.e. the threshold's last bits matter and the exact sequential MAD sum is
 // needed.
@@ -183,7 +183,7 @@ __device__ __forceinline__ int classify(const ExactHyp& H, int k, float2 p32,
 
 // The reference's threshold bit for bit: mean_abs_deviation's left-to-right
 // sum (include/rvk/ransac.hpp:74-84) then mad_threshold's scale
-// (src/ransac.cpp:234-239). One thread; n dependent FP64 adds.
+// (src/ransac.cpp:89-94). One thread; n dependent FP64 adds.
 __device__ __forceinline__ double exact_threshold(const double2* xy64, int n, double med,
                                                   double scale) {
   double acc = 0.0;
@@ -200,7 +200,7 @@ __device__ __forceinline__ double exact_threshold(const double2* xy64, int n, do
 }
 
 // Packs (count, trial) so that a max picks the largest count and, on ties,
-// the lowest trial -- the ascending strict-> scan of src/ransac.cpp:326-334.
+// the lowest trial -- the ascending strict-> scan of src/ransac.cpp:181-189.
 __device__ __forceinline__ unsigned long long pack_best(int count, int trial) {
   return (static_cast<unsigned long long>(static_cast<uint32_t>(count)) << 32) |
          static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(trial));

@@ -2,11 +2,11 @@
 //
 //   std::vector<InlierMask> rvk::run_ransac(const std::vector<Eigen::ArrayX2d>&,
 //                                           const RansacParams&, int workers)
-//       -- include/rvk/ransac.hpp:128-129, replaces src/ransac.cpp:283-344
+//       -- include/rvk/ransac.hpp:128-129, replaces src/ransac.cpp:138-199
 //   std::vector<VelocityEstimate> rvk::estimate_all(const Frame&,
 //                                                   const std::vector<Cluster>&,
 //                                                   const std::vector<InlierMask>&, int workers)
-//       -- include/rvk/velocity.hpp:123-125, replaces src/velocity.cpp:219-248
+//       -- include/rvk/velocity.hpp:123-125, replaces src/velocity.cpp:92-121
 //
 // with the reference's exact signatures, compiled against the reference's
 // public headers (proj/include/rvk) and Eigen. Both marshal into the CSR
@@ -81,14 +81,14 @@ std::vector<InlierMask> run_ransac(const std::vector<Eigen::ArrayX2d>& clusters,
 std::vector<VelocityEstimate> estimate_all(const Frame& frame, const std::vector<Cluster>& clusters,
                                            const std::vector<InlierMask>& masks,
                                            int /*workers*/) {
-  if (clusters.size() != masks.size())  // src/velocity.cpp:222-224
+  if (clusters.size() != masks.size())  // src/velocity.cpp:95-97
     throw std::invalid_argument("estimate_all: one mask per cluster required");
   const int32_t n = static_cast<int32_t>(clusters.size());
   std::vector<int64_t> offsets(static_cast<std::size_t>(n) + 1, 0);
   for (int32_t c = 0; c < n; ++c) {
     const auto& cl = clusters[static_cast<std::size_t>(c)];
     if (masks[static_cast<std::size_t>(c)].mask.size() !=
-        static_cast<Eigen::Index>(cl.point_indices.size()))  // velocity.cpp:231-233
+        static_cast<Eigen::Index>(cl.point_indices.size()))  // velocity.cpp:104-106
       throw std::invalid_argument("estimate_all: mask size does not match cluster size");
     offsets[c + 1] = offsets[c] + static_cast<int64_t>(cl.point_indices.size());
   }

@@ -1,10 +1,10 @@
 // sm_100a kernels of the per-cluster velocity-profile estimator.
 //
 //   prep_kernel    normalize_cluster + median + mad_threshold
-//                  (src/ransac.cpp:214-239, include/rvk/ransac.hpp:53-84)
+//                  (src/ransac.cpp:69-94, include/rvk/ransac.hpp:53-84)
 //   score_kernel   the hot loop: every (cluster, trial) line hypothesis
 //                  against every point of its cluster (run_trial,
-//                  src/ransac.cpp:177-210, scheduled as in :303-319), FP32
+//                  src/ransac.cpp:32-65, scheduled as in :303-319), FP32
 //                  packed FFMA2 with a guard band -> UPPER-BOUND counts
 //   select_kernel  exact argmax (max count, lowest trial; :321-334): the
 //                  best upper bound is verified exactly, then every trial
@@ -224,7 +224,7 @@ __device__ double first_zero(double v, const double* __restrict__ a, int n, doub
   return a[first];
 }
 
-// Per cluster (one CTA): normalize_cluster (src/ransac.cpp:214-232), the
+// Per cluster (one CTA): normalize_cluster (src/ransac.cpp:69-87), the
 // median of the normalized dopplers (ransac.hpp:53-70, exact: bitonic sort in
 // shared memory, or radix select over global memory for huge clusters), and
 // the MAD corridor as a guaranteed interval.
@@ -659,7 +659,7 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
 // (exact[t] <= U[t]), t0 = the lowest trial with the largest U and
 // E0 = exact[t0], a trial t can only beat or tie-win against t0 if
 // U[t] > E0, or U[t] == E0 and t < t0 (ties go to the lowest trial,
-// src/ransac.cpp:326-334). Only those are verified; when U[t0] == E0 there
+// src/ransac.cpp:181-189). Only those are verified; when U[t0] == E0 there
 // are none. Then the winner's mask (evaluate_trial, :274-281) and the LSQ
 // refit on its inliers.
 __global__ void __launch_bounds__(kSelectThreads)
@@ -755,7 +755,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   const int win = unpack_trial(best);
   const int win_count = unpack_count(best);
 
-  // 4. winner mask (evaluate_trial, src/ransac.cpp:274-281).
+  // 4. winner mask (evaluate_trial, src/ransac.cpp:129-136).
   for (int pass = 0; pass < 2; ++pass) {
     const ExactHyp W = make_exact(p64, seed, key, static_cast<uint32_t>(win), n, thr_lo, thr_hi);
     bool und = false;

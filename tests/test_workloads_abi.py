@@ -123,7 +123,7 @@ def test_host_validation_without_gpu():
             as e:
         rvk.run_ransac_csr(off, az, az, rvk.RansacParams())
     assert e.value.cluster == 1
-    # params are checked before cluster sizes (src/ransac.cpp:285-299)
+    # params are checked before cluster sizes (src/ransac.cpp:140-154)
     with pytest.raises(ValueError):
         rvk.run_ransac_csr(off, az, az, rvk.RansacParams(max_trials=0))
     # empty input -> empty output, no device work
