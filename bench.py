@@ -441,8 +441,7 @@ def main():
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals_per_launch,
                 "avg_launch_ms": score_ms, "traffic": traffic,
                 "share_of_step": stage_ms[2] / total_ms if total_ms else None,
-                "stage_ms_per_step": {"prep": stage_ms[0] / n_iso,
-                                      "hyp_setup": stage_ms[1] / n_iso,
+                "stage_ms_per_step": {"prep_hyp_setup": stage_ms[0] / n_iso,
                                       "score": stage_ms[2] / n_iso,
                                       "select_refit": stage_ms[3] / n_iso},
                 "measured": "isolated single-stream pass (%d steps) right after the timed "

@@ -89,7 +89,7 @@ struct HostBuf {
 
 // Device scratch of one stream's in-flight pipeline.
 struct Workspace {
-  DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, aux;
+  DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, tile_count, aux;
 };
 
 struct Context {
@@ -223,13 +223,17 @@ FrameDev stage_frame(Context& ctx, int64_t frame_id, int32_t n_clusters, const i
 
 Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   Scratch s;
+  const ScoreGeom g = score_geom(std::max(T, 1));
+  const size_t C = static_cast<size_t>(n_clusters);
   s.xy64 = w.xy64.get<double2>(P);
-  s.xy32 = w.xy32.get<float2>(P + 2);
-  s.stat = w.thr.get<double4>(n_clusters);
-  s.norm = w.norm.get<double>(4 * static_cast<size_t>(n_clusters));
-  s.upper = w.upper.get<int32_t>(static_cast<size_t>(n_clusters) * std::max(T, 1));
-  s.hyp = w.hyp.get<float4>(static_cast<size_t>(n_clusters) * std::max(T, 1));
-  s.tile_start = w.tiles.get<int32_t>(static_cast<size_t>(n_clusters) + 1);
+  s.xy32 = w.xy32.get<float2>(P + 2 * C + 2);
+  s.stat = w.thr.get<double4>(C);
+  s.norm = w.norm.get<double>(4 * C);
+  s.upper = w.upper.get<int32_t>(C * g.Tg * 8);
+  s.hyp = w.hyp.get<float>(C * g.Tg * 32);
+  s.tile_cap = tile_capacity(g, P, n_clusters);
+  s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
+  s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
   return s;
 }
 
@@ -282,11 +286,12 @@ void stage(int id, cudaStream_t st, F&& launch) {
   g_prof.recs.push_back(r);
 }
 
-// prep -> hyps -> score -> select(+refit): the whole device pipeline of one call.
+// prep+hyps -> score -> select(+refit): the whole device pipeline of one call.
+// Stage ids (rvk_profile_read): 0 = prep + hypothesis setup + tile plan,
+// 2 = score, 3 = select + refit (1 is unused since the fusion of setup into prep).
 void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   const Outputs& o, cudaStream_t st) {
-  stage(0, st, [&] { launch_prep(f, p.threshold_scale, s, st); });
-  stage(1, st, [&] { launch_hyps(f, p, s, st); });
+  stage(0, st, [&] { launch_prep_hyps(f, p, s, st); });
   stage(2, st, [&] { launch_score(f, p, s, st); });
   stage(3, st, [&] { launch_select(f, p, s, o, st); });
   check_launch();

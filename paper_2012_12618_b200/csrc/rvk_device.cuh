@@ -88,6 +88,7 @@ struct FastHyp {
   float A, B, C;
   float t2hi;  // e^2 < t2hi: possible inlier (upper-bound count)
   float t2lo;  // e^2 < t2lo: certain inlier
+  float thi;   // |e| <= thi: possible inlier (linear form of t2hi, same band)
 };
 
 // Coefficients from (m, c) and r ~= 1/den. r may carry a few FP64 ulps of
@@ -106,6 +107,7 @@ __device__ __forceinline__ FastHyp fast_coeffs(double m, double c, double r, dou
   h.C = __double2float_rn(C);
   const double hi = (thr_hi + band) * (1.0 + 0x1p-30);
   h.t2hi = __double2float_ru(hi * hi);
+  h.thi = __double2float_ru(hi);
   if (thr_lo > band) {
     const double lo = (thr_lo - band) * (1.0 - 0x1p-30);
     h.t2lo = __double2float_rd(lo * lo);
@@ -120,6 +122,7 @@ __device__ __forceinline__ FastHyp inert_fast() {
   h.A = h.B = h.C = 0.f;
   h.t2hi = -1.f;
   h.t2lo = -1.f;
+  h.thi = -1.f;
   return h;
 }
 

@@ -40,10 +40,7 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
-constexpr int kScoreThreads = 128;
 constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
-constexpr int kPT = 256;          // points per scoring task (one chunk)
-constexpr int kMaxTileChunks = kScoreThreads / kNH + 1;  // chunks a tile can touch (G >= 8)
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
 constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
@@ -153,7 +150,7 @@ __device__ double block_select_y(const double2* xy, int n, int k,
 
 // k-th smallest (0-based) of n non-negative doubles given as bit patterns in
 // shared memory: MSD radix select with 11-bit digits (6 passes), exact.
-// hist: 2048 counters; sh: 2 ints of scratch.
+// hist: 2048 counters; sh: 2 ints of scratch. Fallback of block_select_pair.
 __device__ unsigned long long block_radix_select(const unsigned long long* keys, int n, int k,
                                                  unsigned int* hist, int* sh) {
   unsigned long long prefix = 0, mask = 0;
@@ -215,6 +212,120 @@ __device__ unsigned long long block_radix_select(const unsigned long long* keys,
   return prefix;
 }
 
+constexpr int kMedBins = 2048;  // value buckets of [0, 1] for the median
+constexpr int kCandCap = 512;   // candidates ranked directly
+
+__device__ __forceinline__ int med_bin(unsigned long long key) {
+  const double y = __longlong_as_double(static_cast<long long>(key));
+  const int b = static_cast<int>(y * kMedBins);  // exact scaling; y in [0, 1]
+  return b < kMedBins - 1 ? b : kMedBins - 1;
+}
+
+struct PrepShared {
+  unsigned long long keys[kSortCap];  // normalized dopplers (bit patterns, sign cleared)
+  unsigned long long cand[kCandCap];
+  unsigned int hist[kMedBins];
+  double red[32];
+  double4 red4[32];
+  unsigned long long sel[2];
+  int sh[4];
+  unsigned int wsum[32];
+  double4 stat;
+};
+
+// The k-th and (k+1)-th smallest keys (k+1 only if `pair`), exact. Keys are
+// bucketed by value (a monotone map), the bucket holding rank k is collected
+// and ranked directly; a crowded bucket falls back to the radix select.
+__device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
+                                  unsigned long long& v0, unsigned long long& v1) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  for (int i = tid; i < kMedBins; i += nt) sm.hist[i] = 0;
+  if (tid == 0) sm.sh[2] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) atomicAdd(&sm.hist[med_bin(sm.keys[i])], 1u);
+  __syncthreads();
+  // bin holding rank k: thread j owns bins [j*per, (j+1)*per)
+  const int per = kMedBins / nt;  // nt divides kMedBins (256 threads)
+  unsigned int local = 0;
+  for (int q = 0; q < per; ++q) local += sm.hist[tid * per + q];
+  const int lane = tid & 31, warp = tid >> 5;
+  unsigned int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) sm.wsum[warp] = incl;
+  __syncthreads();
+  unsigned int base = 0;
+  for (int w = 0; w < warp; ++w) base += sm.wsum[w];
+  const unsigned int excl = base + incl - local;
+  const unsigned int kk = static_cast<unsigned int>(k);
+  if (kk >= excl && kk < excl + local) {
+    unsigned int cum = excl;
+    for (int q = 0; q < per; ++q) {
+      const unsigned int h = sm.hist[tid * per + q];
+      if (kk < cum + h) {
+        sm.sh[0] = tid * per + q;          // bin
+        sm.sh[1] = static_cast<int>(cum);  // keys below the bin
+        break;
+      }
+      cum += h;
+    }
+  }
+  __syncthreads();
+  const int bin = sm.sh[0];
+  const int below = sm.sh[1];
+  const int in_bin = static_cast<int>(sm.hist[bin]);
+  if (in_bin > kCandCap) {  // crowded bucket: exact radix select
+    v0 = block_radix_select(sm.keys, n, k, sm.hist, sm.sh);
+    if (pair) v1 = block_radix_select(sm.keys, n, k + 1, sm.hist, sm.sh);
+    return;
+  }
+  for (int i = tid; i < n; i += nt) {
+    const unsigned long long key = sm.keys[i];
+    if (med_bin(key) == bin) sm.cand[atomicAdd(reinterpret_cast<unsigned int*>(&sm.sh[2]), 1u)] = key;
+  }
+  const bool second_in_bin = pair && k + 1 < below + in_bin;
+  __syncthreads();
+  const int r0 = k - below;
+  for (int i = tid; i < in_bin; i += nt) {
+    const unsigned long long ci = sm.cand[i];
+    int less = 0, eq = 0;
+    for (int j = 0; j < in_bin; ++j) {
+      const unsigned long long cj = sm.cand[j];
+      less += cj < ci;
+      eq += cj == ci;
+    }
+    if (r0 >= less && r0 < less + eq) sm.sel[0] = ci;
+    if (second_in_bin && r0 + 1 >= less && r0 + 1 < less + eq) sm.sel[1] = ci;
+  }
+  if (pair && !second_in_bin) {
+    // the (k+1)-th is the smallest key above the bin
+    unsigned long long m = ~0ull;
+    for (int i = tid; i < n; i += nt) {
+      const unsigned long long key = sm.keys[i];
+      if (med_bin(key) > bin && key < m) m = key;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long u = __shfl_xor_sync(0xffffffffu, m, o);
+      m = u < m ? u : m;
+    }
+    __syncthreads();
+    if (lane == 0) sm.cand[warp] = m;  // cand[] reads are done
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long r = sm.cand[0];
+      for (int w = 1; w < (nt >> 5); ++w) r = sm.cand[w] < r ? sm.cand[w] : r;
+      sm.sel[1] = r;
+    }
+  }
+  __syncthreads();
+  v0 = sm.sel[0];
+  if (pair) v1 = sm.sel[1];
+}
+
 __device__ double first_zero(double v, const double* __restrict__ a, int n, double* red) {
   if (v != 0.0) return v;
   int first = INT_MAX;
@@ -224,10 +335,19 @@ __device__ double first_zero(double v, const double* __restrict__ a, int n, doub
   return a[first];
 }
 
-// Per cluster (one CTA): normalize_cluster (src/ransac.cpp:69-87), the
-// median of the normalized dopplers (ransac.hpp:53-70, exact: bitonic sort in
-// shared memory, or radix select over global memory for huge clusters), and
-// the MAD corridor as a guaranteed interval.
+// Size bucket of a partial tile of `rem` points (1 <= rem < kScorePPT):
+// larger tiles get lower buckets, bucket 0 holds the full tiles.
+__device__ __forceinline__ int tile_bucket(int rem) {
+  return 1 + (kScorePPT - 1 - rem) / (kScorePPT / (kTileBuckets - 1));
+}
+
+__device__ __forceinline__ int64_t xy32_base(const int64_t* offsets, int c) {
+  return ((offsets[c] + 1) & ~int64_t{1}) + 2 * static_cast<int64_t>(c);
+}
+
+// Per cluster (one CTA): normalize_cluster (src/ransac.cpp:69-87), the median
+// of the normalized dopplers (ransac.hpp:53-70, exact selection), and the MAD
+// corridor as a guaranteed interval. Leaves stat in sm.stat for the caller.
 //
 // The reference sums |y_i - med| left to right (ransac.hpp:78-83), n
 // dependent FP64 adds; that order cannot be parallelized bit-exactly. Here
@@ -240,18 +360,10 @@ __device__ double first_zero(double v, const double* __restrict__ a, int n, doub
 // lands inside it (exact_threshold(); practically never).
 //
 // stat[c] = (thr_lo, thr_hi, median, thr_exact or NaN).
-__global__ void __launch_bounds__(kPrepThreads)
-prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
-            const double* __restrict__ az, const double* __restrict__ dop, double scale,
-            double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
-            double* __restrict__ norm) {
-  __shared__ double red[32];
-  __shared__ unsigned long long sy[kSortCap];  // normalized dopplers (bit patterns)
-  __shared__ unsigned int hist[2048];
-  __shared__ unsigned long long sh_prefix;
-  __shared__ int sh_k;
-  __shared__ int sh2[2];
-  const int c = blockIdx.x;
+__device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ offsets,
+                             const double* __restrict__ az, const double* __restrict__ dop,
+                             double scale, double2* xy64, float2* __restrict__ xy32,
+                             double4* __restrict__ stat, double* __restrict__ norm) {
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
 
@@ -272,12 +384,11 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       v.z = fmin(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
       v.w = fmin(v.w, __shfl_xor_sync(0xffffffffu, v.w, o));
     }
-    __shared__ double4 red4[32];
-    if ((threadIdx.x & 31) == 0) red4[threadIdx.x >> 5] = v;
+    if ((threadIdx.x & 31) == 0) sm.red4[threadIdx.x >> 5] = v;
     __syncthreads();
-    v = red4[0];
+    v = sm.red4[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      const double4 u = red4[w];
+      const double4 u = sm.red4[w];
       v.x = fmin(v.x, u.x);
       v.y = fmin(v.y, u.y);
       v.z = fmin(v.z, u.z);
@@ -291,22 +402,25 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   // Eigen's minCoeff/maxCoeff keep the FIRST extreme in index order; values
   // that compare equal differ in bits only for +-0, so an extreme equal to
   // zero takes the bits of its first occurrence (block-uniform branch).
-  lo0 = first_zero(lo0, az + b, n, red);
-  hi0 = first_zero(hi0, az + b, n, red);
-  lo1 = first_zero(lo1, dop + b, n, red);
-  hi1 = first_zero(hi1, dop + b, n, red);
+  lo0 = first_zero(lo0, az + b, n, sm.red);
+  hi0 = first_zero(hi0, az + b, n, sm.red);
+  lo1 = first_zero(lo1, dop + b, n, sm.red);
+  hi1 = first_zero(hi1, dop + b, n, sm.red);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   const bool in_smem = n <= kSortCap;
+  float2* p32 = xy32 + xy32_base(offsets, c);
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
-    xy32[b + k] = make_float2(__double2float_rn(x), __double2float_rn(y));
+    p32[k] = make_float2(__double2float_rn(x), __double2float_rn(y));
     // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
     // std::sort's operator< treats them; every other value is >= +0)
-    if (in_smem) sy[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
+    if (in_smem)
+      sm.keys[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
   }
+  if (threadIdx.x == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);  // pad to even
   if (threadIdx.x == 0 && norm != nullptr) {
     norm[4 * c + 0] = lo0;
     norm[4 * c + 1] = lo1;
@@ -319,51 +433,110 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   if (in_smem) {
     // k-th order statistics (median of the sorted copy, ransac.hpp:60-69).
     const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
-    const unsigned long long v0 = block_radix_select(sy, n, k0, hist, sh2);
+    unsigned long long v0 = 0, v1 = 0;
+    block_select_pair(sm, n, k0, (n & 1) == 0, v0, v1);
     const double d0 = __longlong_as_double(static_cast<long long>(v0));
-    if (n & 1) {
-      med = d0;
-    } else {
-      // next order statistic: v0 again if more than k0+1 keys are <= v0,
-      // else the smallest key above v0.
-      int le = 0;
-      double above = CUDART_INF;
-      for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const unsigned long long key = sy[k];
-        if (key <= v0) {
-          ++le;
-        } else {
-          const double y = __longlong_as_double(static_cast<long long>(key));
-          above = y < above ? y : above;
-        }
-      }
-      le = block_reduce(le, SumI(), reinterpret_cast<int*>(hist));
-      above = block_reduce(above, MinOp(), red);
-      const double d1 = le >= n / 2 + 1 ? d0 : above;
-      med = __ddiv_rn(__dadd_rn(d0, d1), 2.0);
-    }
+    med = (n & 1) ? d0
+                  : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))), 2.0);
   } else {
     const double2* cxy = xy64 + b;
     if (n & 1) {
-      med = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+      med = block_select_y(cxy, n, n / 2, sm.hist, &sm.sel[0], &sm.sh[0]);
     } else {
-      const double lo = block_select_y(cxy, n, n / 2 - 1, hist, &sh_prefix, &sh_k);
-      const double hi = block_select_y(cxy, n, n / 2, hist, &sh_prefix, &sh_k);
+      const double lo = block_select_y(cxy, n, n / 2 - 1, sm.hist, &sm.sel[0], &sm.sh[0]);
+      const double hi = block_select_y(cxy, n, n / 2, sm.hist, &sm.sel[0], &sm.sh[0]);
       med = __ddiv_rn(__dadd_rn(lo, hi), 2.0);
     }
   }
 
   double part = 0.0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const double y = in_smem ? __longlong_as_double(static_cast<long long>(sy[k]))
+    const double y = in_smem ? __longlong_as_double(static_cast<long long>(sm.keys[k]))
                              : xy64[b + k].y;
     part += fabs(__dsub_rn(y, med));
   }
-  const double S = block_reduce(part, SumD(), red);
+  const double S = block_reduce(part, SumD(), sm.red);
   if (threadIdx.x == 0) {
     const double mid = scale * (S / n);
     const double delta = (4.0 * n + 16.0) * 0x1p-53;
-    stat[c] = make_double4(mid * (1.0 - delta), mid * (1.0 + delta), med, CUDART_NAN);
+    const double4 st = make_double4(mid * (1.0 - delta), mid * (1.0 + delta), med, CUDART_NAN);
+    stat[c] = st;
+    sm.stat = st;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPrepThreads)
+prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+            const double* __restrict__ az, const double* __restrict__ dop, double scale,
+            double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
+            double* __restrict__ norm) {
+  __shared__ PrepShared sm;
+  prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
+}
+
+// prep + hypothesis setup + tile registration, one CTA per cluster.
+//
+// Hypotheses (src/ransac.cpp:35-46 for every trial of draw_seed_pair
+// :111-123): exact FP64 slope/intercept from the KeyedRng seed pair, FP32
+// coefficients and corridor bound, stored per group of 8 trials as
+// A[8] B[8] C[8] K[8] (K = -t2hi for the squared compare). Trials beyond T
+// in the last group are inert. The cluster's upper-bound counters are zeroed
+// and its scoring tiles (kScorePPT points x TS groups each) are appended to
+// the size bucket they belong to, so the scoring kernel takes them
+// largest-first.
+__global__ void __launch_bounds__(kPrepThreads)
+prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                const double* __restrict__ az, const double* __restrict__ dop, double scale,
+                const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
+                float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
+                int32_t* __restrict__ upper, int4* __restrict__ tiles,
+                int32_t* __restrict__ tile_count, int64_t tile_cap) {
+  __shared__ PrepShared sm;
+  __shared__ int tile_pos[2];
+  const int c = blockIdx.x;
+  prep_cluster(sm, c, offsets, az, dop, scale, xy64, xy32, stat, nullptr);
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double thr_lo = sm.stat.x, thr_hi = sm.stat.y;
+  const double2* p64 = xy64 + b;  // written by this CTA before the barrier
+  float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
+  int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
+  for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) {
+    FastHyp f = inert_fast();
+    if (t < g.T) {
+      int i, j;
+      seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+      const double2 p = p64[i];
+      const double2 q = p64[j];
+      f = make_fast_from_seeds(p.x, p.y, q.x, q.y, thr_lo, thr_hi);
+    }
+    float* h = hc + (t >> 3) * 32 + (t & 7);
+    h[0] = f.A;
+    h[8] = f.B;
+    h[16] = f.C;
+    h[24] = -f.t2hi;
+    uc[t] = 0;
+  }
+  // scoring tiles of this cluster
+  const int full = n / kScorePPT, rem = n % kScorePPT;
+  if (threadIdx.x == 0) {
+    tile_pos[0] = full ? atomicAdd(&tile_count[0], full * g.nhb) : 0;
+    tile_pos[1] = rem ? atomicAdd(&tile_count[tile_bucket(rem)], g.nhb) : 0;
+  }
+  __syncthreads();
+  const int64_t base32 = xy32_base(offsets, c);
+  for (int i = threadIdx.x; i < full * g.nhb; i += blockDim.x) {
+    const int pb = i / g.nhb, hb = i - pb * g.nhb;
+    tiles[tile_pos[0] + i] =
+        make_int4(c, static_cast<int>(base32 + pb * kScorePPT), kScorePPT, hb * g.TS);
+  }
+  if (rem) {
+    const int bk = tile_bucket(rem);
+    for (int hb = threadIdx.x; hb < g.nhb; hb += blockDim.x)
+      tiles[bk * tile_cap + tile_pos[1] + hb] =
+          make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
   }
 }
 
@@ -387,152 +560,202 @@ __global__ void mad_exact_kernel(int32_t n_clusters, const int64_t* __restrict__
 
 // ------------------------------------------------------------ score kernel
 
-// One thread per (cluster, trial): seed pair (KeyedRng), exact FP64 line,
-// FP32 coefficients and corridor bound -> hyp[c*T + t] = (A, B, C, -t2hi);
-// also zeroes the upper-bound counters the scoring tiles accumulate into.
-__global__ void hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
-                           const double2* __restrict__ xy64, const double4* __restrict__ stat,
-                           const int32_t* __restrict__ keys, int T, uint64_t seed,
-                           float4* __restrict__ hyp, int32_t* __restrict__ upper) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<int64_t>(n_clusters) * T) return;
-  const int c = static_cast<int>(idx / T), t = static_cast<int>(idx - static_cast<int64_t>(c) * T);
-  const int64_t b = offsets[c];
-  const int n = static_cast<int>(offsets[c + 1] - b);
-  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-  const double4 st = stat[c];
-  int i, j;
-  seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-  const double2 p = xy64[b + i];
-  const double2 q = xy64[b + j];
-  const FastHyp f = make_fast_from_seeds(p.x, p.y, q.x, q.y, st.x, st.y);
-  hyp[idx] = make_float4(f.A, f.B, f.C, -f.t2hi);
-  upper[idx] = 0;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
-// Tile plan: a scoring task = (cluster, group of kNH trials, chunk of kPT
-// points); a tile = 128 consecutive tasks of one cluster (groups fastest), so
-// every tile costs about the same (<= 8 x 256 x 128 evaluations) whatever the
-// cluster sizes. tile_start[c] = exclusive prefix of tiles per cluster.
-__device__ __forceinline__ int score_groups(int T) { return max((T + kNH - 1) / kNH, kNH); }
+constexpr int kStages = 3;  // scoring tile ring depth
 
-__global__ void tile_plan_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets, int T,
-                                 int32_t* __restrict__ tile_start) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  const int G = score_groups(T);
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n_clusters; base += blockDim.x) {
-    const int c = base + threadIdx.x;
-    int tiles = 0;
-    if (c < n_clusters) {
-      const int n = static_cast<int>(offsets[c + 1] - offsets[c]);
-      const long long tasks = static_cast<long long>(G) * ((n + kPT - 1) / kPT);
-      tiles = static_cast<int>((tasks + kScoreThreads - 1) / kScoreThreads);
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = tiles;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    int off = carry;
-    for (int w = 0; w < warp; ++w) off += wsum[w];
-    if (c < n_clusters) tile_start[c] = off + incl - tiles;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = off + incl;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) tile_start[n_clusters] = carry;
+struct ScoreShared {
+  uint64_t full[kStages];  // tile landed (expect_tx + bulk-copy bytes)
+  int4 desc[kStages];
+  int done[kStages];       // warps finished with the stage
+  int bstart[kTileBuckets + 1];
+};
+
+__host__ __device__ __forceinline__ size_t score_smem_bytes(const ScoreGeom& g) {
+  // [ScoreShared | hyps x kStages | points x kStages | 16 B read-ahead pad]
+  return 512 + kStages * (static_cast<size_t>(g.TS) * 128 + kScorePPT * 8) + 16;
 }
 
-// The hot loop. Each thread scores kNH = 8 hypotheses (four FFMA2 pairs)
-// against the kPT points of its chunk, staged in shared memory and read as
-// float4 broadcasts (two points). Per point and pair: 3 FFMA2
-// (e = A x + (B y + C); g = e^2 - t2hi) and the sign bit of g added to the
-// count (LEA.HI). Counts are upper bounds (guard band, see make_fast) and
-// accumulate over chunks with integer atomics (order-free, deterministic).
-__global__ void __launch_bounds__(kScoreThreads)
-score_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
-             const float2* __restrict__ xy32, const float4* __restrict__ hyp,
-             const int32_t* __restrict__ tile_start, int T, int32_t* __restrict__ upper) {
-  __shared__ float4 pts[kMaxTileChunks * kPT / 2];
-  const int tile = blockIdx.x;
-  if (tile >= tile_start[n_clusters]) return;
-  // cluster owning this tile: last c with tile_start[c] <= tile
-  int lo = 0, hi = n_clusters - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (tile_start[mid] <= tile) lo = mid; else hi = mid - 1;
-  }
-  const int c = lo;
-  const int64_t b = offsets[c];
-  const int n = static_cast<int>(offsets[c + 1] - b);
-  const int G = score_groups(T);
-  const int nch = (n + kPT - 1) / kPT;
-  const long long tasks = static_cast<long long>(G) * nch;
-  const long long task0 = static_cast<long long>(tile - tile_start[c]) * kScoreThreads;
-  const int k_first = static_cast<int>(task0 / G);
-  const int k_last = static_cast<int>(min(task0 + kScoreThreads - 1, tasks - 1) / G);
-
-  // stage chunks [k_first, k_last] (padded to even counts per chunk)
-  const int p_first = k_first * kPT;
-  const int p_end = min(n, (k_last + 1) * kPT);
-  for (int i = threadIdx.x; i < (k_last - k_first + 1) * (kPT / 2); i += blockDim.x) {
-    const int p = p_first + 2 * i;
-    const float2 p0 = p < p_end ? xy32[b + p] : make_float2(0.f, kPadY);
-    const float2 p1 = p + 1 < p_end ? xy32[b + p + 1] : make_float2(0.f, kPadY);
-    pts[i] = make_float4(p0.x, p0.y, p1.x, p1.y);
-  }
-  const long long task = task0 + threadIdx.x;
-  const bool valid = task < tasks;
-  const int g = valid ? static_cast<int>(task % G) : 0;
-  const int k = valid ? static_cast<int>(task / G) : k_first;
-  const int t0 = g * kNH;
-  float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
-  const float4* hp = hyp + static_cast<int64_t>(c) * T;
+// The hot loop, persistent. Each CTA claims tiles from the LPT-ordered tile
+// list with an atomic counter (largest first, so the tail is short); a tile
+// = (cluster, up to kScorePPT points, TS groups of 8 hypotheses). Tiles
+// stream through a kStages-deep shared-memory ring: the points and the
+// hypothesis coefficients of a tile arrive by cp.async.bulk (TMA engine) on
+// the stage's mbarrier; the last warp to finish a stage claims the next tile
+// and refills it, so warps never wait for each other at a CTA barrier.
+// Thread (slice s, group j) scores its 8 hypotheses (four FFMA2 pairs)
+// against slice s of the tile's points, read as float4 broadcasts (two
+// points): per point and pair 3 FFMA2 (e = A x + (B y + C); g = e^2 - t2hi)
+// and the sign bit of g added to the count (LEA.HI). Counts are upper bounds
+// (guard band, see make_fast) and accumulate over tiles with integer atomics
+// (order-free, deterministic).
+__global__ void __launch_bounds__(kScoreThreads, 2)
+score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
+             int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
+             ScoreGeom g, int32_t* __restrict__ upper) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  ScoreShared& sh = *reinterpret_cast<ScoreShared*>(smem);
+  auto hyps_at = [&](int st) { return reinterpret_cast<float*>(smem + 512 + st * g.TS * 128); };
+  auto pts_at = [&](int st) {
+    return reinterpret_cast<float4*>(smem + 512 + kStages * g.TS * 128 + st * kScorePPT * 8);
+  };
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {  // exclusive prefix of the bucket sizes
+    int carry = 0;
+    for (int b0 = 0; b0 < kTileBuckets; b0 += 32) {
+      const int v = b0 + tid < kTileBuckets ? tile_count[b0 + tid] : 0;
+      int incl = v;
 #pragma unroll
-  for (int q = 0; q < kNH; ++q) {
-    float4 h = make_float4(0.f, 0.f, 0.f, 1.f);  // inert: e^2 + 1 > 0
-    if (valid && t0 + q < T) h = hp[t0 + q];
-    if (q & 1) {
-      A[q >> 1].y = h.x; B[q >> 1].y = h.y; Cc[q >> 1].y = h.z; T2[q >> 1].y = h.w;
-    } else {
-      A[q >> 1].x = h.x; B[q >> 1].x = h.y; Cc[q >> 1].x = h.z; T2[q >> 1].x = h.w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += u;
+      }
+      if (b0 + tid < kTileBuckets) sh.bstart[b0 + tid] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tid == 0) {
+      sh.bstart[kTileBuckets] = carry;
+      for (int s = 0; s < kStages; ++s) {
+        mbar_init(&sh.full[s], 1);
+        sh.done[s] = 0;
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
   __syncthreads();
-  uint32_t cnt[kNH];
+  const int total = sh.bstart[kTileBuckets];
+
+  // Claims the next tile (dynamic, in LPT order) and streams it into stage
+  // st; a negative cluster id marks "no more tiles".
+  int* next_tile = const_cast<int*>(tile_count) + kTileBuckets;
+  auto fetch = [&](int st) {
+    const int i = atomicAdd(next_tile, 1);
+    if (i >= total) {
+      sh.desc[st] = make_int4(-1, 0, 0, 0);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sh.full[st]))
+                   : "memory");
+      return;
+    }
+    int bk = 0;
+    while (sh.bstart[bk + 1] <= i) ++bk;
+    const int4 d = tiles[bk * tile_cap + (i - sh.bstart[bk])];
+    sh.desc[st] = d;
+    const int ng = min(g.TS, g.Tg - d.w);
+    const uint32_t hb = static_cast<uint32_t>(ng) * 128u;
+    const uint32_t pb = static_cast<uint32_t>((d.z + 1) & ~1) * 8u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&sh.full[st], hb + pb);
+    bulk_g2s(hyps_at(st), hyp + (static_cast<int64_t>(d.x) * g.Tg + d.w) * 32, hb, &sh.full[st]);
+    bulk_g2s(pts_at(st), xy32 + d.y, pb, &sh.full[st]);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kStages; ++s) fetch(s);
+
+  const int slice = tid / g.TS;
+  const int j = tid - slice * g.TS;
+  const int warps = kScoreThreads / 32;
+#pragma unroll 1
+  for (int k = 0;; ++k) {
+    const int st = k % kStages;
+    mbar_wait(&sh.full[st], (k / kStages) & 1);
+    const int4 d = sh.desc[st];
+    if (d.x < 0) break;
+    const bool active = j < g.Tg - d.w;
+    uint32_t cnt[kNH];
 #pragma unroll
-  for (int q = 0; q < kNH; ++q) cnt[q] = 0;
-  const float4* cp = pts + (k - k_first) * (kPT / 2);
-  const int m2 = (min(kPT, n - k * kPT) + 1) >> 1;
-#pragma unroll 2
-  for (int i = 0; i < m2; ++i) {
-    const float4 v = cp[i];
+    for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+    if (active) {
+      const float4* hp = reinterpret_cast<const float4*>(hyps_at(st) + j * 32);
+      float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
 #pragma unroll
-    for (int pr = 0; pr < kNH / 2; ++pr) {
-      float2 e = __ffma2_rn(A[pr], make_float2(v.x, v.x),
-                            __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
-      float2 gg = __ffma2_rn(e, e, T2[pr]);
-      cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
-      cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
-      e = __ffma2_rn(A[pr], make_float2(v.z, v.z),
-                     __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
-      gg = __ffma2_rn(e, e, T2[pr]);
-      cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
-      cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
+      for (int h = 0; h < 2; ++h) {
+        const float4 a = hp[h], bb = hp[2 + h], cc = hp[4 + h], kk = hp[6 + h];
+        A[2 * h] = make_float2(a.x, a.y);
+        A[2 * h + 1] = make_float2(a.z, a.w);
+        B[2 * h] = make_float2(bb.x, bb.y);
+        B[2 * h + 1] = make_float2(bb.z, bb.w);
+        Cc[2 * h] = make_float2(cc.x, cc.y);
+        Cc[2 * h + 1] = make_float2(cc.z, cc.w);
+        T2[2 * h] = make_float2(kk.x, kk.y);
+        T2[2 * h + 1] = make_float2(kk.z, kk.w);
+      }
+      // this slice's points: an even-aligned, even-length share of the tile
+      const int len = ((d.z + g.S - 1) / g.S + 1) & ~1;
+      const int p0 = slice * len;
+      const int p1 = min(d.z, p0 + len);
+      const int m2 = p1 > p0 ? (p1 - p0 + 1) >> 1 : 0;
+      const float4* cp = pts_at(st) + (p0 >> 1);
+      // software-pipelined by one point pair: the next LDS.128 is in flight
+      // while the current pair is scored (the read past the slice stays
+      // inside the shared allocation and is discarded)
+      float4 v = cp[0];
+#pragma unroll 1
+      for (int q2 = 0; q2 < m2; ++q2) {
+        const float4 vn = cp[q2 + 1];
+#pragma unroll
+        for (int pr = 0; pr < kNH / 2; ++pr) {
+          float2 e = __ffma2_rn(A[pr], make_float2(v.x, v.x),
+                                __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
+          float2 gg = __ffma2_rn(e, e, T2[pr]);
+          cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
+          cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
+          e = __ffma2_rn(A[pr], make_float2(v.z, v.z),
+                         __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
+          gg = __ffma2_rn(e, e, T2[pr]);
+          cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
+          cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
+        }
+        v = vn;
+      }
+    }
+    // stage st consumed by this warp; the last warp refills it
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&sh.done[st], 1) == warps - 1) {
+        sh.done[st] = 0;
+        __threadfence_block();
+        fetch(st);
+      }
+    }
+    if (active) {
+      int32_t* up = upper + (static_cast<int64_t>(d.x) * g.Tg + d.w + j) * 8;
+#pragma unroll
+      for (int q = 0; q < kNH; ++q)
+        if (cnt[q]) atomicAdd(&up[q], static_cast<int32_t>(cnt[q]));
     }
   }
-  if (!valid) return;
-  int32_t* up = upper + static_cast<int64_t>(c) * T + t0;
-#pragma unroll
-  for (int q = 0; q < kNH; ++q)
-    if (t0 + q < T && cnt[q]) atomicAdd(&up[q], static_cast<int32_t>(cnt[q]));
 }
 
 // ----------------------------------------------------------- select kernel
@@ -683,9 +906,9 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double4 st = stat[c];
   double thr_lo = st.x, thr_hi = st.y;
-  const float2* p32 = xy32 + b;
+  const float2* p32 = xy32 + xy32_base(offsets, c);
   const double2* p64 = xy64 + b;
-  const int32_t* U = upper + static_cast<int64_t>(c) * T;
+  const int32_t* U = upper + static_cast<int64_t>(c) * ((T + 7) / 8) * 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
   // Switches the whole block to the exact sequential threshold (rare).
@@ -810,7 +1033,7 @@ exact_counts_kernel(const int64_t* __restrict__ offsets, const int32_t* __restri
   for (int t = warp; t < T; t += nw) {
     const ExactHyp H = make_exact(xy64 + b, seed, key, static_cast<uint32_t>(t), n, th, th);
     bool und;
-    const int e = warp_exact_count(H, n, xy32 + b, xy64 + b, th, th, &und);
+    const int e = warp_exact_count(H, n, xy32 + xy32_base(offsets, c), xy64 + b, th, th, &und);
     if ((threadIdx.x & 31) == 0) counts[static_cast<int64_t>(c) * T + t] = e;
   }
 }
@@ -848,27 +1071,48 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
   count_launch();
 }
 
-void launch_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
-                 cudaStream_t st) {
+void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                      cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const int T = p.max_trials;
-  const int64_t total = static_cast<int64_t>(f.n_clusters) * T;
-  hyp_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-      f.n_clusters, f.offsets, s.xy64, s.stat, f.keys, T, p.rng_seed, s.hyp, s.upper);
-  count_launch();
-  tile_plan_kernel<<<1, 1024, 0, st>>>(f.n_clusters, f.offsets, T, s.tile_start);
+  const ScoreGeom g = score_geom(p.max_trials);
+  cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  prep_hyp_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(
+      f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
+      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap);
   count_launch();
 }
+
+namespace {
+// Persistent grid: every SM filled to the occupancy the tile's shared memory
+// allows (queried once per shared-memory size).
+int score_grid(const ScoreGeom& g, int64_t max_tiles) {
+  static int sms = 0;
+  static size_t cached_smem = 0;
+  static int per_sm = 0;
+  const size_t smem = score_smem_bytes(g);
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(score_smem_bytes(score_geom(1 << 20))));
+  }
+  if (smem != cached_smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, smem);
+    cached_smem = smem;
+  }
+  const int64_t grid = static_cast<int64_t>(sms) * std::max(per_sm, 1);
+  return static_cast<int>(std::max<int64_t>(1, std::min(grid, max_tiles)));
+}
+}  // namespace
 
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const int T = p.max_trials;
-  // grid bound: sum_c ceil(G * nch_c / 128) <= G * (P / kPT + C) / 128 + C
-  const int64_t G = std::max<int64_t>((T + kNH - 1) / kNH, kNH);
-  const int64_t bound = (G * (f.n_points / kPT + f.n_clusters)) / kScoreThreads + f.n_clusters + 1;
-  score_kernel<<<static_cast<unsigned>(bound), kScoreThreads, 0, st>>>(
-      f.n_clusters, f.offsets, s.xy32, s.hyp, s.tile_start, T, s.upper);
+  const ScoreGeom g = score_geom(p.max_trials);
+  const int64_t max_tiles = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
+  score_kernel<<<score_grid(g, max_tiles), kScoreThreads, score_smem_bytes(g), st>>>(
+      s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
   count_launch();
 }
 

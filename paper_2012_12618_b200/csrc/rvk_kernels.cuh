@@ -23,14 +23,49 @@ struct FrameDev {
   int64_t frame_id = 0;
 };
 
+// Scoring geometry for a given max_trials T (host and device agree on it).
+// Hypotheses are processed in groups of 8 (one scoring thread each); a
+// scoring CTA of kScoreThreads threads covers TS groups x S point slices.
+constexpr int kScoreThreads = 256;
+constexpr int kScorePPT = 512;                   // points per scoring tile (max)
+constexpr int kTileBuckets = kScorePPT / 8 + 1;   // 0: full tiles; 1..64: by size, descending
+
+struct ScoreGeom {
+  int T = 0;    // max_trials
+  int Tg = 0;   // hypothesis groups of 8 per cluster
+  int TS = 0;   // groups per tile (power of two <= kScoreThreads)
+  int S = 0;    // point slices per tile = kScoreThreads / TS
+  int nhb = 0;  // hypothesis blocks per cluster = ceil(Tg / TS)
+};
+
+inline __host__ __device__ ScoreGeom score_geom(int T) {
+  ScoreGeom g;
+  g.T = T;
+  g.Tg = (T + 7) / 8;
+  int ts = 1;
+  while (ts < g.Tg && ts < kScoreThreads) ts <<= 1;
+  g.TS = ts;
+  g.S = kScoreThreads / ts;
+  g.nhb = (g.Tg + ts - 1) / ts;
+  return g;
+}
+
+// Capacity of one tile bucket: bounds the total tile count of a frame.
+inline int64_t tile_capacity(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
+  return static_cast<int64_t>(g.nhb) * (n_points / kScorePPT + n_clusters) + 1;
+}
+
 struct Scratch {
   double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
-  float2* xy32 = nullptr;    // [P] normalized (x, y), FP32
+  float2* xy32 = nullptr;    // [P + 2C + 2] normalized (x, y), FP32, each cluster
+                             // starting at an even index, odd sizes padded
   double4* stat = nullptr;   // [C] (thr_lo, thr_hi, median, thr_exact|NaN)
   double* norm = nullptr;    // [4C] (offset_az, offset_dop, scale_az, scale_dop)
-  int32_t* upper = nullptr;  // [C*T] fast-pass upper-bound counts
-  float4* hyp = nullptr;     // [C*T] (A, B, C, -t2hi) per hypothesis
-  int32_t* tile_start = nullptr;  // [C+1] scoring tile plan
+  int32_t* upper = nullptr;  // [C*Tg*8] fast-pass upper-bound counts
+  float* hyp = nullptr;      // [C*Tg*32] per group of 8: A[8] B[8] C[8] K[8]
+  int4* tiles = nullptr;     // [kTileBuckets * tile_cap] scoring tile descriptors
+  int32_t* tile_count = nullptr;  // [kTileBuckets + 1] tiles per bucket + claim counter (zeroed per call)
+  int64_t tile_cap = 0;
 };
 
 struct Outputs {
@@ -47,9 +82,10 @@ void launch_prep(const FrameDev& f, double threshold_scale, const Scratch& s, cu
 // Exact (left-to-right) MAD threshold into stat[c].w (and .x = .y).
 void launch_mad_exact(const FrameDev& f, double threshold_scale, const Scratch& s,
                       cudaStream_t st);
-// Hypothesis setup (seed pairs, FP64 lines, FP32 coefficients) + tile plan.
-void launch_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
-                 cudaStream_t st);
+// normalize + median + MAD + hypothesis setup (seed pairs, FP64 lines, FP32
+// coefficients) + scoring-tile registration, one CTA per cluster.
+void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                      cudaStream_t st);
 // Fast FP32 scoring: upper-bound inlier counts for every (cluster, trial).
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);

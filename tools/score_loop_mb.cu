@@ -1,0 +1,161 @@
+// Scoring inner-loop shapes (development microbenchmark, not shipped).
+// Each variant: 8 hypotheses per thread, points broadcast from shared
+// memory, squared corridor compare, sign-bit counting; only the code shape
+// (operand layout / instruction order) differs.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o tools/score_loop_mb tools/score_loop_mb.cu
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
+
+constexpr int kPts = 2048;
+__device__ __forceinline__ uint32_t hsh(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352d; x ^= x >> 15; x *= 0x846ca68b; x ^= x >> 16; return x;
+}
+__device__ __forceinline__ float u01(uint32_t x) { return (hsh(x) >> 8) * (1.0f / 16777216.0f); }
+
+struct Hy { float2 A[4], B[4], C[4], T[4]; };
+__device__ __forceinline__ void init_h(Hy& h, uint32_t base) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t s = base + q * 8u;
+    h.A[q] = make_float2(u01(s) - 0.5f, u01(s + 1) - 0.5f);
+    h.B[q] = make_float2(0.8f + 0.1f * u01(s + 2), 0.8f + 0.1f * u01(s + 3));
+    h.C[q] = make_float2(-0.4f * u01(s + 4), -0.4f * u01(s + 5));
+    const float t = 0.05f + 0.1f * u01(s + 6);
+    h.T[q] = make_float2(-t * t, -t * t);
+  }
+}
+
+// V=0: per point, per pair: B-step, A-step, square (production shape)
+// V=1: per point pair: all B-steps, then all A-steps, then squares
+// V=2: point-pair packing: smem float4 (x1,x2,y1,y2); hypothesis scalars
+template <int V, int TH, int MINB, int UNR>
+__global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
+  __shared__ float4 pts[kPts / 2];
+  for (int i = threadIdx.x; i < kPts / 2; i += blockDim.x) {
+    const uint32_t s = blockIdx.x * 7919u + i * 4u;
+    pts[i] = make_float4(u01(s), u01(s + 1), u01(s + 2), u01(s + 3));
+  }
+  Hy h;
+  init_h(h, (blockIdx.x * TH + threadIdx.x) * 64u);
+  uint32_t cnt[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) cnt[q] = 0;
+  __syncthreads();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll UNR
+    for (int i = 0; i < kPts / 2; ++i) {
+      const float4 v = pts[i];
+      if (V == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 e = __ffma2_rn(h.A[q], make_float2(v.x, v.x), __ffma2_rn(h.B[q], make_float2(v.y, v.y), h.C[q]));
+          float2 g = __ffma2_rn(e, e, h.T[q]);
+          cnt[2 * q] += __float_as_uint(g.x) >> 31; cnt[2 * q + 1] += __float_as_uint(g.y) >> 31;
+          e = __ffma2_rn(h.A[q], make_float2(v.z, v.z), __ffma2_rn(h.B[q], make_float2(v.w, v.w), h.C[q]));
+          g = __ffma2_rn(e, e, h.T[q]);
+          cnt[2 * q] += __float_as_uint(g.x) >> 31; cnt[2 * q + 1] += __float_as_uint(g.y) >> 31;
+        }
+      } else if (V == 1) {
+        float2 t0[4], t1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t0[q] = __ffma2_rn(h.B[q], make_float2(v.y, v.y), h.C[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t1[q] = __ffma2_rn(h.B[q], make_float2(v.w, v.w), h.C[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t0[q] = __ffma2_rn(h.A[q], make_float2(v.x, v.x), t0[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t1[q] = __ffma2_rn(h.A[q], make_float2(v.z, v.z), t1[q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 g0 = __ffma2_rn(t0[q], t0[q], h.T[q]);
+          const float2 g1 = __ffma2_rn(t1[q], t1[q], h.T[q]);
+          cnt[2 * q] += (__float_as_uint(g0.x) >> 31) + (__float_as_uint(g1.x) >> 31);
+          cnt[2 * q + 1] += (__float_as_uint(g0.y) >> 31) + (__float_as_uint(g1.y) >> 31);
+        }
+      } else {
+        // v = (x1, x2, y1, y2)
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float a = hh ? h.A[q].y : h.A[q].x, b = hh ? h.B[q].y : h.B[q].x;
+            const float c = hh ? h.C[q].y : h.C[q].x, t = hh ? h.T[q].y : h.T[q].x;
+            const float2 e = __ffma2_rn(X, make_float2(a, a), __ffma2_rn(Y, make_float2(b, b), make_float2(c, c)));
+            const float2 g = __ffma2_rn(e, e, make_float2(t, t));
+            cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+          }
+        }
+      }
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += cnt[q] * (q + 1);
+  out[blockIdx.x * TH + threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) ffma3_peak(int iters, float m, float c, float* out) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = 1.0f + i + threadIdx.x;
+  for (int k = 0; k < iters; ++k)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = __fmaf_rn(a[i], m, c);
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i];
+  if (s == 1.2345f) out[0] = s;
+}
+
+template <class F> float time_ms(F f) {
+  cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+  f(); CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int i = 0; i < 3; ++i) {
+    CK(cudaEventRecord(a)); f(); CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    float t; CK(cudaEventElapsedTime(&t, a, b)); best = t < best ? t : best;
+  }
+  return best;
+}
+
+template <int V, int TH, int MINB, int UNR>
+void run(int sms, double peak, uint32_t* d) {
+  int per = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, loop_mb<V, TH, MINB, UNR>, TH, 0));
+  const int blocks = sms * per * 4, reps = 4;
+  const float ms = time_ms([&] { loop_mb<V, TH, MINB, UNR><<<blocks, TH>>>(reps, d); });
+  CK(cudaGetLastError());
+  const double ev = double(blocks) * TH * 8 * kPts * reps;
+  const double rate = ev / (ms * 1e-3);
+  cudaFuncAttributes fa; CK(cudaFuncGetAttributes(&fa, loop_mb<V, TH, MINB, UNR>));
+  printf("{\"V\": %d, \"threads\": %d, \"minb\": %d, \"unroll\": %d, \"regs\": %d, \"ctas_per_sm\": %d, "
+         "\"evals_per_s\": %.4e, \"frac_of_ffma_peak\": %.3f}\n",
+         V, TH, MINB, UNR, fa.numRegs, per, rate, rate * 4 / peak);
+}
+
+int main() {
+  int sms = 0; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  float* df; uint32_t* du;
+  CK(cudaMalloc(&df, 1024)); CK(cudaMalloc(&du, sizeof(uint32_t) * sms * 64 * 1024));
+  const int pb = sms * 8, iters = 20000;
+  const float mp = time_ms([&] { ffma3_peak<<<pb, 256>>>(iters, 0.9999f, 1e-7f, df); });
+  const double peak = double(pb) * 256 * iters * 16 * 2 / (mp * 1e-3);
+  printf("{\"ffma_peak_tflops\": %.2f}\n", peak / 1e12);
+  run<0, 256, 2, 2>(sms, peak, du);
+  run<0, 256, 3, 2>(sms, peak, du);
+  run<0, 256, 2, 4>(sms, peak, du);
+  run<0, 128, 6, 2>(sms, peak, du);
+  run<0, 128, 4, 1>(sms, peak, du);
+  run<1, 256, 2, 2>(sms, peak, du);
+  run<1, 256, 3, 1>(sms, peak, du);
+  run<2, 256, 2, 2>(sms, peak, du);
+  run<2, 256, 3, 2>(sms, peak, du);
+  run<2, 128, 4, 2>(sms, peak, du);
+  return 0;
+}

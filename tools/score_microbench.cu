@@ -208,6 +208,77 @@ void run(const char* name, int blocks, double peak_flops, uint32_t* d_out) {
          name, V, NH, blocks, ms, rate, rate * 4 / 1e12, rate * 4 / peak_flops);
 }
 
+// Correct per-hypothesis counting with a mix of the two compare forms over a
+// point pair (v.xy, v.zw): pairs q < NF use the squared FFMA2 compare +
+// LEA.HI sign accumulate; pairs q >= NF use FSET(|e| <= t) on both points and
+// one IADD3 per hypothesis (cnt - s0 - s1).
+template <int NF>
+__global__ void __launch_bounds__(256) score_mix(int n, int reps, uint32_t* out) {
+  __shared__ float4 pts[kPts / 2];
+  for (int i = threadIdx.x; i < kPts / 2; i += blockDim.x) {
+    const uint32_t s = blockIdx.x * 7919u + i * 4u;
+    pts[i] = make_float4(u01(s), u01(s + 1), u01(s + 2), u01(s + 3));
+  }
+  constexpr int NP = 4;
+  float2 A[NP], B[NP], Cc[NP], K[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    const uint32_t s = (blockIdx.x * 256 + threadIdx.x) * 64u + q * 8u;
+    A[q] = make_float2(u01(s) - 0.5f, u01(s + 1) - 0.5f);
+    B[q] = make_float2(0.8f + 0.1f * u01(s + 2), 0.8f + 0.1f * u01(s + 3));
+    Cc[q] = make_float2(-0.4f * u01(s + 4), -0.4f * u01(s + 5));
+    const float t = 0.05f + 0.1f * u01(s + 6);
+    K[q] = q < NF ? make_float2(-t * t, -t * t) : make_float2(t, t);
+  }
+  uint32_t cnt[2 * NP];
+#pragma unroll
+  for (int q = 0; q < 2 * NP; ++q) cnt[q] = 0;
+  __syncthreads();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 2
+    for (int i = 0; i < n / 2; ++i) {
+      const float4 v = pts[i];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const float2 e0 = __ffma2_rn(A[q], make_float2(v.x, v.x),
+                                     __ffma2_rn(B[q], make_float2(v.y, v.y), Cc[q]));
+        const float2 e1 = __ffma2_rn(A[q], make_float2(v.z, v.z),
+                                     __ffma2_rn(B[q], make_float2(v.w, v.w), Cc[q]));
+        if (q < NF) {
+          const float2 g0 = __ffma2_rn(e0, e0, K[q]);
+          const float2 g1 = __ffma2_rn(e1, e1, K[q]);
+          cnt[2 * q] += (__float_as_uint(g0.x) >> 31) + (__float_as_uint(g1.x) >> 31);
+          cnt[2 * q + 1] += (__float_as_uint(g0.y) >> 31) + (__float_as_uint(g1.y) >> 31);
+        } else {
+          uint32_t a0, a1, b0, b1;
+          asm("set.le.u32.f32 %0, %1, %2;" : "=r"(a0) : "f"(fabsf(e0.x)), "f"(K[q].x));
+          asm("set.le.u32.f32 %0, %1, %2;" : "=r"(a1) : "f"(fabsf(e1.x)), "f"(K[q].x));
+          asm("set.le.u32.f32 %0, %1, %2;" : "=r"(b0) : "f"(fabsf(e0.y)), "f"(K[q].y));
+          asm("set.le.u32.f32 %0, %1, %2;" : "=r"(b1) : "f"(fabsf(e1.y)), "f"(K[q].y));
+          cnt[2 * q] = cnt[2 * q] - a0 - a1;
+          cnt[2 * q + 1] = cnt[2 * q + 1] - b0 - b1;
+        }
+      }
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < 2 * NP; ++q) s += cnt[q] * (q + 1);
+  out[blockIdx.x * 256 + threadIdx.x] = s;
+}
+
+template <int NF>
+void run_mix(const char* name, int blocks, double peak_flops, uint32_t* d_out) {
+  const int n = kPts, reps = 8;
+  const float ms = time_ms([&] { score_mix<NF><<<blocks, 256>>>(n, reps, d_out); });
+  CK(cudaGetLastError());
+  const double evals = double(blocks) * 256 * 8 * n * reps;
+  const double rate = evals / (ms * 1e-3);
+  printf("{\"variant\": \"%s\", \"NF\": %d, \"blocks\": %d, \"ms\": %.3f, "
+         "\"evals_per_s\": %.4e, \"tflops_4_per_eval\": %.2f, \"frac_of_peak\": %.3f}\n",
+         name, NF, blocks, ms, rate, rate * 4 / 1e12, rate * 4 / peak_flops);
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -224,6 +295,14 @@ int main() {
   const double alu = double(pb) * 256 * iters * 16 / (ms_a * 1e-3);
   printf("{\"sms\": %d, \"ffma_imm_tflops\": %.2f, \"ffma_3reg_tflops\": %.2f, "
          "\"alu_xor_shr_add_gops\": %.1f}\n", sms, peak / 1e12, peak3 / 1e12, alu / 1e9);
+  for (int waves : {3, 6}) {
+    const int blocks = sms * waves;
+    run_mix<4>("mix_sq4_fset0", blocks, peak, d_u);
+    run_mix<3>("mix_sq3_fset1", blocks, peak, d_u);
+    run_mix<2>("mix_sq2_fset2", blocks, peak, d_u);
+    run_mix<1>("mix_sq1_fset3", blocks, peak, d_u);
+    run_mix<0>("mix_sq0_fset4", blocks, peak, d_u);
+  }
   for (int waves : {6}) {
     const int blocks = sms * waves;
     run<0, 8>("ffma2_all", blocks, peak, d_u);
