@@ -67,12 +67,6 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
   return r;
 }
 
-struct MinOp {
-  __device__ double operator()(double a, double b) const { return b < a ? b : a; }
-};
-struct MaxOp {
-  __device__ double operator()(double a, double b) const { return b > a ? b : a; }
-};
 struct SumI {
   __device__ int operator()(int a, int b) const { return a + b; }
 };
@@ -223,6 +217,7 @@ __device__ __forceinline__ int med_bin(unsigned long long key) {
 
 struct PrepShared {
   unsigned long long keys[kSortCap];  // normalized dopplers (bit patterns, sign cleared)
+  double xs[kSortCap];                // normalized azimuths
   unsigned long long cand[kCandCap];
   unsigned int hist[kMedBins];
   double red[32];
@@ -417,8 +412,10 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
     p32[k] = make_float2(__double2float_rn(x), __double2float_rn(y));
     // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
     // std::sort's operator< treats them; every other value is >= +0)
-    if (in_smem)
+    if (in_smem) {
       sm.keys[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
+      sm.xs[k] = x;
+    }
   }
   if (threadIdx.x == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);  // pad to even
   if (threadIdx.x == 0 && norm != nullptr) {
@@ -508,8 +505,14 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     if (t < g.T) {
       int i, j;
       seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-      const double2 p = p64[i];
-      const double2 q = p64[j];
+      double2 p, q;
+      if (n <= kSortCap) {  // normalized points are still in shared memory (y >= +0)
+        p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
+        q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
+      } else {
+        p = p64[i];
+        q = p64[j];
+      }
       f = make_fast_from_seeds(p.x, p.y, q.x, q.y, thr_lo, thr_hi);
     }
     float* h = hc + (t >> 3) * 32 + (t & 7);
@@ -620,7 +623,7 @@ __host__ __device__ __forceinline__ size_t score_smem_bytes(const ScoreGeom& g) 
 // and the sign bit of g added to the count (LEA.HI). Counts are upper bounds
 // (guard band, see make_fast) and accumulate over tiles with integer atomics
 // (order-free, deterministic).
-__global__ void __launch_bounds__(kScoreThreads, 2)
+__global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
              ScoreGeom g, int32_t* __restrict__ upper) {
@@ -716,13 +719,10 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
       const int p1 = min(d.z, p0 + len);
       const int m2 = p1 > p0 ? (p1 - p0 + 1) >> 1 : 0;
       const float4* cp = pts_at(st) + (p0 >> 1);
-      // software-pipelined by one point pair: the next LDS.128 is in flight
-      // while the current pair is scored (the read past the slice stays
-      // inside the shared allocation and is discarded)
-      float4 v = cp[0];
-#pragma unroll 1
-      for (int q2 = 0; q2 < m2; ++q2) {
-        const float4 vn = cp[q2 + 1];
+      // software-pipelined, two point pairs per iteration: the LDS.128 of
+      // the next pair is in flight while the current one is scored (reads
+      // past the slice stay inside the shared allocation and are unused)
+      auto score_pair = [&](const float4& v) {
 #pragma unroll
         for (int pr = 0; pr < kNH / 2; ++pr) {
           float2 e = __ffma2_rn(A[pr], make_float2(v.x, v.x),
@@ -736,8 +736,17 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
           cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
           cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
         }
-        v = vn;
+      };
+      float4 v0 = cp[0];
+      int q2 = 0;
+#pragma unroll 1
+      for (; q2 + 2 <= m2; q2 += 2) {
+        const float4 v1 = cp[q2 + 1];
+        score_pair(v0);
+        v0 = cp[q2 + 2];
+        score_pair(v1);
       }
+      if (q2 < m2) score_pair(v0);
     }
     // stage st consumed by this warp; the last warp refills it
     __syncwarp();
@@ -780,20 +789,16 @@ __device__ int warp_exact_count(const ExactHyp& H, int n, const float2* __restri
 // LSQ refit + heading of one cluster (estimate_cluster_velocity,
 // src/velocity.cpp:26-90; solve_velocity / min_norm_fallback,
 // include/rvk/velocity.hpp:46-105; heading_angle velocity.cpp:19-24).
-// Reductions use a fixed tree, so results are deterministic; they differ
-// from Eigen's reduction order only in the last bits (tolerance-checked).
-// `mask` may have been written earlier in the same kernel: no __restrict__.
-__device__ void block_refit(int n, const double* __restrict__ az, const double* __restrict__ dop,
-                            const uint8_t* mask, int64_t frame_id, int cluster_id,
-                            rvk_estimate* __restrict__ out, double* red) {
-  __shared__ int redi[32];
+// Each thread accumulates the normal-equation sums of its inliers
+// (RefitAcc::add); one fused block reduction with a fixed tree follows, so
+// results are deterministic; they differ from Eigen's reduction order only
+// in the last bits (tolerance-checked).
+struct RefitAcc {
   double g00 = 0, g01 = 0, g11 = 0, b0 = 0, b1 = 0, ds = 0;
   int nin = 0, first = INT_MAX;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    if (!mask[k]) continue;
+  __device__ __forceinline__ void add(int k, double a, double d) {
     double s, c;
-    sincos(az[k], &s, &c);
-    const double d = dop[k];
+    sincos(a, &s, &c);
     g00 += c * c;
     g01 += c * s;
     g11 += s * s;
@@ -803,15 +808,69 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
     ++nin;
     first = k < first ? k : first;
   }
-  nin = block_reduce(nin, SumI(), redi);
-  first = block_reduce(first, MinI(), redi);
-  g00 = block_reduce(g00, SumD(), red);
-  g01 = block_reduce(g01, SumD(), red);
-  g11 = block_reduce(g11, SumD(), red);
-  b0 = block_reduce(b0, SumD(), red);
-  b1 = block_reduce(b1, SumD(), red);
-  ds = block_reduce(ds, SumD(), red);
-  if (threadIdx.x != 0) return;
+};
+
+struct RefitShared {
+  double v[kSelectThreads / 32][6];
+  int i[kSelectThreads / 32][2];
+};
+
+// Block-wide sum of the accumulators; the total is valid in thread 0.
+__device__ RefitAcc block_reduce_refit(RefitAcc a, RefitShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a.g00 += __shfl_xor_sync(0xffffffffu, a.g00, o);
+    a.g01 += __shfl_xor_sync(0xffffffffu, a.g01, o);
+    a.g11 += __shfl_xor_sync(0xffffffffu, a.g11, o);
+    a.b0 += __shfl_xor_sync(0xffffffffu, a.b0, o);
+    a.b1 += __shfl_xor_sync(0xffffffffu, a.b1, o);
+    a.ds += __shfl_xor_sync(0xffffffffu, a.ds, o);
+    a.nin += __shfl_xor_sync(0xffffffffu, a.nin, o);
+    a.first = min(a.first, __shfl_xor_sync(0xffffffffu, a.first, o));
+  }
+  __syncthreads();  // sh may still be read by a previous reduction
+  if (lane == 0) {
+    sh.v[warp][0] = a.g00;
+    sh.v[warp][1] = a.g01;
+    sh.v[warp][2] = a.g11;
+    sh.v[warp][3] = a.b0;
+    sh.v[warp][4] = a.b1;
+    sh.v[warp][5] = a.ds;
+    sh.i[warp][0] = a.nin;
+    sh.i[warp][1] = a.first;
+  }
+  __syncthreads();
+  RefitAcc t;
+  if (threadIdx.x == 0) {
+    t.g00 = sh.v[0][0];
+    t.g01 = sh.v[0][1];
+    t.g11 = sh.v[0][2];
+    t.b0 = sh.v[0][3];
+    t.b1 = sh.v[0][4];
+    t.ds = sh.v[0][5];
+    t.nin = sh.i[0][0];
+    t.first = sh.i[0][1];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      t.g00 += sh.v[w][0];
+      t.g01 += sh.v[w][1];
+      t.g11 += sh.v[w][2];
+      t.b0 += sh.v[w][3];
+      t.b1 += sh.v[w][4];
+      t.ds += sh.v[w][5];
+      t.nin += sh.i[w][0];
+      t.first = min(t.first, sh.i[w][1]);
+    }
+  }
+  return t;
+}
+
+// Thread 0: the 2x2 solve, fallback and heading from the reduced sums.
+__device__ void finish_refit(const RefitAcc& a, const double* __restrict__ az,
+                             const double* __restrict__ dop, int64_t frame_id, int cluster_id,
+                             rvk_estimate* __restrict__ out) {
+  const double g00 = a.g00, g01 = a.g01, g11 = a.g11, b0 = a.b0, b1 = a.b1;
+  const int nin = a.nin, first = a.first;
   rvk_estimate e;
   e.frame_id = frame_id;
   e.cluster_id = cluster_id;
@@ -864,7 +923,7 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
         u0 = -u0;
         u1 = -u1;
       }
-      const double mean = ds / nin;
+      const double mean = a.ds / nin;
       e.v_x = mean * u0;
       e.v_y = mean * u1;
       e.condition_ok = 0;
@@ -878,14 +937,27 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
   *out = e;
 }
 
+// estimate_cluster_velocity on a mask in memory.
+__device__ void block_refit(int n, const double* __restrict__ az, const double* __restrict__ dop,
+                            const uint8_t* mask, int64_t frame_id, int cluster_id,
+                            rvk_estimate* __restrict__ out, RefitShared& sh) {
+  RefitAcc acc;
+  for (int k = threadIdx.x; k < n; k += blockDim.x)
+    if (mask[k]) acc.add(k, az[k], dop[k]);
+  const RefitAcc t = block_reduce_refit(acc, sh);
+  if (threadIdx.x == 0) finish_refit(t, az, dop, frame_id, cluster_id, out);
+}
+
 // Exact winner per cluster (one CTA). With U = the fast pass's upper bounds
 // (exact[t] <= U[t]), t0 = the lowest trial with the largest U and
 // E0 = exact[t0], a trial t can only beat or tie-win against t0 if
 // U[t] > E0, or U[t] == E0 and t < t0 (ties go to the lowest trial,
 // src/ransac.cpp:181-189). Only those are verified; when U[t0] == E0 there
-// are none. Then the winner's mask (evaluate_trial, :274-281) and the LSQ
-// refit on its inliers.
-__global__ void __launch_bounds__(kSelectThreads)
+// are none. One pass over the points classifies them for t0 exactly, writes
+// the mask (evaluate_trial, :129-136) and accumulates the LSQ refit sums of
+// its inliers; only if another trial wins (or a distance fell inside the
+// threshold interval) is the pass repeated.
+__global__ void __launch_bounds__(kSelectThreads, 3)
 select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
               const double* __restrict__ dop, const int32_t* __restrict__ keys,
               const int32_t* __restrict__ cluster_ids, int64_t frame_id,
@@ -895,8 +967,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
               int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
               rvk_estimate* __restrict__ est) {
   __shared__ unsigned long long redu[32];
-  __shared__ int redi[32];
-  __shared__ double redd[32];
+  __shared__ RefitShared rsh;
   __shared__ unsigned long long best;
   __shared__ double sh_thr;
   __shared__ int sh_need_exact;
@@ -908,14 +979,42 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   double thr_lo = st.x, thr_hi = st.y;
   const float2* p32 = xy32 + xy32_base(offsets, c);
   const double2* p64 = xy64 + b;
+  const double* caz = az + b;
+  const double* cdop = dop + b;
+  uint8_t* cmask = mask + b;
   const int32_t* U = upper + static_cast<int64_t>(c) * ((T + 7) / 8) * 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool refit = est != nullptr;
 
   // Switches the whole block to the exact sequential threshold (rare).
   auto go_exact = [&]() {
     if (threadIdx.x == 0) sh_thr = exact_threshold(p64, n, st.z, scale);
     __syncthreads();
     thr_lo = thr_hi = sh_thr;
+  };
+  // One pass for trial t: mask + exact count + refit sums. Returns false if
+  // some distance was undecided (then nothing is valid and the caller
+  // switches to the exact threshold).
+  auto pass = [&](int t, int& count, RefitAcc& total) -> bool {
+    const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
+    RefitAcc acc;
+    bool und = false;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int d = H.L.degenerate ? kOut : classify(H, k, p32[k], p64, thr_lo, thr_hi);
+      und |= d == kUndecided;
+      cmask[k] = d == kIn ? 1 : 0;
+      if (d == kIn) {
+        if (refit) acc.add(k, caz[k], cdop[k]);
+        else ++acc.nin;
+      }
+    }
+    if (__syncthreads_or(und)) return false;
+    total = block_reduce_refit(acc, rsh);
+    if (threadIdx.x == 0) redu[0] = static_cast<unsigned long long>(total.nin);
+    __syncthreads();
+    count = static_cast<int>(redu[0]);
+    __syncthreads();
+    return true;
   };
 
   // 1. trial with the largest upper bound (lowest index on ties).
@@ -925,24 +1024,12 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   const int t0 = unpack_trial(v);
   const int u0 = unpack_count(v);
 
-  // 2. its exact count.
+  // 2. its exact count, mask and refit sums in one pass.
   int e0 = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const ExactHyp H0 = make_exact(p64, seed, key, static_cast<uint32_t>(t0), n, thr_lo, thr_hi);
-    int cnt = 0;
-    bool und = false;
-    if (!H0.L.degenerate)
-      for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const int d = classify(H0, k, p32[k], p64, thr_lo, thr_hi);
-        cnt += d == kIn;
-        und |= d == kUndecided;
-      }
-    if (__syncthreads_or(und)) {
-      go_exact();
-      continue;
-    }
-    e0 = block_reduce(cnt, SumI(), redi);
-    break;
+  RefitAcc tot;
+  if (!pass(t0, e0, tot)) {
+    go_exact();
+    pass(t0, e0, tot);
   }
   if (threadIdx.x == 0) {
     best = pack_best(e0, t0);
@@ -952,7 +1039,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
 
   // 3. verify the trials that could still win (none when u0 == e0).
   if (u0 > e0) {
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int round = 0; round < 2; ++round) {
       for (int t = warp; t < T; t += nw) {
         const int u = U[t];
         if (t == t0 || u < e0 || (u == e0 && t > t0)) continue;
@@ -965,9 +1052,12 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
           atomicMax(&best, pack_best(e, t));
         }
       }
-      if (__syncthreads_or(sh_need_exact) && pass == 0) {
-        go_exact();  // redo every candidate with the exact threshold
+      if (__syncthreads_or(sh_need_exact) && round == 0) {
+        go_exact();  // redo every candidate (and t0) with the exact threshold
         if (threadIdx.x == 0) sh_need_exact = 0;
+        __syncthreads();
+        pass(t0, e0, tot);
+        if (threadIdx.x == 0) best = pack_best(e0, t0);
         __syncthreads();
         continue;
       }
@@ -978,43 +1068,32 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   const int win = unpack_trial(best);
   const int win_count = unpack_count(best);
 
-  // 4. winner mask (evaluate_trial, src/ransac.cpp:129-136).
-  for (int pass = 0; pass < 2; ++pass) {
-    const ExactHyp W = make_exact(p64, seed, key, static_cast<uint32_t>(win), n, thr_lo, thr_hi);
-    bool und = false;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-      const int d = W.L.degenerate ? kOut : classify(W, k, p32[k], p64, thr_lo, thr_hi);
-      und |= d == kUndecided;
-      mask[b + k] = d == kIn ? 1 : 0;
-    }
-    if (__syncthreads_or(und)) {
+  // 4. another trial won: its mask and refit sums.
+  if (win != t0) {
+    int cnt;
+    if (!pass(win, cnt, tot)) {
       go_exact();
-      continue;
+      pass(win, cnt, tot);
     }
-    break;
   }
   if (threadIdx.x == 0) {
     if (out_count) out_count[c] = win_count;
     if (out_trial) out_trial[c] = win;
+    if (refit)
+      finish_refit(tot, caz, cdop, frame_id, cluster_ids ? cluster_ids[c] : c, est + c);
   }
-  if (est == nullptr) return;
-  __syncthreads();  // mask visible to the whole block
-
-  // 5. LSQ refit on the winning inliers.
-  block_refit(n, az + b, dop + b, mask + b, frame_id, cluster_ids ? cluster_ids[c] : c, est + c,
-              redd);
 }
 
 __global__ void __launch_bounds__(kSelectThreads)
 refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
              const double* __restrict__ dop, const int32_t* __restrict__ cluster_ids,
              int64_t frame_id, const uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
-  __shared__ double redd[32];
+  __shared__ RefitShared rsh;
   const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   block_refit(n, az + b, dop + b, mask + b, frame_id, cluster_ids ? cluster_ids[c] : c, est + c,
-              redd);
+              rsh);
 }
 
 // Exact count of every (cluster, trial) (warp per trial). Requires the exact

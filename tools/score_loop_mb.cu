@@ -77,6 +77,25 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
           cnt[2 * q] += (__float_as_uint(g0.x) >> 31) + (__float_as_uint(g1.x) >> 31);
           cnt[2 * q + 1] += (__float_as_uint(g0.y) >> 31) + (__float_as_uint(g1.y) >> 31);
         }
+      } else if (V == 3) {
+        // hypothesis-pair outer, 4 points inner: the coefficient pairs sit in
+        // the same operand slot of consecutive FFMA2s (operand-reuse cache)
+        const float4 w = pts[(i + 1) & (kPts / 2 - 1)];
+        const float xs[4] = {v.x, v.z, w.x, w.z}, ys[4] = {v.y, v.w, w.y, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 t[4];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) t[p] = __ffma2_rn(h.B[q], make_float2(ys[p], ys[p]), h.C[q]);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) t[p] = __ffma2_rn(h.A[q], make_float2(xs[p], xs[p]), t[p]);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const float2 g = __ffma2_rn(t[p], t[p], h.T[q]);
+            cnt[2 * q] += __float_as_uint(g.x) >> 31; cnt[2 * q + 1] += __float_as_uint(g.y) >> 31;
+          }
+        }
+        ++i;
       } else {
         // v = (x1, x2, y1, y2)
         const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
@@ -148,6 +167,9 @@ int main() {
   const double peak = double(pb) * 256 * iters * 16 * 2 / (mp * 1e-3);
   printf("{\"ffma_peak_tflops\": %.2f}\n", peak / 1e12);
   run<0, 256, 2, 2>(sms, peak, du);
+  run<3, 256, 3, 1>(sms, peak, du);
+  run<3, 256, 2, 1>(sms, peak, du);
+  run<3, 128, 6, 1>(sms, peak, du);
   run<0, 256, 3, 2>(sms, peak, du);
   run<0, 256, 2, 4>(sms, peak, du);
   run<0, 128, 6, 2>(sms, peak, du);
