@@ -8,8 +8,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -102,14 +104,22 @@ struct Context {
   // in flight concurrently; the host API uses `stream`.
   std::unordered_map<cudaStream_t, Workspace> ws;
   Workspace& workspace(cudaStream_t s) { return ws[s]; }
-  // two internal streams for the chunked host pipeline
+  // chunked host pipeline: one copy stream streams every chunk's H2D back
+  // to back; two compute streams take the chunks alternately as they land
+  cudaStream_t copy = nullptr;
   cudaStream_t pipe[2] = {nullptr, nullptr};
-  cudaEvent_t pipe_ev[1] = {nullptr};
-  void ensure_pipe() {
-    if (pipe[0]) return;
-    RVK_CUDA(cudaStreamCreateWithFlags(&pipe[0], cudaStreamNonBlocking));
-    RVK_CUDA(cudaStreamCreateWithFlags(&pipe[1], cudaStreamNonBlocking));
-    RVK_CUDA(cudaEventCreateWithFlags(&pipe_ev[0], cudaEventDisableTiming));
+  std::vector<cudaEvent_t> landed;  // per chunk: its H2D is done
+  void ensure_pipe(int chunks) {
+    if (!copy) {
+      RVK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+      RVK_CUDA(cudaStreamCreateWithFlags(&pipe[0], cudaStreamNonBlocking));
+      RVK_CUDA(cudaStreamCreateWithFlags(&pipe[1], cudaStreamNonBlocking));
+    }
+    while (static_cast<int>(landed.size()) < chunks + 1) {
+      cudaEvent_t e;
+      RVK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      landed.push_back(e);
+    }
   }
 };
 
@@ -308,20 +318,44 @@ bool is_pinned(const void* p) {
 }
 
 // Host API: the frame is split into up to kPipeMax cluster-aligned chunks of
-// >= kPipeChunk points; chunk i runs H2D -> prep -> hyps -> score -> select
-// -> D2H on internal stream i % 2, so the copies of one chunk overlap the
-// kernels of the other. Pinned caller buffers are copied directly (no host
+// >= kPipeChunk points. A copy stream issues every chunk's H2D back to back
+// (PCIe runs at full rate for the whole call); chunk i's kernels (prep+hyps
+// -> score -> select) and its D2H run on compute stream i % 2 once its bytes
+// have landed, so copies and kernels of different chunks overlap. Pinned caller buffers are copied directly (no host
 // staging memcpy); pageable ones go through the context's pinned staging.
 // RNG keys stay frame-positional, so the result does not depend on the
 // chunking.
-constexpr int64_t kPipeChunk = 1 << 17;
-constexpr int kPipeMax = 8;
+constexpr int64_t kPipeChunk = 1 << 18;
+constexpr int kPipeMax = 4;
+
+// Tunables (environment, read once): RVK_PIPE_CHUNK = minimum points per
+// chunk, RVK_PIPE_MAX = maximum number of chunks.
+int64_t env_or(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (v == nullptr || *v == 0) return dflt;
+  const long long x = std::atoll(v);
+  return x > 0 ? x : dflt;
+}
+int64_t pipe_chunk() {
+  static const int64_t v = env_or("RVK_PIPE_CHUNK", kPipeChunk);
+  return v;
+}
+bool trace_on() {
+  static const bool v = env_or("RVK_TRACE", 0) != 0;
+  return v;
+}
+int pipe_max() {
+  static const int v = static_cast<int>(env_or("RVK_PIPE_MAX", kPipeMax));
+  return v;
+}
 
 int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
                          const double* az, const double* dop, const int32_t* ids,
                          const rvk_ransac_params* params, const int32_t* keys,
                          int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
                          rvk_estimate* out, bool refit) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   int st = validate_params(params, "run_ransac");
   if (st != RVK_OK) return st;
   st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
@@ -330,11 +364,10 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   if ((az == nullptr || dop == nullptr) && offsets[n_clusters] > 0)
     return fail(RVK_EINVAL, "run_ransac: null point arrays");
   Context& ctx = context();
-  ctx.ensure_pipe();
   const int64_t P = offsets[n_clusters];
 
   // chunk boundaries (cluster-aligned)
-  int K = static_cast<int>(std::min<int64_t>(kPipeMax, std::max<int64_t>(1, P / kPipeChunk)));
+  int K = static_cast<int>(std::min<int64_t>(pipe_max(), std::max<int64_t>(1, P / pipe_chunk())));
   std::vector<int32_t> cut(1, 0);
   for (int i = 1; i < K; ++i) {
     const int64_t target = P * i / K;
@@ -344,9 +377,11 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   }
   cut.push_back(n_clusters);
   K = static_cast<int>(cut.size()) - 1;
+  ctx.ensure_pipe(K);
 
   const bool pin_in = is_pinned(az) && is_pinned(dop);
   const bool pin_mask = is_pinned(mask);
+  const auto t1 = clk::now();
 
   // device input block: [offsets (rebased per chunk) | keys | ids] + az | dop
   const size_t o_keys = align_up(sizeof(int64_t) * (n_clusters + K));
@@ -376,18 +411,36 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   const OutLayout L(n_clusters, P);
   char* dout = ctx.out.get<char>(L.total);
   char* hout = static_cast<char*>(ctx.stage_out.get(L.total));
-  cudaStream_t s0 = ctx.pipe[0];
-  RVK_CUDA(cudaMemcpyAsync(d, h, small, cudaMemcpyHostToDevice, s0));  // small arrays, once
-  RVK_CUDA(cudaEventRecord(ctx.pipe_ev[0], s0));
-  RVK_CUDA(cudaStreamWaitEvent(ctx.pipe[1], ctx.pipe_ev[0], 0));
+  // all H2D on the copy stream, in chunk order, back to back (RVK_COPY_STREAM=0:
+  // each chunk's H2D on its compute stream instead)
+  const bool copy_stream = env_or("RVK_COPY_STREAM", 1) != 0;
+  cudaStream_t cs = copy_stream ? ctx.copy : ctx.pipe[0];
+  RVK_CUDA(cudaMemcpyAsync(d, h, small, cudaMemcpyHostToDevice, cs));  // small arrays
+  RVK_CUDA(cudaEventRecord(ctx.landed[K], cs));
+  for (int i = 0; copy_stream && i < K; ++i) {
+    const int64_t p0 = offsets[cut[i]], np = offsets[cut[i + 1]] - p0;
+    RVK_CUDA(cudaMemcpyAsync(d + o_az + sizeof(double) * p0, src_az + p0, sizeof(double) * np,
+                             cudaMemcpyHostToDevice, ctx.copy));
+    RVK_CUDA(cudaMemcpyAsync(d + o_dop + sizeof(double) * p0, src_dop + p0, sizeof(double) * np,
+                             cudaMemcpyHostToDevice, ctx.copy));
+    RVK_CUDA(cudaEventRecord(ctx.landed[i], ctx.copy));
+  }
   for (int i = 0; i < K; ++i) {
     cudaStream_t sc = ctx.pipe[i & 1];
+    if (copy_stream) {
+      RVK_CUDA(cudaStreamWaitEvent(sc, ctx.landed[i], 0));
+    } else {
+      if (sc != cs) RVK_CUDA(cudaStreamWaitEvent(sc, ctx.landed[K], 0));
+      const int64_t q0 = offsets[cut[i]], nq = offsets[cut[i + 1]] - q0;
+      RVK_CUDA(cudaMemcpyAsync(d + o_az + sizeof(double) * q0, src_az + q0, sizeof(double) * nq,
+                               cudaMemcpyHostToDevice, sc));
+      RVK_CUDA(cudaMemcpyAsync(d + o_dop + sizeof(double) * q0, src_dop + q0,
+                               sizeof(double) * nq, cudaMemcpyHostToDevice, sc));
+    }
     const int32_t c0 = cut[i], nc = cut[i + 1] - cut[i];
     const int64_t p0 = offsets[c0], np = offsets[cut[i + 1]] - p0;
     char* daz = d + o_az + sizeof(double) * p0;
     char* ddop = d + o_dop + sizeof(double) * p0;
-    RVK_CUDA(cudaMemcpyAsync(daz, src_az + p0, sizeof(double) * np, cudaMemcpyHostToDevice, sc));
-    RVK_CUDA(cudaMemcpyAsync(ddop, src_dop + p0, sizeof(double) * np, cudaMemcpyHostToDevice, sc));
     FrameDev f;
     f.n_clusters = nc;
     f.n_points = np;
@@ -419,12 +472,25 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
       RVK_CUDA(cudaMemcpyAsync(reinterpret_cast<rvk_estimate*>(hout + L.o_est) + c0, o.est,
                                sizeof(rvk_estimate) * nc, cudaMemcpyDeviceToHost, sc));
   }
+  const auto t2 = clk::now();
   RVK_CUDA(cudaStreamSynchronize(ctx.pipe[0]));
   RVK_CUDA(cudaStreamSynchronize(ctx.pipe[1]));
+  const auto t3 = clk::now();
   if (inlier_count) std::memcpy(inlier_count, hout + L.o_cnt, sizeof(int32_t) * n_clusters);
   if (winning_trial) std::memcpy(winning_trial, hout + L.o_tr, sizeof(int32_t) * n_clusters);
   if (mask && !pin_mask) std::memcpy(mask, hout + L.o_mask, P);
   if (out && refit) std::memcpy(out, hout + L.o_est, sizeof(rvk_estimate) * n_clusters);
+  if (trace_on()) {
+    const auto t4 = clk::now();
+    auto us = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    std::fprintf(stderr,
+                 "[rvk trace] P=%lld C=%d chunks=%d pinned_in=%d pinned_mask=%d validate=%.1fus "
+                 "enqueue=%.1fus wait=%.1fus copy_out=%.1fus total=%.1fus\n",
+                 static_cast<long long>(P), n_clusters, K, pin_in, pin_mask, us(t0, t1),
+                 us(t1, t2), us(t2, t3), us(t3, t4), us(t0, t4));
+  }
   return RVK_OK;
 }
 

@@ -26,6 +26,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include <math_constants.h>
 
@@ -41,6 +42,7 @@ namespace {
 constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
 constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
+constexpr int kDefaultIntPairs = 0;  // see score_int_pairs()
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
 constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
@@ -519,7 +521,14 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     h[0] = f.A;
     h[8] = f.B;
     h[16] = f.C;
-    h[24] = -f.t2hi;
+    // K: -t2hi for the squared compare; for the integer compare (the last
+    // g.ni pairs of the group) 2*bits(thi) + 1, or 0 for inert trials
+    if ((t & 7) < 8 - 2 * g.ni) {
+      h[24] = -f.t2hi;
+    } else {
+      const uint32_t kb = f.thi > 0.f ? (__float_as_uint(f.thi) << 1) + 1u : 0u;
+      h[24] = __uint_as_float(kb);
+    }
     uc[t] = 0;
   }
   // scoring tiles of this cluster
@@ -623,6 +632,7 @@ __host__ __device__ __forceinline__ size_t score_smem_bytes(const ScoreGeom& g) 
 // and the sign bit of g added to the count (LEA.HI). Counts are upper bounds
 // (guard band, see make_fast) and accumulate over tiles with integer atomics
 // (order-free, deterministic).
+template <int NI>
 __global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
@@ -722,19 +732,30 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
       // software-pipelined, two point pairs per iteration: the LDS.128 of
       // the next pair is in flight while the current one is scored (reads
       // past the slice stay inside the shared allocation and are unused)
+      // pairs pr < 4 - NI: squared compare (FFMA2) + sign count; the last NI
+      // pairs: integer compare of |e| against thi on the ALU pipe
+      // (sign of 2*bits(e) - (2*bits(thi) + 1)), balancing FMA and ALU work
       auto score_pair = [&](const float4& v) {
 #pragma unroll
         for (int pr = 0; pr < kNH / 2; ++pr) {
-          float2 e = __ffma2_rn(A[pr], make_float2(v.x, v.x),
-                                __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
-          float2 gg = __ffma2_rn(e, e, T2[pr]);
-          cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
-          cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
-          e = __ffma2_rn(A[pr], make_float2(v.z, v.z),
-                         __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
-          gg = __ffma2_rn(e, e, T2[pr]);
-          cnt[2 * pr] += __float_as_uint(gg.x) >> 31;
-          cnt[2 * pr + 1] += __float_as_uint(gg.y) >> 31;
+          float2 e0 = __ffma2_rn(A[pr], make_float2(v.x, v.x),
+                                 __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
+          float2 e1 = __ffma2_rn(A[pr], make_float2(v.z, v.z),
+                                 __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
+          if (pr < kNH / 2 - NI) {
+            e0 = __ffma2_rn(e0, e0, T2[pr]);
+            e1 = __ffma2_rn(e1, e1, T2[pr]);
+            cnt[2 * pr] += __float_as_uint(e0.x) >> 31;
+            cnt[2 * pr + 1] += __float_as_uint(e0.y) >> 31;
+            cnt[2 * pr] += __float_as_uint(e1.x) >> 31;
+            cnt[2 * pr + 1] += __float_as_uint(e1.y) >> 31;
+          } else {
+            const uint32_t k0 = __float_as_uint(T2[pr].x), k1 = __float_as_uint(T2[pr].y);
+            cnt[2 * pr] += ((__float_as_uint(e0.x) << 1) - k0) >> 31;
+            cnt[2 * pr + 1] += ((__float_as_uint(e0.y) << 1) - k1) >> 31;
+            cnt[2 * pr] += ((__float_as_uint(e1.x) << 1) - k0) >> 31;
+            cnt[2 * pr + 1] += ((__float_as_uint(e1.y) << 1) - k1) >> 31;
+          }
         }
       };
       float4 v0 = cp[0];
@@ -1150,10 +1171,20 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
   count_launch();
 }
 
+// Trial pairs per group scored with the integer compare (RVK_SCORE_NI, 0..2).
+int score_int_pairs() {
+  static const int v = [] {
+    const char* e = std::getenv("RVK_SCORE_NI");
+    const int x = e ? std::atoi(e) : kDefaultIntPairs;
+    return x < 0 ? 0 : (x > 2 ? 2 : x);
+  }();
+  return v;
+}
+
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const ScoreGeom g = score_geom(p.max_trials);
+  const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
   cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
   prep_hyp_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
@@ -1164,6 +1195,7 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
 namespace {
 // Persistent grid: every SM filled to the occupancy the tile's shared memory
 // allows (queried once per shared-memory size).
+template <int NI>
 int score_grid(const ScoreGeom& g, int64_t max_tiles) {
   static int sms = 0;
   static size_t cached_smem = 0;
@@ -1173,11 +1205,11 @@ int score_grid(const ScoreGeom& g, int64_t max_tiles) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(score_kernel<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(score_smem_bytes(score_geom(1 << 20))));
   }
   if (smem != cached_smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<NI>, kScoreThreads, smem);
     cached_smem = smem;
   }
   const int64_t grid = static_cast<int64_t>(sms) * std::max(per_sm, 1);
@@ -1188,10 +1220,22 @@ int score_grid(const ScoreGeom& g, int64_t max_tiles) {
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const ScoreGeom g = score_geom(p.max_trials);
+  const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
   const int64_t max_tiles = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
-  score_kernel<<<score_grid(g, max_tiles), kScoreThreads, score_smem_bytes(g), st>>>(
-      s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+  const size_t smem = score_smem_bytes(g);
+  switch (g.ni) {
+    case 1:
+      score_kernel<1><<<score_grid<1>(g, max_tiles), kScoreThreads, smem, st>>>(
+          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+      break;
+    case 2:
+      score_kernel<2><<<score_grid<2>(g, max_tiles), kScoreThreads, smem, st>>>(
+          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+      break;
+    default:
+      score_kernel<0><<<score_grid<0>(g, max_tiles), kScoreThreads, smem, st>>>(
+          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+  }
   count_launch();
 }
 

@@ -36,11 +36,13 @@ struct ScoreGeom {
   int TS = 0;   // groups per tile (power of two <= kScoreThreads)
   int S = 0;    // point slices per tile = kScoreThreads / TS
   int nhb = 0;  // hypothesis blocks per cluster = ceil(Tg / TS)
+  int ni = 0;   // trial pairs (of 4 per group) scored with the integer compare
 };
 
-inline __host__ __device__ ScoreGeom score_geom(int T) {
+inline __host__ __device__ ScoreGeom score_geom(int T, int ni = 0) {
   ScoreGeom g;
   g.T = T;
+  g.ni = ni;
   g.Tg = (T + 7) / 8;
   int ts = 1;
   while (ts < g.Tg && ts < kScoreThreads) ts <<= 1;
