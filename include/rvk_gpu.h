@@ -154,6 +154,38 @@ int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const dou
                            const double* doppler, double threshold_scale, double* norm,
                            double* threshold);
 
+/* Pipelined frame stream: the per-frame loop of the reference's estimate
+ * pipeline (tools/rvk_main.cpp:125-149 -- for each frame, run_ransac then
+ * estimate_all) with up to `depth` frames in flight, so the H2D copy of
+ * frame k+1 overlaps the kernels of frame k and the D2H of frame k-1.
+ * Results are identical to rvk_ransac_estimate on the same frame.
+ *
+ *   rvk_stream_create   params are validated once (src/ransac.cpp:140-145);
+ *                       depth in [1, 8] (0 = default 3).
+ *   rvk_stream_submit   validates the frame like run_ransac
+ *                       (src/ransac.cpp:147-156) and enqueues it; returns a
+ *                       ticket. Pinned (cudaHostAlloc / cudaHostRegister)
+ *                       input and output arrays are read / written by DMA
+ *                       directly and must stay valid until the ticket is
+ *                       waited for; pageable inputs are staged during the
+ *                       call. Blocks only when all `depth` slots are busy
+ *                       (it then completes the oldest frame).
+ *   rvk_stream_wait     blocks until the ticket's outputs are in the caller's
+ *                       arrays (idempotent; completed tickets return RVK_OK).
+ *   rvk_stream_destroy  completes every in-flight frame and frees the stream.
+ *
+ * A stream belongs to the device that was current at creation and is used
+ * by one host thread at a time. */
+typedef struct rvk_frame_stream rvk_frame_stream;
+int rvk_stream_create(const rvk_ransac_params* params, int32_t depth, rvk_frame_stream** out);
+int rvk_stream_submit(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
+                      const int64_t* offsets, const double* azimuth, const double* doppler,
+                      const int32_t* cluster_ids, const int32_t* rng_cluster_index,
+                      int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                      rvk_estimate* out, int64_t* ticket);
+int rvk_stream_wait(rvk_frame_stream* s, int64_t ticket);
+int rvk_stream_destroy(rvk_frame_stream* s);
+
 /* Stage timing for benchmarking/profiling. When enabled, CUDA events bracket
  * every pipeline stage launch on its stream (0 = prep, 1 = hypothesis
  * setup + tile plan, 2 = score, 3 = select+refit); rvk_profile_read waits for them, returns the accumulated

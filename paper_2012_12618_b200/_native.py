@@ -65,6 +65,10 @@ GPU_SIGNATURES = {
     "rvk_trial_counts": (C.c_int, [_I32, _P, _P, _P, _P, _P, _P]),
     "rvk_seed_pairs": (C.c_int, [_I32, _P, _P, _P, _P]),
     "rvk_cluster_thresholds": (C.c_int, [_I32, _P, _P, _P, _F64, _P, _P]),
+    "rvk_stream_create": (C.c_int, [_P, _I32, _P]),
+    "rvk_stream_submit": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "rvk_stream_wait": (C.c_int, [_P, _I64]),
+    "rvk_stream_destroy": (C.c_int, [_P]),
     "rvk_profile_enable": (None, [_I32]),
     "rvk_profile_read": (C.c_int, [_P, _P, _I32]),
 }

@@ -256,6 +256,77 @@ def ransac_estimate_device(offsets, azimuth, doppler, params: RansacParams, out,
         N.ptr(out["winning_trial"]), N.ptr(out["mask"]), N.ptr(out["est"]), s))
 
 
+class FrameStream:
+    """rvk_stream_*: the reference's per-frame loop (tools/rvk_main.cpp:125-149)
+    pipelined on the device, up to `depth` frames in flight.
+
+    ``submit`` enqueues one CSR frame (or a batch of frames with frame-local
+    ``rng_cluster_index``) and returns a ticket; ``result(ticket)`` waits and
+    returns ``(RansacResult, estimates)``. Arrays handed to ``submit`` are kept
+    alive by the stream until their ticket completes; pass pinned arrays
+    (``pinned_empty``) to let the copy engines read/write them directly.
+    """
+
+    def __init__(self, params: RansacParams, depth: int = 3):
+        self._lib = N.gpu()
+        self._p = params.c()
+        h = C.c_void_p()
+        _check(self._lib.rvk_stream_create(C.addressof(self._p), int(depth), C.byref(h)))
+        self._h = h
+        self._inputs = {}
+        self._outs = {}
+
+    def submit(self, offsets, azimuth, doppler, frame_id: int = 0, cluster_ids=None,
+               rng_cluster_index=None, out=None) -> int:
+        offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+        n = offsets.size - 1
+        if out is None:
+            out = (np.zeros(n, np.int32), np.zeros(n, np.int32),
+                   np.zeros(int(offsets[-1]), np.uint8), np.zeros(n, N.ESTIMATE_DTYPE))
+        cnt, tr, mask, est = out
+        ids = _opt_i32(cluster_ids, n)
+        keys = _opt_i32(rng_cluster_index, n)
+        t = C.c_int64(-1)
+        _check(self._lib.rvk_stream_submit(self._h, frame_id, n, N.ptr(offsets), N.ptr(azimuth),
+                                           N.ptr(doppler), N.ptr(ids), N.ptr(keys), N.ptr(cnt),
+                                           N.ptr(tr), N.ptr(mask), N.ptr(est), C.byref(t)))
+        self._inputs[t.value] = (offsets, azimuth, doppler, ids, keys)
+        self._outs[t.value] = out
+        # tickets >= depth (<= 8) behind are complete: their inputs are free
+        for k in [k for k in self._inputs if k < t.value - 8]:
+            del self._inputs[k]
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        _check(self._lib.rvk_stream_wait(self._h, int(ticket)))
+
+    def result(self, ticket: int):
+        self.wait(ticket)
+        self._inputs.pop(ticket, None)
+        cnt, tr, mask, est = self._outs.pop(ticket)
+        return RansacResult(cnt, tr, mask), est
+
+    def close(self) -> None:
+        if self._h:
+            st = self._lib.rvk_stream_destroy(self._h)
+            self._h = None
+            self._inputs.clear()
+            _check(st)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._lib.rvk_stream_destroy(self._h)
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def estimates_from_records(rec: np.ndarray):
     return [VelocityEstimate(int(r["frame_id"]), int(r["cluster_id"]), float(r["v_x"]),
                              float(r["v_y"]), float(r["heading"]) if r["has_heading"] else None,

@@ -61,7 +61,9 @@ struct DevBuf {
   T* get(size_t count) {
     const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
     if (bytes > cap) {
-      const size_t want = std::max(bytes, cap * 2);
+      // headroom: frames of a stream vary in size, and every regrow is a
+      // device-synchronizing cudaFree/cudaMalloc
+      const size_t want = std::max(bytes + bytes / 4, cap * 2);
       if (p) cudaFree(p);
       p = nullptr;
       cap = 0;
@@ -81,7 +83,7 @@ struct HostBuf {
       if (p) cudaFreeHost(p);
       p = nullptr;
       cap = 0;
-      const size_t want = std::max<size_t>(bytes, 1 << 20);
+      const size_t want = std::max<size_t>(bytes + bytes / 4, 1 << 20);
       RVK_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
       cap = want;
     }
@@ -494,6 +496,149 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
   return RVK_OK;
 }
 
+// ---- pipelined frame stream (rvk_stream_*) ----
+//
+// Slot k % depth holds frame k: its own device input/output blocks, scratch
+// and pinned staging. Frame k's H2D runs on the copy stream; its kernels and
+// D2H on compute stream k % 2 once its bytes have landed. A slot is reused
+// only after its previous frame completed (host wait on its `done` event),
+// so no device buffer is ever overwritten while in use.
+struct StreamSlot {
+  DevBuf in, out;
+  HostBuf small_in, big_in, stage_out;
+  Workspace ws;
+  cudaEvent_t landed = nullptr, done = nullptr;
+  int64_t ticket = -1;  // frame in the slot (-1: none pending)
+  int32_t C = 0;
+  int64_t P = 0;
+  OutLayout L{0, 0};
+  int32_t* cnt = nullptr;
+  int32_t* tr = nullptr;
+  uint8_t* mask = nullptr;
+  rvk_estimate* est = nullptr;
+  bool pin_mask = false;
+};
+
+struct FrameStream {
+  int device = 0;
+  rvk_ransac_params params{};
+  int depth = 3;
+  cudaStream_t copy = nullptr;
+  cudaStream_t compute[2] = {nullptr, nullptr};
+  std::vector<StreamSlot> slots;
+  int64_t next = 0;
+
+  // Delivers slot s's outputs to the caller's arrays (waits for its D2H).
+  void complete(StreamSlot& s) {
+    if (s.ticket < 0) return;
+    RVK_CUDA(cudaEventSynchronize(s.done));
+    const char* h = static_cast<const char*>(s.stage_out.p);
+    if (s.cnt) std::memcpy(s.cnt, h + s.L.o_cnt, sizeof(int32_t) * s.C);
+    if (s.tr) std::memcpy(s.tr, h + s.L.o_tr, sizeof(int32_t) * s.C);
+    if (s.est) std::memcpy(s.est, h + s.L.o_est, sizeof(rvk_estimate) * s.C);
+    if (s.mask && !s.pin_mask) std::memcpy(s.mask, h + s.L.o_mask, s.P);
+    s.ticket = -1;
+  }
+
+  int submit(int64_t frame_id, int32_t n_clusters, const int64_t* offsets, const double* az,
+             const double* dop, const int32_t* ids, const int32_t* keys, int32_t* cnt,
+             int32_t* tr, uint8_t* mask, rvk_estimate* est, int64_t* ticket) {
+    int st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
+    if (st != RVK_OK) return st;
+    const int64_t P = n_clusters ? offsets[n_clusters] : 0;
+    if ((az == nullptr || dop == nullptr) && P > 0)
+      return fail(RVK_EINVAL, "run_ransac: null point arrays");
+    RVK_CUDA(cudaSetDevice(device));
+    const int64_t k = next;
+    StreamSlot& s = slots[k % depth];
+    const auto tw = std::chrono::steady_clock::now();
+    complete(s);  // frees the slot (the frame submitted `depth` calls ago)
+    if (trace_on())
+      std::fprintf(stderr, "[rvk stream] ticket %lld waited %.1fus for slot %lld\n",
+                   static_cast<long long>(k),
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw)
+                       .count(),
+                   static_cast<long long>(k % depth));
+    if (ticket) *ticket = k;
+    ++next;
+    if (n_clusters == 0) return RVK_OK;
+    cudaStream_t sc = compute[k & 1];
+
+    // small arrays: offsets | keys | ids, always through pinned staging
+    const size_t o_keys = align_up(sizeof(int64_t) * (n_clusters + 1));
+    const size_t o_ids = align_up(o_keys + sizeof(int32_t) * n_clusters);
+    const size_t small = align_up(o_ids + sizeof(int32_t) * n_clusters);
+    const size_t o_az = small;
+    const size_t o_dop = align_up(o_az + sizeof(double) * P);
+    const size_t in_total = align_up(o_dop + sizeof(double) * P);
+    char* h = static_cast<char*>(s.small_in.get(small));
+    char* d = s.in.get<char>(in_total);
+    std::memcpy(h, offsets, sizeof(int64_t) * (n_clusters + 1));
+    int32_t* h_keys = reinterpret_cast<int32_t*>(h + o_keys);
+    int32_t* h_ids = reinterpret_cast<int32_t*>(h + o_ids);
+    for (int32_t c = 0; c < n_clusters; ++c) h_keys[c] = keys ? keys[c] : c;
+    for (int32_t c = 0; c < n_clusters; ++c) h_ids[c] = ids ? ids[c] : c;
+    const bool pin_in = is_pinned(az) && is_pinned(dop);
+    RVK_CUDA(cudaMemcpyAsync(d, h, small, cudaMemcpyHostToDevice, copy));
+    if (pin_in) {
+      RVK_CUDA(cudaMemcpyAsync(d + o_az, az, sizeof(double) * P, cudaMemcpyHostToDevice, copy));
+      RVK_CUDA(cudaMemcpyAsync(d + o_dop, dop, sizeof(double) * P, cudaMemcpyHostToDevice, copy));
+    } else {
+      char* hb = static_cast<char*>(s.big_in.get(in_total - o_az));
+      std::memcpy(hb, az, sizeof(double) * P);
+      std::memcpy(hb + (o_dop - o_az), dop, sizeof(double) * P);
+      RVK_CUDA(cudaMemcpyAsync(d + o_az, hb, in_total - o_az, cudaMemcpyHostToDevice, copy));
+    }
+    RVK_CUDA(cudaEventRecord(s.landed, copy));
+    RVK_CUDA(cudaStreamWaitEvent(sc, s.landed, 0));
+
+    FrameDev f;
+    f.n_clusters = n_clusters;
+    f.n_points = P;
+    f.offsets = reinterpret_cast<const int64_t*>(d);
+    f.azimuth = reinterpret_cast<const double*>(d + o_az);
+    f.doppler = reinterpret_cast<const double*>(d + o_dop);
+    f.keys = reinterpret_cast<const int32_t*>(d + o_keys);
+    f.cluster_ids = reinterpret_cast<const int32_t*>(d + o_ids);
+    f.frame_id = frame_id;
+    s.L = OutLayout(n_clusters, P);
+    char* dout = s.out.get<char>(s.L.total);
+    char* hout = static_cast<char*>(s.stage_out.get(s.L.total));
+    Scratch scr = scratch(s.ws, n_clusters, P, params.max_trials);
+    Outputs o;
+    o.inlier_count = reinterpret_cast<int32_t*>(dout + s.L.o_cnt);
+    o.winning_trial = reinterpret_cast<int32_t*>(dout + s.L.o_tr);
+    o.est = reinterpret_cast<rvk_estimate*>(dout + s.L.o_est);
+    o.mask = reinterpret_cast<uint8_t*>(dout + s.L.o_mask);
+    run_pipeline(f, params, scr, o, sc);
+    s.pin_mask = is_pinned(mask);
+    // counts | trials | estimates in one D2H, the mask straight to the caller
+    // when it is pinned
+    if (cnt || tr || est)
+      RVK_CUDA(cudaMemcpyAsync(hout, dout, s.L.o_mask, cudaMemcpyDeviceToHost, sc));
+    if (mask)
+      RVK_CUDA(cudaMemcpyAsync(s.pin_mask ? static_cast<void*>(mask) : hout + s.L.o_mask,
+                               o.mask, P, cudaMemcpyDeviceToHost, sc));
+    RVK_CUDA(cudaEventRecord(s.done, sc));
+    s.ticket = k;
+    s.C = n_clusters;
+    s.P = P;
+    s.cnt = cnt;
+    s.tr = tr;
+    s.mask = mask;
+    s.est = est;
+    return RVK_OK;
+  }
+
+  int wait(int64_t ticket) {
+    if (ticket < 0 || ticket >= next) return fail(RVK_EINVAL, "rvk_stream_wait: unknown ticket");
+    RVK_CUDA(cudaSetDevice(device));
+    StreamSlot& s = slots[ticket % depth];
+    if (s.ticket == ticket) complete(s);
+    return RVK_OK;  // older tickets were completed when their slot was reused
+  }
+};
+
 }  // namespace
 
 void count_launch() { ++g_launches; }
@@ -501,6 +646,10 @@ void count_launch() { ++g_launches; }
 }  // namespace rvk_gpu
 
 using namespace rvk_gpu;
+
+struct rvk_frame_stream {
+  FrameStream impl;
+};
 
 extern "C" {
 
@@ -692,6 +841,82 @@ int rvk_cluster_thresholds(int32_t n_clusters, const int64_t* offsets, const dou
     if (threshold)
       for (int32_t c = 0; c < n_clusters; ++c) threshold[c] = stv[c].w;
     return RVK_OK;
+  });
+}
+
+int rvk_stream_create(const rvk_ransac_params* params, int32_t depth, rvk_frame_stream** out) {
+  return guarded([&]() -> int {
+    if (out == nullptr) return fail(RVK_EINVAL, "rvk_stream_create: out is null");
+    *out = nullptr;
+    const int st = validate_params(params, "run_ransac");
+    if (st != RVK_OK) return st;
+    if (depth < 0 || depth > 8) return fail(RVK_EINVAL, "rvk_stream_create: depth must be in [0, 8]");
+    auto* h = new rvk_frame_stream();
+    FrameStream& fs = h->impl;
+    fs.params = *params;
+    fs.depth = depth ? depth : 3;
+    try {
+      RVK_CUDA(cudaGetDevice(&fs.device));
+      RVK_CUDA(cudaStreamCreateWithFlags(&fs.copy, cudaStreamNonBlocking));
+      for (auto& c : fs.compute) RVK_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
+      fs.slots.resize(fs.depth);
+      for (auto& s : fs.slots) {
+        RVK_CUDA(cudaEventCreateWithFlags(&s.landed, cudaEventDisableTiming));
+        RVK_CUDA(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+      }
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+    return RVK_OK;
+  });
+}
+
+int rvk_stream_submit(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
+                      const int64_t* offsets, const double* azimuth, const double* doppler,
+                      const int32_t* cluster_ids, const int32_t* rng_cluster_index,
+                      int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                      rvk_estimate* out, int64_t* ticket) {
+  return guarded([&]() -> int {
+    if (s == nullptr) return fail(RVK_EINVAL, "rvk_stream_submit: null stream");
+    return s->impl.submit(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
+                          rng_cluster_index, inlier_count, winning_trial, mask, out, ticket);
+  });
+}
+
+int rvk_stream_wait(rvk_frame_stream* s, int64_t ticket) {
+  return guarded([&]() -> int {
+    if (s == nullptr) return fail(RVK_EINVAL, "rvk_stream_wait: null stream");
+    return s->impl.wait(ticket);
+  });
+}
+
+int rvk_stream_destroy(rvk_frame_stream* s) {
+  return guarded([&]() -> int {
+    if (s == nullptr) return RVK_OK;
+    FrameStream& fs = s->impl;
+    int rc = RVK_OK;
+    try {
+      RVK_CUDA(cudaSetDevice(fs.device));
+      for (auto& sl : fs.slots) fs.complete(sl);
+    } catch (const CudaError& e) {
+      rc = fail(RVK_ECUDA, "CUDA error %s in %s", cudaGetErrorName(e.e), e.what);
+    }
+    for (auto& sl : fs.slots) {
+      if (sl.landed) cudaEventDestroy(sl.landed);
+      if (sl.done) cudaEventDestroy(sl.done);
+      for (DevBuf* b : {&sl.in, &sl.out, &sl.ws.xy64, &sl.ws.xy32, &sl.ws.thr, &sl.ws.norm,
+                        &sl.ws.upper, &sl.ws.hyp, &sl.ws.tiles, &sl.ws.tile_count, &sl.ws.aux})
+        if (b->p) cudaFree(b->p);
+      for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out})
+        if (b->p) cudaFreeHost(b->p);
+    }
+    if (fs.copy) cudaStreamDestroy(fs.copy);
+    for (auto& c : fs.compute)
+      if (c) cudaStreamDestroy(c);
+    delete s;
+    return rc;
   });
 }
 

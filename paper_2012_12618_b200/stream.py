@@ -12,7 +12,9 @@ Frames are independent and the RNG is keyed on the frame-local cluster index
   per-frame calls (the reference's worker-count invariance,
   include/rvk/ransac.hpp:124-125).
 * ``estimate_stream(frames, params)`` -- this rank's frames through the
-  device pipeline in batches (host API: pinned staging, chunked H2D/D2H).
+  device pipeline in batches: a ``FrameStream`` (rvk_stream_*) keeps up to
+  ``depth`` batches in flight, so the H2D of batch k+1 overlaps the kernels
+  of batch k.
 * ``gather_to_root(results)``   -- the only cross-rank step: a host gather of
   the per-frame results to rank 0, in frame order (torch.distributed
   ``gather_object``; gloo or NCCL process group).
@@ -78,17 +80,29 @@ def _device_estimator(params):
 
 
 def estimate_stream(frames: Sequence, params, frame_ids: Optional[Sequence[int]] = None,
-                    batch: int = 8, estimator: Optional[Callable] = None) -> List[FrameResult]:
+                    batch: int = 8, estimator: Optional[Callable] = None,
+                    depth: int = 3) -> List[FrameResult]:
     """run_ransac + estimate_all for each frame, `batch` frames per device
-    call. `estimator(offsets, az, dop, keys) -> (count, trial, mask, est)`
-    defaults to the sm_100a pipeline; tests may inject the CPU oracle."""
-    run = estimator or _device_estimator(params)
+    call, `depth` calls in flight. `estimator(offsets, az, dop, keys) ->
+    (count, trial, mask, est)` replaces the sm_100a pipeline (tests inject
+    the CPU oracle)."""
     ids = list(frame_ids) if frame_ids is not None else list(range(len(frames)))
     out: List[FrameResult] = []
+    batches = []
     for b0 in range(0, len(frames), batch):
-        chunk = frames[b0:b0 + batch]
-        off, az, dop, keys, cr, pr = batch_frames(chunk)
-        cnt, tr, mask, est = run(off, az, dop, keys)
+        batches.append((b0, batch_frames(frames[b0:b0 + batch])))
+    if estimator is not None:
+        results = [estimator(off, az, dop, keys) for _, (off, az, dop, keys, _, _) in batches]
+    else:
+        from .api import FrameStream
+        results = []
+        with FrameStream(params, depth=depth) as fs:
+            tickets = [fs.submit(off, az, dop, rng_cluster_index=keys)
+                       for _, (off, az, dop, keys, _, _) in batches]
+            for t in tickets:
+                r, est = fs.result(t)
+                results.append((r.inlier_count, r.winning_trial, r.mask, est))
+    for (b0, (_, _, _, _, cr, pr)), (cnt, tr, mask, est) in zip(batches, results):
         for k, ((ca, cb), (pa, pb)) in enumerate(zip(cr, pr)):
             e = est[ca:cb].copy()
             e["frame_id"] = ids[b0 + k]

@@ -277,3 +277,46 @@ def test_reference_acceptance_against_dropin(gpu_lib):
     assert code == 0, log[-4000:]
     for crit in ("C1", "C2", "C3", "C5", "C6", "C7"):
         assert f"[ACCEPTANCE] {crit}" in log and ": PASS" in log
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_frame_stream_matches_host_api(gpu_lib, depth):
+    """rvk_stream_*: pipelined frames give the same bytes as one-shot calls,
+    for pinned and pageable inputs, any depth, waits in any order."""
+    import torch
+    frames = [W.automotive(seed=70 + i, n_clusters=30) for i in range(7)]
+    p = rvk.RansacParams(256, 1.0, 11)
+    want = [rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p, frame_id=i)
+            for i, w in enumerate(frames)]
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    with rvk.FrameStream(p, depth=depth) as fs:
+        tickets = []
+        for i, w in enumerate(frames):
+            if i % 2:
+                az, dop = pin(w.azimuth), pin(w.doppler)
+                out = (pin(np.zeros(w.n_clusters, np.int32)), pin(np.zeros(w.n_clusters, np.int32)),
+                       pin(np.zeros(w.n_points, np.uint8)), np.zeros(w.n_clusters, est_dtype()))
+            else:
+                az, dop, out = w.azimuth, w.doppler, None
+            tickets.append(fs.submit(w.offsets, az, dop, frame_id=i, out=out))
+        assert tickets == list(range(len(frames)))
+        order = list(reversed(tickets)) if depth > 1 else tickets
+        got = {t: fs.result(t) for t in order}
+        fs.wait(tickets[0])  # idempotent
+        with pytest.raises(ValueError, match="unknown ticket"):
+            fs.wait(len(frames) + 5)
+        with pytest.raises(rvk.ClusterTooSmall):
+            fs.submit(np.array([0, 2], np.int64), np.zeros(2), np.zeros(2))
+    for t, (r, est) in zip(tickets, want):
+        g, ge = got[t]
+        np.testing.assert_array_equal(g.mask, r.mask)
+        np.testing.assert_array_equal(g.winning_trial, r.winning_trial)
+        np.testing.assert_array_equal(g.inlier_count, r.inlier_count)
+        for f in ("frame_id", "cluster_id", "v_x", "v_y", "heading", "inlier_count",
+                  "condition_ok", "has_heading"):
+            np.testing.assert_array_equal(ge[f], est[f])
+
+
+def est_dtype():
+    from paper_2012_12618_b200 import _native
+    return _native.ESTIMATE_DTYPE
