@@ -94,6 +94,7 @@ struct HostBuf {
 // Device scratch of one stream's in-flight pipeline.
 struct Workspace {
   DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, tile_count, aux;
+  DevBuf tc_hyp, tc_pts, tc_items, tc_count;
 };
 
 struct Context {
@@ -242,10 +243,19 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   s.stat = w.thr.get<double4>(C);
   s.norm = w.norm.get<double>(4 * C);
   s.upper = w.upper.get<int32_t>(C * g.Tg * 8);
-  s.hyp = w.hyp.get<float>(C * g.Tg * 32);
-  s.tile_cap = tile_capacity(g, P, n_clusters);
-  s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
-  s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
+  s.tc = score_uses_tc();
+  if (s.tc) {
+    const size_t nhb = static_cast<size_t>(tc_blocks(std::max(T, 1)));
+    s.tc_hyp = w.tc_hyp.get<float>(C * nhb * kTcHypFloats);
+    s.tc_pts = w.tc_pts.get<float>((static_cast<size_t>(P) + 32 * C + 32) * 8);
+    s.tc_items = w.tc_items.get<int4>(static_cast<size_t>(kTcBuckets) * C);
+    s.tc_count = w.tc_count.get<int32_t>(kTcBuckets + 1);
+  } else {
+    s.hyp = w.hyp.get<float>(C * g.Tg * 32);
+    s.tile_cap = tile_capacity(g, P, n_clusters);
+    s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
+    s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
+  }
   return s;
 }
 
@@ -907,7 +917,9 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
       if (sl.landed) cudaEventDestroy(sl.landed);
       if (sl.done) cudaEventDestroy(sl.done);
       for (DevBuf* b : {&sl.in, &sl.out, &sl.ws.xy64, &sl.ws.xy32, &sl.ws.thr, &sl.ws.norm,
-                        &sl.ws.upper, &sl.ws.hyp, &sl.ws.tiles, &sl.ws.tile_count, &sl.ws.aux})
+                        &sl.ws.upper, &sl.ws.hyp, &sl.ws.tiles, &sl.ws.tile_count, &sl.ws.aux,
+                        &sl.ws.tc_hyp, &sl.ws.tc_pts, &sl.ws.tc_items,
+                        &sl.ws.tc_count})
         if (b->p) cudaFree(b->p);
       for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out})
         if (b->p) cudaFreeHost(b->p);

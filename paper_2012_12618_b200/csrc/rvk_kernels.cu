@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include <math_constants.h>
 
@@ -474,6 +475,76 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
 }
 
+// ------------------------------------------------ tensor-core operand layout
+//
+// The scoring MMA computes D[h][p] = sum_k Hyp[h][k] * Pt[p][k] over K = 8
+// tf32 values per row, with every FP64 coefficient and coordinate split into
+// two tf32 parts (v = v1 + v2 + O(2^-22 v)):
+//   hypothesis row h: [A1, A1, A2, B1, B1, B2, C1, C2]
+//   point row p:      [x1, x2, x1, y1, y2, y1, 1,  1 ]
+// so D = A x + B y + C with |D - exact| <= ~2^-22 S (measured 2^-22.3 S,
+// tools/tc_probe.cu; S = |A| + |B| + |C|). The corridor band is 2^-18 S.
+// Rows are stored in the K-major, no-swizzle canonical layout of
+// tcgen05.mma: 8-row x 16-byte core matrices, the two 16-byte K halves
+// 128 B apart (LBO), consecutive 8-row groups 256 B apart (SBO).
+constexpr float kTcBig = 0x1p100f;  // inert rows: |D| >= 2^100 is never inside a corridor
+
+struct TcOut {
+  float* hyp = nullptr;
+  float* pts = nullptr;
+  int4* items = nullptr;
+  int32_t* count = nullptr;
+  int64_t cap = 0;  // entries per size class
+};
+
+__host__ __device__ __forceinline__ int tc_kmaj_off(int row, int k) {  // in floats
+  return (row >> 3) * 64 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
+}
+__device__ __forceinline__ float tf32_rna(float f) {
+  return __uint_as_float((__float_as_uint(f) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void tf32_split(double v, float& hi, float& lo) {
+  hi = tf32_rna(__double2float_rn(v));
+  lo = tf32_rna(__double2float_rn(v - static_cast<double>(hi)));
+}
+// Writes one K = 8 operand row (two 16-byte halves) of a K-major tile.
+__device__ __forceinline__ void tc_store_row(float* tile, int row, float4 lo, float4 hi) {
+  *reinterpret_cast<float4*>(tile + tc_kmaj_off(row, 0)) = lo;
+  *reinterpret_cast<float4*>(tile + tc_kmaj_off(row, 4)) = hi;
+}
+__device__ __forceinline__ void tc_store_point(float* tile, int row, double x, double y) {
+  float x1, x2, y1, y2;
+  tf32_split(x, x1, x2);
+  tf32_split(y, y1, y2);
+  tc_store_row(tile, row, make_float4(x1, x2, x1, y1), make_float4(y2, y1, 1.f, 1.f));
+}
+__device__ __forceinline__ void tc_store_inert_point(float* tile, int row) {
+  tc_store_row(tile, row, make_float4(0.f, 0.f, 0.f, kTcBig), make_float4(0.f, kTcBig, 1.f, 1.f));
+}
+// Hypothesis row + squared corridor bound from the exact seeds (the same
+// FP64 slope/intercept as make_line, 1/den by rsqrt: a few ulps of 1/den
+// move A, B, C by ~1e-16 relative, far inside the band).
+__device__ __forceinline__ float tc_store_hyp(float* tile, int row, double x1, double y1,
+                                              double x2, double y2, double thr_hi) {
+  const double dx = __dsub_rn(x2, x1);
+  if (fabs(dx) < kSeedEpsilon) {  // degenerate seeds score 0 (src/ransac.cpp:40-42)
+    tc_store_row(tile, row, make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, kTcBig, 0.f));
+    return -1.f;
+  }
+  const double m = __ddiv_rn(__dsub_rn(y2, y1), dx);
+  const double c = __dsub_rn(y1, __dmul_rn(m, x1));
+  const double r = rsqrt(__dadd_rn(__dmul_rn(m, m), 1.0));
+  const double A = -m * r, B = r, C = -c * r;
+  float a1, a2, b1, b2, c1, c2;
+  tf32_split(A, a1, a2);
+  tf32_split(B, b1, b2);
+  tf32_split(C, c1, c2);
+  tc_store_row(tile, row, make_float4(a1, a1, a2, b1), make_float4(b1, b2, c1, c2));
+  const double band = (fabs(A) + fabs(B) + fabs(C)) * 0x1p-18;
+  const double hi = (thr_hi + band) * (1.0 + 0x1p-30);
+  return __double2float_ru(hi * hi);
+}
+
 // prep + hypothesis setup + tile registration, one CTA per cluster.
 //
 // Hypotheses (src/ransac.cpp:35-46 for every trial of draw_seed_pair
@@ -490,7 +561,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
                 float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
                 int32_t* __restrict__ upper, int4* __restrict__ tiles,
-                int32_t* __restrict__ tile_count, int64_t tile_cap) {
+                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc) {
   __shared__ PrepShared sm;
   __shared__ int tile_pos[2];
   const int c = blockIdx.x;
@@ -500,8 +571,56 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double thr_lo = sm.stat.x, thr_hi = sm.stat.y;
   const double2* p64 = xy64 + b;  // written by this CTA before the barrier
-  float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
+  if (tc.hyp != nullptr) {
+    // tensor-core operands: point rows, hypothesis tiles, corridor bounds
+    const int nhb = tc_blocks(g.T);
+    float* pts = tc.pts + tc_row_base(b, c) * 8;
+    const int nr = (n + 15) & ~15;
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+      float* tile = pts + (k & ~(kTcN - 1)) * 8;
+      if (k >= n) {
+        tc_store_inert_point(tile, k & (kTcN - 1));
+      } else if (n <= kSortCap) {
+        tc_store_point(tile, k & (kTcN - 1), sm.xs[k],
+                       __longlong_as_double(static_cast<long long>(sm.keys[k])));
+      } else {
+        const double2 q = p64[k];
+        tc_store_point(tile, k & (kTcN - 1), q.x, q.y);
+      }
+    }
+    float* hb0 = tc.hyp + static_cast<int64_t>(c) * nhb * kTcHypFloats;
+    for (int t = threadIdx.x; t < nhb * kTcM; t += blockDim.x) {
+      float* tile = hb0 + (t / kTcM) * kTcHypFloats;
+      float t2 = -1.f;
+      if (t < g.T) {
+        int i, j;
+        seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+        double2 p, q;
+        if (n <= kSortCap) {
+          p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
+          q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
+        } else {
+          p = p64[i];
+          q = p64[j];
+        }
+        t2 = tc_store_hyp(tile, t % kTcM, p.x, p.y, q.x, q.y, thr_hi);
+      } else {
+        tc_store_row(tile, t % kTcM, make_float4(0.f, 0.f, 0.f, 0.f),
+                     make_float4(0.f, 0.f, kTcBig, 0.f));
+      }
+      tile[kTcM * 8 + t % kTcM] = t2;
+    }
+    for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) uc[t] = 0;
+    if (threadIdx.x == 0) {
+      const int bk = kTcBuckets - 1 - min(kTcBuckets - 1, (n - 1) >> 6);
+      const int64_t r0 = tc_row_base(b, c);
+      tc.items[static_cast<int64_t>(bk) * tc.cap + atomicAdd(&tc.count[bk], 1)] =
+          make_int4(c, n, static_cast<int>(r0 & 0xFFFFFFFF), static_cast<int>(r0 >> 32));
+    }
+    return;
+  }
+  float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) {
     FastHyp f = inert_fast();
     if (t < g.T) {
@@ -584,16 +703,24 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Waits for the phase with the given parity. A wait that never completes is
+// a pipeline bug: trap (the launch fails with an error) instead of hanging.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint32_t spins = 0; !mbar_try_wait(bar, parity);)
+    if (++spins == (1u << 26)) __trap();
 }
 // 1-D bulk copy global -> shared (TMA engine), completion on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -785,6 +912,292 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
       for (int q = 0; q < kNH; ++q)
         if (cnt[q]) atomicAdd(&up[q], static_cast<int32_t>(cnt[q]));
     }
+  }
+}
+
+// ---------------------------------------------------- tensor-core scoring
+//
+// score_tc_kernel: persistent, warp-specialized, one CTA per SM, 18 warps:
+//   warp 0      producer: claims work items (batches of 8, largest clusters
+//               first) and streams each item's hypothesis tile (+ corridor
+//               bounds) and its point tiles into shared memory with
+//               cp.async.bulk (TMA engine) on mbarriers;
+//   warp 1      MMA issuer (one lane): per point block ONE tcgen05.mma
+//               kind::tf32 (M = 128 hypotheses, N <= kTcN points, K = 8)
+//               into one of the TMEM accumulator buffers, tcgen05.commit to the
+//               epilogue and to the smem stages it frees;
+//   warps 2-17  epilogue: tcgen05.ld of the accumulator (thread = one
+//               hypothesis row, registers = points; four warps per TMEM lane
+//               quarter, kTcN / 4 columns each), g = D^2 - t2hi (FFMA2 over column
+//               pairs), sign-bit count (LEA.HI); per item one integer atomic
+//               per thread.
+// A work item = (cluster, block of 128 hypotheses) over all of the cluster's
+// points. Counts are upper bounds of the exact FP64 counts (band 2^-18 S,
+// see the operand layout above), as the FFMA2 path's; select_kernel decides
+// exactly.
+constexpr int kTcAStages = 4;
+constexpr int kTcBStages = 8;
+constexpr int kTcDStages = 8;
+constexpr int kTcTBufs = 512 / kTcN;                // TMEM accumulator buffers
+constexpr int kTcW = kTcN / 4;                      // columns per epilogue warp and block
+constexpr int kTcEpiWarps = 16;
+constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
+constexpr int kTcBatch = 8;                          // items per claim
+constexpr uint32_t kTcTmemCols = kTcTBufs * kTcN;    // 512: the whole TMEM
+constexpr uint32_t kTcATileBytes = kTcHypFloats * 4; // operand tile + bounds
+constexpr uint32_t kTcAStageBytes = 5120;
+constexpr uint32_t kTcBTileBytes = kTcN * kTcRowBytes;
+constexpr size_t kTcSmemUsed = 1024 + kTcAStages * kTcAStageBytes + kTcBStages * kTcBTileBytes;
+// more than half of the SM's shared memory: two scoring CTAs (each owning all
+// 512 TMEM columns) can never be co-resident
+constexpr size_t kTcSmemBytes = 116 * 1024;
+static_assert(kTcSmemUsed <= kTcSmemBytes, "stages exceed the reservation");
+
+struct TcShared {
+  uint64_t a_full[kTcAStages], a_empty[kTcAStages];
+  uint64_t b_full[kTcBStages], b_empty[kTcBStages];
+  uint64_t t_full[kTcTBufs], t_empty[kTcTBufs];
+  uint64_t d_full[kTcDStages], d_empty[kTcDStages];
+  int4 desc[kTcDStages];
+  int bstart[kTcBuckets + 1];
+  uint32_t tmem;
+};
+static_assert(sizeof(TcShared) <= 1024, "TcShared must fit the 1 KB header");
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// Shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO 256 B.
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
+}
+// D[tmem] = A[smem] * B[smem]^T, kind::tf32, f32 result (no accumulation).
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t rows) {
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((rows >> 3) << 17) |
+                         (static_cast<uint32_t>(kTcM >> 4) << 24);
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(0)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// Sign-bit count of D^2 - t2hi over 16 accumulator columns (FFMA2 pairs).
+__device__ __forceinline__ void tc_count16(const uint32_t (&r)[16], float2 nt2,
+                                           uint32_t (&cnt)[4]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 e = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+    const float2 g = __ffma2_rn(e, e, nt2);
+    cnt[(2 * j) & 3] += __float_as_uint(g.x) >> 31;
+    cnt[(2 * j + 1) & 3] += __float_as_uint(g.y) >> 31;
+  }
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+score_tc_kernel(const int4* __restrict__ items, int64_t cap, int32_t* __restrict__ item_count,
+                const float* __restrict__ hyp, const float* __restrict__ pts, int T, int Tg8,
+                int32_t* __restrict__ upper) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  TcShared& sh = *reinterpret_cast<TcShared*>(smem);
+  unsigned char* a_st = smem + 1024;
+  unsigned char* b_st = a_st + kTcAStages * kTcAStageBytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nhb = tc_blocks(T);
+  if (warp == 0) {
+    const int v = lane < kTcBuckets ? item_count[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane < kTcBuckets) sh.bstart[lane] = incl - v;
+    if (lane == 31) sh.bstart[kTcBuckets] = incl;
+    if (lane == 0) {
+      for (int i = 0; i < kTcAStages; ++i) {
+        mbar_init(&sh.a_full[i], 1);
+        mbar_init(&sh.a_empty[i], 1 + kTcEpiWarps);  // MMA done + bounds read
+      }
+      for (int i = 0; i < kTcBStages; ++i) {
+        mbar_init(&sh.b_full[i], 1);
+        mbar_init(&sh.b_empty[i], 1);
+      }
+      for (int i = 0; i < kTcTBufs; ++i) {
+        mbar_init(&sh.t_full[i], 1);
+        mbar_init(&sh.t_empty[i], kTcEpiWarps);
+      }
+      for (int i = 0; i < kTcDStages; ++i) {
+        mbar_init(&sh.d_full[i], 1);
+        mbar_init(&sh.d_empty[i], kTcEpiWarps + 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sh.tmem)),
+                 "n"(kTcTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sh.tmem;
+  const int total = sh.bstart[kTcBuckets] * nhb;
+
+  if (warp == 0) {  // ---- producer
+    int* next = item_count + kTcBuckets;
+    int k = 0, kb = 0;
+    for (bool done = false; !done;) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(next, kTcBatch);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      // lanes 0..7 resolve one item each: (cluster, n, row base), hyp block
+      int4 e = make_int4(-1, 0, 0, 0);
+      int hb = 0;
+      const int i = base + lane;
+      if (lane < kTcBatch && i < total) {
+        const int li = i / nhb;
+        hb = i - li * nhb;
+        int bk = 0;
+        while (sh.bstart[bk + 1] <= li) ++bk;
+        e = items[bk * cap + (li - sh.bstart[bk])];
+      }
+      for (int j = 0; j <= kTcBatch; ++j) {
+        const int c = j < kTcBatch ? __shfl_sync(0xffffffffu, e.x, j) : -1;
+        if (j == kTcBatch) break;  // batch done, claim the next one
+        const int n = __shfl_sync(0xffffffffu, e.y, j);
+        const int64_t row0 = (static_cast<int64_t>(__shfl_sync(0xffffffffu, e.w, j)) << 32) |
+                             static_cast<uint32_t>(__shfl_sync(0xffffffffu, e.z, j));
+        const int h = __shfl_sync(0xffffffffu, hb, j);
+        const int ds = k % kTcDStages;
+        if (lane == 0) {
+          mbar_wait(&sh.d_empty[ds], ((k / kTcDStages) & 1) ^ 1);
+          sh.desc[ds] = make_int4(c, h, n, 0);
+          mbar_arrive(&sh.d_full[ds]);
+        }
+        if (c < 0) {
+          done = true;
+          break;
+        }
+        if (lane == 0) {
+          const int as = k % kTcAStages;
+          mbar_wait(&sh.a_empty[as], ((k / kTcAStages) & 1) ^ 1);
+          mbar_expect_tx(&sh.a_full[as], kTcATileBytes);
+          bulk_g2s(a_st + as * kTcAStageBytes,
+                   hyp + (static_cast<int64_t>(c) * nhb + h) * kTcHypFloats, kTcATileBytes,
+                   &sh.a_full[as]);
+          for (int p0 = 0; p0 < n; p0 += kTcN, ++kb) {
+            const int bs = kb % kTcBStages;
+            const uint32_t rows = static_cast<uint32_t>(min(kTcN, (n - p0 + 15) & ~15));
+            mbar_wait(&sh.b_empty[bs], ((kb / kTcBStages) & 1) ^ 1);
+            mbar_expect_tx(&sh.b_full[bs], rows * kTcRowBytes);
+            bulk_g2s(b_st + bs * kTcBTileBytes, pts + (row0 + p0) * 8, rows * kTcRowBytes,
+                     &sh.b_full[bs]);
+          }
+        }
+        ++k;
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      int kb = 0, kt = 0;
+      for (int k = 0;; ++k) {
+        const int ds = k % kTcDStages;
+        mbar_wait(&sh.d_full[ds], (k / kTcDStages) & 1);
+        const int4 d = sh.desc[ds];
+        mbar_arrive(&sh.d_empty[ds]);
+        if (d.x < 0) break;
+        const int n = d.z;
+        const int as = k % kTcAStages;
+        mbar_wait(&sh.a_full[as], (k / kTcAStages) & 1);
+        const uint64_t da = tc_desc(smem_u32(a_st + as * kTcAStageBytes));
+        for (int p0 = 0; p0 < n; p0 += kTcN, ++kb, ++kt) {
+          const int bs = kb % kTcBStages, tb = kt % kTcTBufs;
+          const uint32_t rows = static_cast<uint32_t>(min(kTcN, (n - p0 + 15) & ~15));
+          mbar_wait(&sh.b_full[bs], (kb / kTcBStages) & 1);
+          mbar_wait(&sh.t_empty[tb], ((kt / kTcTBufs) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          tc_mma(tmem + tb * kTcN, da, tc_desc(smem_u32(b_st + bs * kTcBTileBytes)), rows);
+          tc_commit(&sh.t_full[tb]);
+          tc_commit(&sh.b_empty[bs]);
+        }
+        tc_commit(&sh.a_empty[as]);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue
+    const int quarter = warp & 3;          // a warp reads TMEM lanes 32 * (warp % 4) ..
+    const int part = (warp - 2) >> 2;      // columns [32 part, 32 part + 32) of each block
+    const int row = quarter * 32 + lane;
+    int kt = 0;
+    for (int k = 0;; ++k) {
+      const int ds = k % kTcDStages;
+      mbar_wait(&sh.d_full[ds], (k / kTcDStages) & 1);
+      const int4 d = sh.desc[ds];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.d_empty[ds]);
+      if (d.x < 0) break;
+      const int c = d.x, hb = d.y, n = d.z;
+      const int t = hb * kTcM + row;
+      const int as = k % kTcAStages;
+      mbar_wait(&sh.a_full[as], (k / kTcAStages) & 1);
+      const float bound =
+          reinterpret_cast<const float*>(a_st + as * kTcAStageBytes)[kTcM * 8 + row];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.a_empty[as]);
+      const float2 nt2 = make_float2(-bound, -bound);
+      uint32_t cnt[4] = {0u, 0u, 0u, 0u};
+      for (int p0 = 0; p0 < n; p0 += kTcN, ++kt) {
+        const int tb = kt % kTcTBufs;
+        const int rows = min(kTcN, (n - p0 + 15) & ~15);
+        const int c0 = part * kTcW;
+        mbar_wait(&sh.t_full[tb], (kt / kTcTBufs) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base =
+            tmem + (static_cast<uint32_t>(quarter * 32) << 16) + tb * kTcN + c0;
+        uint32_t r[kTcW / 16][16];
+#pragma unroll
+        for (int q = 0; q < kTcW / 16; ++q)
+          if (c0 + 16 * q < rows) tc_ld16(base + 16 * q, r[q]);
+        tc_ld_wait();
+#pragma unroll
+        for (int q = 0; q < kTcW / 16; ++q)
+          if (c0 + 16 * q < rows) tc_count16(r[q], nt2, cnt);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.t_empty[tb]);
+      }
+      const uint32_t tot = cnt[0] + cnt[1] + cnt[2] + cnt[3];
+      if (t < T && tot)
+        atomicAdd(&upper[static_cast<int64_t>(c) * Tg8 + t], static_cast<int32_t>(tot));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTcTmemCols));
   }
 }
 
@@ -1181,14 +1594,37 @@ int score_int_pairs() {
   return v;
 }
 
+// The FFMA2 kernel is the default: measured on B200 (config 2, 8 frames per
+// call) it scores in 0.149 ms vs 0.183 ms for score_tc_kernel -- a kind::tf32
+// MMA of 128 x 256 x 8 keeps the tensor pipe busy ~470 cycles, so the tensor
+// path caps near 70 evals/cycle/SM while its epilogue still needs one ALU
+// instruction per eval (profiles/r1c_summary.md). RVK_SCORE=tc selects it.
+bool score_uses_tc() {
+  static const bool v = [] {
+    const char* e = std::getenv("RVK_SCORE");
+    return e && std::strcmp(e, "tc") == 0;
+  }();
+  return v;
+}
+
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st) {
   if (f.n_clusters == 0) return;
   const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
-  cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  TcOut tc;
+  if (s.tc) {
+    tc.hyp = s.tc_hyp;
+    tc.pts = s.tc_pts;
+    tc.items = s.tc_items;
+    tc.count = s.tc_count;
+    tc.cap = f.n_clusters;
+    cudaMemsetAsync(s.tc_count, 0, sizeof(int32_t) * (kTcBuckets + 1), st);
+  } else {
+    cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  }
   prep_hyp_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap);
+      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc);
   count_launch();
 }
 
@@ -1220,6 +1656,26 @@ int score_grid(const ScoreGeom& g, int64_t max_tiles) {
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
+  if (s.tc) {
+    static int grid = 0;
+    if (grid == 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kTcSmemBytes));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_tc_kernel, kTcThreads,
+                                                    kTcSmemBytes);
+      grid = sms;  // one CTA per SM: it owns all 512 TMEM columns
+    }
+    const int64_t items = static_cast<int64_t>(f.n_clusters) * tc_blocks(p.max_trials);
+    const ScoreGeom g = score_geom(p.max_trials);
+    score_tc_kernel<<<static_cast<int>(std::min<int64_t>(grid, items)), kTcThreads, kTcSmemBytes,
+                      st>>>(s.tc_items, f.n_clusters, s.tc_count, s.tc_hyp, s.tc_pts,
+                            p.max_trials, g.Tg * 8, s.upper);
+    count_launch();
+    return;
+  }
   const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
   const int64_t max_tiles = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
   const size_t smem = score_smem_bytes(g);

@@ -57,6 +57,23 @@ inline int64_t tile_capacity(const ScoreGeom& g, int64_t n_points, int32_t n_clu
   return static_cast<int64_t>(g.nhb) * (n_points / kScorePPT + n_clusters) + 1;
 }
 
+// Tensor-core scoring (score_tc_kernel): D[h][p] = A_h x_p + B_h y_p + C_h
+// for a block of kTcM hypotheses x up to kTcN points is ONE tcgen05.mma
+// kind::tf32 (K = 8) over split operands; the epilogue squares and counts.
+constexpr int kTcM = 128;         // hypotheses per block (MMA M, TMEM lanes)
+constexpr int kTcN = 256;         // points per block (MMA N, TMEM columns per buffer)
+constexpr int kTcBuckets = 32;    // item size classes (cluster size / 64), largest first
+constexpr int kTcRowBytes = 32;   // one K = 8 row of tf32 operands
+// one hypothesis block in HBM: the 4 KB operand tile + its 128 corridor bounds
+constexpr int kTcHypFloats = kTcM * 8 + kTcM;
+
+inline __host__ __device__ int tc_blocks(int T) { return (T + kTcM - 1) / kTcM; }
+// first operand row of cluster c in the point-tile array (16-row aligned,
+// room for the padding of every cluster before it)
+inline __host__ __device__ int64_t tc_row_base(int64_t offset_c, int c) {
+  return ((offset_c + 15) & ~int64_t{15}) + 32 * static_cast<int64_t>(c);
+}
+
 struct Scratch {
   double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
   float2* xy32 = nullptr;    // [P + 2C + 2] normalized (x, y), FP32, each cluster
@@ -68,6 +85,13 @@ struct Scratch {
   int4* tiles = nullptr;     // [kTileBuckets * tile_cap] scoring tile descriptors
   int32_t* tile_count = nullptr;  // [kTileBuckets + 1] tiles per bucket + claim counter (zeroed per call)
   int64_t tile_cap = 0;
+  // tensor-core scoring
+  float* tc_hyp = nullptr;     // [C][tc_blocks(T)][kTcHypFloats]: K-major operand tile
+                               // (4 KB) + squared corridor bound per hypothesis
+  float* tc_pts = nullptr;     // [P + 32C + 32] K-major operand rows (points), tc_row_base
+  int4* tc_items = nullptr;    // [kTcBuckets][C] (cluster, n, row base) by size class
+  int32_t* tc_count = nullptr; // [kTcBuckets + 1] per-class counts + claim counter (zeroed per call)
+  bool tc = false;             // scoring path: tensor cores (default) or FFMA2
 };
 
 struct Outputs {
@@ -88,7 +112,10 @@ void launch_mad_exact(const FrameDev& f, double threshold_scale, const Scratch& 
 // coefficients) + scoring-tile registration, one CTA per cluster.
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st);
-// Fast FP32 scoring: upper-bound inlier counts for every (cluster, trial).
+// Scoring path selection (RVK_SCORE=tc selects the tensor-core kernel; default FFMA2).
+bool score_uses_tc();
+// Upper-bound inlier counts for every (cluster, trial): tensor-core (tcgen05)
+// or FFMA2 scoring.
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);
 // Exact argmax (verifying every candidate that could win), winner mask,

@@ -8,6 +8,7 @@ exact (assert_estimates_close).
 """
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -320,3 +321,17 @@ def test_frame_stream_matches_host_api(gpu_lib, depth):
 def est_dtype():
     from paper_2012_12618_b200 import _native
     return _native.ESTIMATE_DTYPE
+
+
+def test_tensor_core_scoring_path_parity(gpu_lib):
+    """The tcgen05 scoring kernel (RVK_SCORE=tc) must give the same bytes:
+    the golden, C3 and full-size parity tests re-run in a child process with
+    that path selected (the selection is read once per process)."""
+    env = dict(os.environ, RVK_SCORE="tc")
+    r = subprocess.run(
+        [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+         os.path.join(ROOT, "tests", "test_gpu_parity.py"),
+         "-k", "golden or c3 or config1 or full_size or edge or batch_composition or smoke"],
+        capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
