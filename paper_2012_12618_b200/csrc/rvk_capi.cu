@@ -239,7 +239,7 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   const ScoreGeom g = score_geom(std::max(T, 1));
   const size_t C = static_cast<size_t>(n_clusters);
   s.xy64 = w.xy64.get<double2>(P);
-  s.xy32 = w.xy32.get<float2>(P + 2 * C + 2);
+  s.xy32 = w.xy32.get<float2>(P + 2 * C + 10);
   s.stat = w.thr.get<double4>(C);
   s.norm = w.norm.get<double>(4 * C);
   s.upper = w.upper.get<int32_t>(C * g.Tg * 8);

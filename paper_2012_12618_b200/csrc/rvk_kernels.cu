@@ -43,7 +43,6 @@ namespace {
 constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
 constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
-constexpr int kDefaultIntPairs = 0;  // see score_int_pairs()
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
 constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
@@ -640,14 +639,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     h[0] = f.A;
     h[8] = f.B;
     h[16] = f.C;
-    // K: -t2hi for the squared compare; for the integer compare (the last
-    // g.ni pairs of the group) 2*bits(thi) + 1, or 0 for inert trials
-    if ((t & 7) < 8 - 2 * g.ni) {
-      h[24] = -f.t2hi;
-    } else {
-      const uint32_t kb = f.thi > 0.f ? (__float_as_uint(f.thi) << 1) + 1u : 0u;
-      h[24] = __uint_as_float(kb);
-    }
+    h[24] = -f.t2hi;  // K: the squared compare's bound
     uc[t] = 0;
   }
   // scoring tiles of this cluster
@@ -732,44 +724,52 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kStages = 3;  // scoring tile ring depth
-
-struct ScoreShared {
-  uint64_t full[kStages];  // tile landed (expect_tx + bulk-copy bytes)
-  int4 desc[kStages];
-  int done[kStages];       // warps finished with the stage
-  int bstart[kTileBuckets + 1];
-};
-
-__host__ __device__ __forceinline__ size_t score_smem_bytes(const ScoreGeom& g) {
-  // [ScoreShared | hyps x kStages | points x kStages | 16 B read-ahead pad]
-  return 512 + kStages * (static_cast<size_t>(g.TS) * 128 + kScorePPT * 8) + 16;
+// The hot loop, persistent and warp-granular. Every warp claims scoring
+// units from the LPT-ordered unit list with an atomic counter (largest
+// first, so the tail is short); a unit = (cluster, 32 groups of 8
+// hypotheses, up to kScorePPT points). Lane j holds group j's 8 hypotheses
+// (A, B, C, K = -t2hi; four FFMA2 pairs) in registers and streams the
+// unit's points (staged in the warp's shared-memory slot) as float4
+// broadcast loads (two points each): per point and pair 3 FFMA2 (e = A x + (B y + C); g = e^2 - t2hi) and the sign
+// bit of g added to the count (LEA.HI). No shared memory and no CTA
+// barrier in the loop: the per-unit latency of one warp (claim, descriptor,
+// hypothesis loads) is covered by the other warps of the SM sub-partition.
+// Counts are upper bounds (guard band, see make_fast) and accumulate over
+// units with integer atomics (order-free, deterministic).
+// Unit index (LPT order) -> descriptor: binary search of the bucket starts.
+__device__ __forceinline__ int4 unit_desc(const int* bstart, const int4* __restrict__ tiles,
+                                          int64_t tile_cap, int u) {
+  int lo = 0, hi = kTileBuckets;  // bstart[lo] <= u < bstart[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (bstart[mid] <= u) lo = mid;
+    else hi = mid;
+  }
+  return tiles[lo * tile_cap + (u - bstart[lo])];
 }
 
-// The hot loop, persistent. Each CTA claims tiles from the LPT-ordered tile
-// list with an atomic counter (largest first, so the tail is short); a tile
-// = (cluster, up to kScorePPT points, TS groups of 8 hypotheses). Tiles
-// stream through a kStages-deep shared-memory ring: the points and the
-// hypothesis coefficients of a tile arrive by cp.async.bulk (TMA engine) on
-// the stage's mbarrier; the last warp to finish a stage claims the next tile
-// and refills it, so warps never wait for each other at a CTA barrier.
-// Thread (slice s, group j) scores its 8 hypotheses (four FFMA2 pairs)
-// against slice s of the tile's points, read as float4 broadcasts (two
-// points): per point and pair 3 FFMA2 (e = A x + (B y + C); g = e^2 - t2hi)
-// and the sign bit of g added to the count (LEA.HI). Counts are upper bounds
-// (guard band, see make_fast) and accumulate over tiles with integer atomics
-// (order-free, deterministic).
-template <int NI>
+// Stages a unit's points (an even-aligned run of float2 = (n + 1) / 2 float4)
+// into a warp's shared-memory slot: cp.async, 16 B per lane and step, one
+// commit group per unit.
+__device__ __forceinline__ void stage_points(float4* slot, const float2* __restrict__ xy32,
+                                             int4 d, int lane) {
+  const float4* src = reinterpret_cast<const float4*>(xy32 + d.y);
+  const int m2 = (d.z + 1) >> 1;
+  for (int i = lane; i < m2; i += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(slot + i)),
+                 "l"(src + i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
              ScoreGeom g, int32_t* __restrict__ upper) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  ScoreShared& sh = *reinterpret_cast<ScoreShared*>(smem);
-  auto hyps_at = [&](int st) { return reinterpret_cast<float*>(smem + 512 + st * g.TS * 128); };
-  auto pts_at = [&](int st) {
-    return reinterpret_cast<float4*>(smem + 512 + kStages * g.TS * 128 + st * kScorePPT * 8);
-  };
+  constexpr int kSlot = kScorePPT / 2 + 2;  // float4 per slot (+2: read-ahead slack)
+  __shared__ int bstart[kTileBuckets + 1];
+  // two point slots per warp: the current unit's and the next unit's (prefetch)
+  __shared__ __align__(16) float4 pts_s[kScoreThreads / 32][2][kSlot];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 32) {  // exclusive prefix of the bucket sizes
     int carry = 0;
@@ -781,66 +781,39 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
         const int u = __shfl_up_sync(0xffffffffu, incl, o);
         if (tid >= o) incl += u;
       }
-      if (b0 + tid < kTileBuckets) sh.bstart[b0 + tid] = carry + incl - v;
+      if (b0 + tid < kTileBuckets) bstart[b0 + tid] = carry + incl - v;
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (tid == 0) {
-      sh.bstart[kTileBuckets] = carry;
-      for (int s = 0; s < kStages; ++s) {
-        mbar_init(&sh.full[s], 1);
-        sh.done[s] = 0;
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (tid == 0) bstart[kTileBuckets] = carry;
   }
   __syncthreads();
-  const int total = sh.bstart[kTileBuckets];
-
-  // Claims the next tile (dynamic, in LPT order) and streams it into stage
-  // st; a negative cluster id marks "no more tiles".
-  int* next_tile = const_cast<int*>(tile_count) + kTileBuckets;
-  auto fetch = [&](int st) {
-    const int i = atomicAdd(next_tile, 1);
-    if (i >= total) {
-      sh.desc[st] = make_int4(-1, 0, 0, 0);
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sh.full[st]))
-                   : "memory");
-      return;
-    }
-    int bk = 0;
-    while (sh.bstart[bk + 1] <= i) ++bk;
-    const int4 d = tiles[bk * tile_cap + (i - sh.bstart[bk])];
-    sh.desc[st] = d;
-    const int ng = min(g.TS, g.Tg - d.w);
-    const uint32_t hb = static_cast<uint32_t>(ng) * 128u;
-    const uint32_t pb = static_cast<uint32_t>((d.z + 1) & ~1) * 8u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(&sh.full[st], hb + pb);
-    bulk_g2s(hyps_at(st), hyp + (static_cast<int64_t>(d.x) * g.Tg + d.w) * 32, hb, &sh.full[st]);
-    bulk_g2s(pts_at(st), xy32 + d.y, pb, &sh.full[st]);
-  };
-  if (tid == 0)
-    for (int s = 0; s < kStages; ++s) fetch(s);
-
-  const int slice = tid / g.TS;
-  const int j = tid - slice * g.TS;
-  const int warps = kScoreThreads / 32;
+  const int total = bstart[kTileBuckets];
+  int* next = const_cast<int*>(tile_count) + kTileBuckets;
+  int u = 0, un = 0;
+  if (lane == 0) {
+    u = atomicAdd(next, 1);
+    un = atomicAdd(next, 1);
+  }
+  u = __shfl_sync(0xffffffffu, u, 0);
+  int4 d = make_int4(0, 0, 0, 0);
+  int buf = 0;
+  if (u < total) {
+    d = unit_desc(bstart, tiles, tile_cap, u);
+    stage_points(pts_s[tid >> 5][0], xy32, d, lane);
+  }
 #pragma unroll 1
-  for (int k = 0;; ++k) {
-    const int st = k % kStages;
-    mbar_wait(&sh.full[st], (k / kStages) & 1);
-    const int4 d = sh.desc[st];
-    if (d.x < 0) break;
-    const bool active = j < g.Tg - d.w;
-    uint32_t cnt[kNH];
-#pragma unroll
-    for (int q = 0; q < kNH; ++q) cnt[q] = 0;
-    if (active) {
-      const float4* hp = reinterpret_cast<const float4*>(hyps_at(st) + j * 32);
-      float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
+  while (u < total) {
+    // 1. this unit's hypotheses: lane j holds group d.w + j (A, B, C, K x 8)
+    const int gi = d.w + lane;
+    const bool active = gi < g.Tg;
+    float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
+    {
+      const float4* hp = reinterpret_cast<const float4*>(
+          hyp + (static_cast<int64_t>(d.x) * g.Tg + (active ? gi : d.w)) * 32);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const float4 a = hp[h], bb = hp[2 + h], cc = hp[4 + h], kk = hp[6 + h];
+        const float4 a = __ldg(hp + h), bb = __ldg(hp + 2 + h), cc = __ldg(hp + 4 + h),
+                     kk = __ldg(hp + 6 + h);
         A[2 * h] = make_float2(a.x, a.y);
         A[2 * h + 1] = make_float2(a.z, a.w);
         B[2 * h] = make_float2(bb.x, bb.y);
@@ -850,69 +823,66 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
         T2[2 * h] = make_float2(kk.x, kk.y);
         T2[2 * h + 1] = make_float2(kk.z, kk.w);
       }
-      // this slice's points: an even-aligned, even-length share of the tile
-      const int len = ((d.z + g.S - 1) / g.S + 1) & ~1;
-      const int p0 = slice * len;
-      const int p1 = min(d.z, p0 + len);
-      const int m2 = p1 > p0 ? (p1 - p0 + 1) >> 1 : 0;
-      const float4* cp = pts_at(st) + (p0 >> 1);
-      // software-pipelined, two point pairs per iteration: the LDS.128 of
-      // the next pair is in flight while the current one is scored (reads
-      // past the slice stay inside the shared allocation and are unused)
-      // pairs pr < 4 - NI: squared compare (FFMA2) + sign count; the last NI
-      // pairs: integer compare of |e| against thi on the ALU pipe
-      // (sign of 2*bits(e) - (2*bits(thi) + 1)), balancing FMA and ALU work
-      auto score_pair = [&](const float4& v) {
-#pragma unroll
-        for (int pr = 0; pr < kNH / 2; ++pr) {
-          float2 e0 = __ffma2_rn(A[pr], make_float2(v.x, v.x),
-                                 __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
-          float2 e1 = __ffma2_rn(A[pr], make_float2(v.z, v.z),
-                                 __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
-          if (pr < kNH / 2 - NI) {
-            e0 = __ffma2_rn(e0, e0, T2[pr]);
-            e1 = __ffma2_rn(e1, e1, T2[pr]);
-            cnt[2 * pr] += __float_as_uint(e0.x) >> 31;
-            cnt[2 * pr + 1] += __float_as_uint(e0.y) >> 31;
-            cnt[2 * pr] += __float_as_uint(e1.x) >> 31;
-            cnt[2 * pr + 1] += __float_as_uint(e1.y) >> 31;
-          } else {
-            const uint32_t k0 = __float_as_uint(T2[pr].x), k1 = __float_as_uint(T2[pr].y);
-            cnt[2 * pr] += ((__float_as_uint(e0.x) << 1) - k0) >> 31;
-            cnt[2 * pr + 1] += ((__float_as_uint(e0.y) << 1) - k1) >> 31;
-            cnt[2 * pr] += ((__float_as_uint(e1.x) << 1) - k0) >> 31;
-            cnt[2 * pr + 1] += ((__float_as_uint(e1.y) << 1) - k1) >> 31;
-          }
-        }
-      };
-      float4 v0 = cp[0];
-      int q2 = 0;
-#pragma unroll 1
-      for (; q2 + 2 <= m2; q2 += 2) {
-        const float4 v1 = cp[q2 + 1];
-        score_pair(v0);
-        v0 = cp[q2 + 2];
-        score_pair(v1);
-      }
-      if (q2 < m2) score_pair(v0);
     }
-    // stage st consumed by this warp; the last warp refills it
+    // 2. the next unit (claimed one unit ago): descriptor + point prefetch,
+    //    and the claim after it
+    const int u_next = __shfl_sync(0xffffffffu, un, 0);
+    int4 dn = make_int4(0, 0, 0, 0);
+    if (u_next < total) {
+      dn = unit_desc(bstart, tiles, tile_cap, u_next);
+      stage_points(pts_s[tid >> 5][buf ^ 1], xy32, dn, lane);
+    } else {
+      asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+    }
+    if (lane == 0) un = atomicAdd(next, 1);
+    // 3. this unit's points have landed (all but the newest group)
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&sh.done[st], 1) == warps - 1) {
-        sh.done[st] = 0;
-        __threadfence_block();
-        fetch(st);
+
+    uint32_t cnt[kNH];
+#pragma unroll
+    for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+    auto score_pair = [&](const float4& v) {
+#pragma unroll
+      for (int pr = 0; pr < kNH / 2; ++pr) {
+        float2 e0 = __ffma2_rn(A[pr], make_float2(v.x, v.x),
+                               __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
+        float2 e1 = __ffma2_rn(A[pr], make_float2(v.z, v.z),
+                               __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
+        e0 = __ffma2_rn(e0, e0, T2[pr]);
+        e1 = __ffma2_rn(e1, e1, T2[pr]);
+        cnt[2 * pr] += __float_as_uint(e0.x) >> 31;
+        cnt[2 * pr + 1] += __float_as_uint(e0.y) >> 31;
+        cnt[2 * pr] += __float_as_uint(e1.x) >> 31;
+        cnt[2 * pr + 1] += __float_as_uint(e1.y) >> 31;
       }
+    };
+    // 4. broadcast LDS.128 (two points), two float4 per iteration, one ahead
+    const float4* cp = pts_s[tid >> 5][buf];
+    const int m2 = (d.z + 1) >> 1;
+    float4 v0 = cp[0], v1 = cp[1];
+    int q2 = 0;
+#pragma unroll 1
+    for (; q2 + 2 <= m2; q2 += 2) {
+      const float4 v2 = cp[q2 + 2], v3 = cp[q2 + 3];
+      score_pair(v0);
+      score_pair(v1);
+      v0 = v2;
+      v1 = v3;
     }
+    if (q2 < m2) score_pair(v0);
     if (active) {
-      int32_t* up = upper + (static_cast<int64_t>(d.x) * g.Tg + d.w + j) * 8;
+      int32_t* up = upper + (static_cast<int64_t>(d.x) * g.Tg + gi) * 8;
 #pragma unroll
       for (int q = 0; q < kNH; ++q)
         if (cnt[q]) atomicAdd(&up[q], static_cast<int32_t>(cnt[q]));
     }
+    __syncwarp();  // this slot is refilled two units from now
+    u = u_next;
+    d = dn;
+    buf ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---------------------------------------------------- tensor-core scoring
@@ -1584,16 +1554,6 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
   count_launch();
 }
 
-// Trial pairs per group scored with the integer compare (RVK_SCORE_NI, 0..2).
-int score_int_pairs() {
-  static const int v = [] {
-    const char* e = std::getenv("RVK_SCORE_NI");
-    const int x = e ? std::atoi(e) : kDefaultIntPairs;
-    return x < 0 ? 0 : (x > 2 ? 2 : x);
-  }();
-  return v;
-}
-
 // The FFMA2 kernel is the default: measured on B200 (config 2, 8 frames per
 // call) it scores in 0.149 ms vs 0.183 ms for score_tc_kernel -- a kind::tf32
 // MMA of 128 x 256 x 8 keeps the tensor pipe busy ~470 cycles, so the tensor
@@ -1610,7 +1570,7 @@ bool score_uses_tc() {
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
+  const ScoreGeom g = score_geom(p.max_trials);
   TcOut tc;
   if (s.tc) {
     tc.hyp = s.tc_hyp;
@@ -1629,27 +1589,19 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
 }
 
 namespace {
-// Persistent grid: every SM filled to the occupancy the tile's shared memory
-// allows (queried once per shared-memory size).
-template <int NI>
-int score_grid(const ScoreGeom& g, int64_t max_tiles) {
-  static int sms = 0;
-  static size_t cached_smem = 0;
-  static int per_sm = 0;
-  const size_t smem = score_smem_bytes(g);
-  if (sms == 0) {
-    int dev = 0;
+// Persistent grid: every SM filled to the scoring kernel's occupancy.
+int score_grid(int64_t max_units) {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(score_kernel<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(score_smem_bytes(score_geom(1 << 20))));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, 0);
+    grid = sms * std::max(per_sm, 1);
   }
-  if (smem != cached_smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<NI>, kScoreThreads, smem);
-    cached_smem = smem;
-  }
-  const int64_t grid = static_cast<int64_t>(sms) * std::max(per_sm, 1);
-  return static_cast<int>(std::max<int64_t>(1, std::min(grid, max_tiles)));
+  const int64_t warps_per_cta = kScoreThreads / 32;
+  return static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + warps_per_cta - 1) / warps_per_cta)));
 }
 }  // namespace
 
@@ -1676,22 +1628,10 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
     count_launch();
     return;
   }
-  const ScoreGeom g = score_geom(p.max_trials, score_int_pairs());
-  const int64_t max_tiles = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
-  const size_t smem = score_smem_bytes(g);
-  switch (g.ni) {
-    case 1:
-      score_kernel<1><<<score_grid<1>(g, max_tiles), kScoreThreads, smem, st>>>(
-          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
-      break;
-    case 2:
-      score_kernel<2><<<score_grid<2>(g, max_tiles), kScoreThreads, smem, st>>>(
-          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
-      break;
-    default:
-      score_kernel<0><<<score_grid<0>(g, max_tiles), kScoreThreads, smem, st>>>(
-          s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
-  }
+  const ScoreGeom g = score_geom(p.max_trials);
+  const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
+  score_kernel<<<score_grid(max_units), kScoreThreads, 0, st>>>(s.tile_count, s.tiles, s.tile_cap,
+                                                                s.xy32, s.hyp, g, s.upper);
   count_launch();
 }
 

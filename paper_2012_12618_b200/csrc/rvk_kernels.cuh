@@ -24,31 +24,27 @@ struct FrameDev {
 };
 
 // Scoring geometry for a given max_trials T (host and device agree on it).
-// Hypotheses are processed in groups of 8 (one scoring thread each); a
-// scoring CTA of kScoreThreads threads covers TS groups x S point slices.
+// Hypotheses are processed in groups of 8 (one scoring lane each); a scoring
+// unit is one warp's work: kUnitGroups groups (256 hypotheses) of one cluster
+// against up to kScorePPT of its points.
 constexpr int kScoreThreads = 256;
-constexpr int kScorePPT = 512;                   // points per scoring tile (max)
-constexpr int kTileBuckets = kScorePPT / 8 + 1;   // 0: full tiles; 1..64: by size, descending
+constexpr int kUnitGroups = 32;                   // groups of 8 hypotheses per unit (one per lane)
+constexpr int kScorePPT = 256;                    // points per scoring unit (max)
+constexpr int kTileBuckets = kScorePPT / 4 + 1;   // 0: full units; 1..64: by size, descending
 
 struct ScoreGeom {
   int T = 0;    // max_trials
   int Tg = 0;   // hypothesis groups of 8 per cluster
-  int TS = 0;   // groups per tile (power of two <= kScoreThreads)
-  int S = 0;    // point slices per tile = kScoreThreads / TS
+  int TS = 0;   // groups per unit (kUnitGroups)
   int nhb = 0;  // hypothesis blocks per cluster = ceil(Tg / TS)
-  int ni = 0;   // trial pairs (of 4 per group) scored with the integer compare
 };
 
-inline __host__ __device__ ScoreGeom score_geom(int T, int ni = 0) {
+inline __host__ __device__ ScoreGeom score_geom(int T) {
   ScoreGeom g;
   g.T = T;
-  g.ni = ni;
   g.Tg = (T + 7) / 8;
-  int ts = 1;
-  while (ts < g.Tg && ts < kScoreThreads) ts <<= 1;
-  g.TS = ts;
-  g.S = kScoreThreads / ts;
-  g.nhb = (g.Tg + ts - 1) / ts;
+  g.TS = kUnitGroups;
+  g.nhb = (g.Tg + g.TS - 1) / g.TS;
   return g;
 }
 
@@ -76,8 +72,9 @@ inline __host__ __device__ int64_t tc_row_base(int64_t offset_c, int c) {
 
 struct Scratch {
   double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
-  float2* xy32 = nullptr;    // [P + 2C + 2] normalized (x, y), FP32, each cluster
-                             // starting at an even index, odd sizes padded
+  float2* xy32 = nullptr;    // [P + 2C + 10] normalized (x, y), FP32, each cluster
+                             // starting at an even index, odd sizes padded (+8
+                             // slack: the scoring loop reads ahead)
   double4* stat = nullptr;   // [C] (thr_lo, thr_hi, median, thr_exact|NaN)
   double* norm = nullptr;    // [4C] (offset_az, offset_dop, scale_az, scale_dop)
   int32_t* upper = nullptr;  // [C*Tg*8] fast-pass upper-bound counts

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
   printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
@@ -33,13 +34,17 @@ __device__ __forceinline__ void init_h(Hy& h, uint32_t base) {
 // V=0: per point, per pair: B-step, A-step, square (production shape)
 // V=1: per point pair: all B-steps, then all A-steps, then squares
 // V=2: point-pair packing: smem float4 (x1,x2,y1,y2); hypothesis scalars
+__device__ float4 g_pts[64][kPts / 2];  // V=4: points in global memory (L1-cached broadcast)
+
 template <int V, int TH, int MINB, int UNR>
 __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
-  __shared__ float4 pts[kPts / 2];
-  for (int i = threadIdx.x; i < kPts / 2; i += blockDim.x) {
-    const uint32_t s = blockIdx.x * 7919u + i * 4u;
-    pts[i] = make_float4(u01(s), u01(s + 1), u01(s + 2), u01(s + 3));
-  }
+  __shared__ float4 pts_s[V == 4 ? 1 : kPts / 2];
+  float4* pts = V == 4 ? g_pts[blockIdx.x & 63] : pts_s;
+  if (V != 4)
+    for (int i = threadIdx.x; i < kPts / 2; i += blockDim.x) {
+      const uint32_t s = blockIdx.x * 7919u + i * 4u;
+      pts[i] = make_float4(u01(s), u01(s + 1), u01(s + 2), u01(s + 3));
+    }
   Hy h;
   init_h(h, (blockIdx.x * TH + threadIdx.x) * 64u);
   uint32_t cnt[8];
@@ -49,8 +54,8 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
   for (int r = 0; r < reps; ++r) {
 #pragma unroll UNR
     for (int i = 0; i < kPts / 2; ++i) {
-      const float4 v = pts[i];
-      if (V == 0) {
+      const float4 v = V == 4 ? __ldg(&pts[i]) : pts[i];
+      if (V == 0 || V == 4) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float2 e = __ffma2_rn(h.A[q], make_float2(v.x, v.x), __ffma2_rn(h.B[q], make_float2(v.y, v.y), h.C[q]));
@@ -166,6 +171,14 @@ int main() {
   const float mp = time_ms([&] { ffma3_peak<<<pb, 256>>>(iters, 0.9999f, 1e-7f, df); });
   const double peak = double(pb) * 256 * iters * 16 * 2 / (mp * 1e-3);
   printf("{\"ffma_peak_tflops\": %.2f}\n", peak / 1e12);
+  {
+    std::vector<float4> h(64 * (kPts / 2));
+    for (size_t i = 0; i < h.size(); ++i) h[i] = make_float4(0.1f * (i % 7), 0.2f, 0.3f * (i % 3), 0.4f);
+    CK(cudaMemcpyToSymbol(g_pts, h.data(), h.size() * sizeof(float4)));
+  }
+  run<4, 256, 2, 2>(sms, peak, du);
+  run<4, 256, 3, 2>(sms, peak, du);
+  run<4, 128, 6, 2>(sms, peak, du);
   run<0, 256, 2, 2>(sms, peak, du);
   run<3, 256, 3, 1>(sms, peak, du);
   run<3, 256, 2, 1>(sms, peak, du);
