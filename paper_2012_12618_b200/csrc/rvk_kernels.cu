@@ -44,7 +44,6 @@ constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
 constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
-constexpr int kSortCap = 2048;    // clusters up to this size sort in shared memory
 
 // ---------------------------------------------------------------- helpers
 
@@ -208,18 +207,20 @@ __device__ unsigned long long block_radix_select(const unsigned long long* keys,
   return prefix;
 }
 
-constexpr int kMedBins = 2048;  // value buckets of [0, 1] for the median
+constexpr int kMedBins = 2048;  // value buckets of [0, 1] for the median (maximum)
 constexpr int kCandCap = 512;   // candidates ranked directly
 
-__device__ __forceinline__ int med_bin(unsigned long long key) {
+// nb: a power of two <= kMedBins, so y * nb is exact and the map monotone
+__device__ __forceinline__ int med_bin(unsigned long long key, int nb) {
   const double y = __longlong_as_double(static_cast<long long>(key));
-  const int b = static_cast<int>(y * kMedBins);  // exact scaling; y in [0, 1]
-  return b < kMedBins - 1 ? b : kMedBins - 1;
+  const int b = static_cast<int>(y * nb);  // exact scaling; y in [0, 1]
+  return b < nb - 1 ? b : nb - 1;
 }
 
 struct PrepShared {
-  unsigned long long keys[kSortCap];  // normalized dopplers (bit patterns, sign cleared)
-  double xs[kSortCap];                // normalized azimuths
+  unsigned long long* keys;  // [cap] normalized dopplers (bit patterns, sign cleared), dynamic smem
+  double* xs;                // [cap] normalized azimuths, dynamic smem
+  int cap;                   // clusters up to this size are kept in shared memory
   unsigned long long cand[kCandCap];
   unsigned int hist[kMedBins];
   double red[32];
@@ -236,13 +237,17 @@ struct PrepShared {
 __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
                                   unsigned long long& v0, unsigned long long& v1) {
   const int nt = blockDim.x, tid = threadIdx.x;
-  for (int i = tid; i < kMedBins; i += nt) sm.hist[i] = 0;
+  // about one bucket per point (small clusters scan few empty buckets), at
+  // least one per thread
+  int nb = nt;
+  while (nb < n && nb < kMedBins) nb <<= 1;
+  for (int i = tid; i < nb; i += nt) sm.hist[i] = 0;
   if (tid == 0) sm.sh[2] = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += nt) atomicAdd(&sm.hist[med_bin(sm.keys[i])], 1u);
+  for (int i = tid; i < n; i += nt) atomicAdd(&sm.hist[med_bin(sm.keys[i], nb)], 1u);
   __syncthreads();
   // bin holding rank k: thread j owns bins [j*per, (j+1)*per)
-  const int per = kMedBins / nt;  // nt divides kMedBins (256 threads)
+  const int per = nb / nt;  // both powers of two, nb >= nt
   unsigned int local = 0;
   for (int q = 0; q < per; ++q) local += sm.hist[tid * per + q];
   const int lane = tid & 31, warp = tid >> 5;
@@ -281,7 +286,7 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
   }
   for (int i = tid; i < n; i += nt) {
     const unsigned long long key = sm.keys[i];
-    if (med_bin(key) == bin) sm.cand[atomicAdd(reinterpret_cast<unsigned int*>(&sm.sh[2]), 1u)] = key;
+    if (med_bin(key, nb) == bin) sm.cand[atomicAdd(reinterpret_cast<unsigned int*>(&sm.sh[2]), 1u)] = key;
   }
   const bool second_in_bin = pair && k + 1 < below + in_bin;
   __syncthreads();
@@ -302,7 +307,7 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
     unsigned long long m = ~0ull;
     for (int i = tid; i < n; i += nt) {
       const unsigned long long key = sm.keys[i];
-      if (med_bin(key) > bin && key < m) m = key;
+      if (med_bin(key, nb) > bin && key < m) m = key;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -405,7 +410,7 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
   hi1 = first_zero(hi1, dop + b, n, sm.red);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
-  const bool in_smem = n <= kSortCap;
+  const bool in_smem = n <= sm.cap;
   float2* p32 = xy32 + xy32_base(offsets, c);
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
@@ -469,8 +474,12 @@ __global__ void __launch_bounds__(kPrepThreads)
 prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
             const double* __restrict__ az, const double* __restrict__ dop, double scale,
             double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
-            double* __restrict__ norm) {
+            double* __restrict__ norm, int cap) {
   __shared__ PrepShared sm;
+  extern __shared__ __align__(16) unsigned char prep_dyn[];
+  sm.keys = reinterpret_cast<unsigned long long*>(prep_dyn);
+  sm.xs = reinterpret_cast<double*>(prep_dyn + 8 * cap);
+  sm.cap = cap;
   prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
 }
 
@@ -560,8 +569,12 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
                 float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
                 int32_t* __restrict__ upper, int4* __restrict__ tiles,
-                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc) {
+                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc, int cap) {
   __shared__ PrepShared sm;
+  extern __shared__ __align__(16) unsigned char prep_dyn[];
+  sm.keys = reinterpret_cast<unsigned long long*>(prep_dyn);
+  sm.xs = reinterpret_cast<double*>(prep_dyn + 8 * cap);
+  sm.cap = cap;
   __shared__ int tile_pos[2];
   const int c = blockIdx.x;
   prep_cluster(sm, c, offsets, az, dop, scale, xy64, xy32, stat, nullptr);
@@ -580,7 +593,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       float* tile = pts + (k & ~(kTcN - 1)) * 8;
       if (k >= n) {
         tc_store_inert_point(tile, k & (kTcN - 1));
-      } else if (n <= kSortCap) {
+      } else if (n <= sm.cap) {
         tc_store_point(tile, k & (kTcN - 1), sm.xs[k],
                        __longlong_as_double(static_cast<long long>(sm.keys[k])));
       } else {
@@ -596,7 +609,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
         int i, j;
         seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
         double2 p, q;
-        if (n <= kSortCap) {
+        if (n <= sm.cap) {
           p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
           q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
         } else {
@@ -626,7 +639,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       int i, j;
       seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
       double2 p, q;
-      if (n <= kSortCap) {  // normalized points are still in shared memory (y >= +0)
+      if (n <= sm.cap) {  // normalized points are still in shared memory (y >= +0)
         p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
         q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
       } else {
@@ -1403,13 +1416,35 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
     const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
     RefitAcc acc;
     bool und = false;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) {
-      const int d = H.L.degenerate ? kOut : classify(H, k, p32[k], p64, thr_lo, thr_hi);
-      und |= d == kUndecided;
-      cmask[k] = d == kIn ? 1 : 0;
-      if (d == kIn) {
-        if (refit) acc.add(k, caz[k], cdop[k]);
-        else ++acc.nin;
+    const int nt = blockDim.x;
+    // four points per thread and step, every load issued before the first
+    // use (the loop is latency-bound: few points per thread, one CTA per
+    // cluster)
+    for (int k0 = threadIdx.x; k0 < n; k0 += 4 * nt) {
+      float2 pp[4];
+      double pa[4], pd[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * nt;
+        if (k < n) {
+          pp[u] = p32[k];
+          if (refit) {
+            pa[u] = caz[k];
+            pd[u] = cdop[k];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * nt;
+        if (k >= n) break;
+        const int d = H.L.degenerate ? kOut : classify(H, k, pp[u], p64, thr_lo, thr_hi);
+        und |= d == kUndecided;
+        cmask[k] = d == kIn ? 1 : 0;
+        if (d == kIn) {
+          if (refit) acc.add(k, pa[u], pd[u]);
+          else ++acc.nin;
+        }
       }
     }
     if (__syncthreads_or(und)) return false;
@@ -1423,7 +1458,18 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
 
   // 1. trial with the largest upper bound (lowest index on ties).
   unsigned long long v = 0;
-  for (int t = threadIdx.x; t < T; t += blockDim.x) v = MaxU64()(v, pack_best(U[t], t));
+  {
+    // U rows are padded to a multiple of 8 trials (16 B aligned): int4 loads
+    const int4* U4 = reinterpret_cast<const int4*>(U);
+    for (int q = threadIdx.x; 4 * q < T; q += blockDim.x) {
+      const int4 w = U4[q];
+      const int t = 4 * q;
+      v = MaxU64()(v, pack_best(w.x, t));
+      if (t + 1 < T) v = MaxU64()(v, pack_best(w.y, t + 1));
+      if (t + 2 < T) v = MaxU64()(v, pack_best(w.z, t + 2));
+      if (t + 3 < T) v = MaxU64()(v, pack_best(w.w, t + 3));
+    }
+  }
   v = block_reduce(v, MaxU64(), redu);
   const int t0 = unpack_trial(v);
   const int u0 = unpack_count(v);
@@ -1539,11 +1585,36 @@ __global__ void seed_pairs_kernel(const int64_t* __restrict__ offsets,
 
 // ---------------------------------------------------------------- launchers
 
+// Per-cluster CTA shape: many small clusters run best with small CTAs (more
+// clusters in flight per SM, fewer threads idling at every block barrier);
+// large ones with 256 threads. Chosen from the mean cluster size; the
+// kernels are correct for any cluster size at any shape (clusters larger
+// than the shared-memory cap take the global-memory selection path).
+struct CtaShape {
+  int threads;
+  int cap;  // shared-memory sort capacity (points)
+};
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+// Measured on B200 (profiles/r1d_summary.md): prep wants 128 threads for
+// clusters of ~200 points and 256 above ~400; select wants 64 for ~200 points.
+CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env, bool select) {
+  const int64_t avg = n_clusters ? n_points / n_clusters : 0;
+  int t = avg < 384 ? (select ? 64 : 128) : 256;
+  t = env_int(env, t);
+  t = t <= 64 ? 64 : (t <= 128 ? 128 : 256);
+  return {t, t * 8};
+}
+size_t prep_dyn_bytes(int cap) { return static_cast<size_t>(cap) * 16; }
+
 void launch_prep(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  prep_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(f.n_clusters, f.offsets, f.azimuth,
-                                                      f.doppler, scale, s.xy64, s.xy32, s.stat,
-                                                      s.norm);
+  const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
+  prep_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
+      f.n_clusters, f.offsets, f.azimuth, f.doppler, scale, s.xy64, s.xy32, s.stat, s.norm,
+      sh.cap);
   count_launch();
 }
 
@@ -1582,9 +1653,10 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
   } else {
     cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
   }
-  prep_hyp_kernel<<<f.n_clusters, kPrepThreads, 0, st>>>(
+  const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
+  prep_hyp_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc);
+      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, sh.cap);
   count_launch();
 }
 
@@ -1638,7 +1710,8 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
 void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                    const Outputs& o, cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  select_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
+  const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_SELECT_THREADS", true);
+  select_kernel<<<f.n_clusters, sh.threads, 0, st>>>(
       f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
       p.threshold_scale, s.upper, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial,
       o.mask, o.est);

@@ -323,15 +323,20 @@ def est_dtype():
     return _native.ESTIMATE_DTYPE
 
 
-def test_tensor_core_scoring_path_parity(gpu_lib):
-    """The tcgen05 scoring kernel (RVK_SCORE=tc) must give the same bytes:
-    the golden, C3 and full-size parity tests re-run in a child process with
-    that path selected (the selection is read once per process)."""
-    env = dict(os.environ, RVK_SCORE="tc")
+@pytest.mark.parametrize("env", [{"RVK_SCORE": "tc"},
+                                 {"RVK_PREP_THREADS": "256", "RVK_SELECT_THREADS": "256"},
+                                 {"RVK_PREP_THREADS": "64", "RVK_SELECT_THREADS": "64"}],
+                         ids=["tensor_core_scoring", "cta256", "cta64"])
+def test_alternative_kernel_shapes_parity(gpu_lib, env):
+    """Every kernel variant must give the same bytes: the tcgen05 scoring
+    kernel (RVK_SCORE=tc) and the per-cluster CTA shapes of prep/select
+    (normally chosen from the mean cluster size). The golden, C3 and
+    full-size parity tests re-run in a child process with the variant
+    selected (selections are read once per process)."""
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
          os.path.join(ROOT, "tests", "test_gpu_parity.py"),
-         "-k", "golden or c3 or config1 or full_size or edge or batch_composition or smoke"],
-        capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+         "-k", "golden or c3 or config1 or full_size or edge or batch_composition or radar"],
+        capture_output=True, text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
