@@ -94,7 +94,7 @@ struct HostBuf {
 // Device scratch of one stream's in-flight pipeline.
 struct Workspace {
   DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, tile_count, aux;
-  DevBuf tc_hyp, tc_pts, tc_items, tc_count;
+  DevBuf tc_hyp, tc_pts, tc_items, tc_count, big;
 };
 
 struct Context {
@@ -255,6 +255,8 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
     s.tile_cap = tile_capacity(g, P, n_clusters);
     s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
     s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
+    s.big_ctl = w.big.get<int32_t>(C + 8);
+    s.big_list = s.big_ctl + 8;
   }
   return s;
 }
@@ -918,7 +920,7 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
       if (sl.done) cudaEventDestroy(sl.done);
       for (DevBuf* b : {&sl.in, &sl.out, &sl.ws.xy64, &sl.ws.xy32, &sl.ws.thr, &sl.ws.norm,
                         &sl.ws.upper, &sl.ws.hyp, &sl.ws.tiles, &sl.ws.tile_count, &sl.ws.aux,
-                        &sl.ws.tc_hyp, &sl.ws.tc_pts, &sl.ws.tc_items,
+                        &sl.ws.tc_hyp, &sl.ws.tc_pts, &sl.ws.tc_items, &sl.ws.big,
                         &sl.ws.tc_count})
         if (b->p) cudaFree(b->p);
       for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out})

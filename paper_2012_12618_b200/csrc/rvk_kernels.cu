@@ -144,17 +144,17 @@ __device__ double block_select_y(const double2* xy, int n, int k,
 // ------------------------------------------------------------- prep kernel
 
 // k-th smallest (0-based) of n non-negative doubles given as bit patterns in
-// shared memory: MSD radix select with 11-bit digits (6 passes), exact.
-// hist: 2048 counters; sh: 2 ints of scratch. Fallback of block_select_pair.
+// shared memory: MSD radix select with `bits`-bit digits (11: 6 passes over
+// 2048 counters, 8: 8 passes over 256), exact. hist: 2^bits counters; sh: 2
+// ints of scratch. Fallback of block_select_pair.
 __device__ unsigned long long block_radix_select(const unsigned long long* keys, int n, int k,
-                                                 unsigned int* hist, int* sh) {
+                                                 unsigned int* hist, int* sh, int bits) {
   unsigned long long prefix = 0, mask = 0;
   const int nt = blockDim.x;
 #pragma unroll 1
-  for (int pass = 0; pass < 6; ++pass) {
-    const int shift = pass < 5 ? 53 - 11 * pass : 0;
-    const int bits = pass < 5 ? 11 : 9;
-    const unsigned int nb = 1u << bits;
+  for (int top = 64; top > 0; top -= bits) {
+    const int shift = top > bits ? top - bits : 0;
+    const unsigned int nb = 1u << (top - shift);
     for (int i = threadIdx.x; i < (int)nb; i += nt) hist[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += nt) {
@@ -208,7 +208,7 @@ __device__ unsigned long long block_radix_select(const unsigned long long* keys,
 }
 
 constexpr int kMedBins = 2048;  // value buckets of [0, 1] for the median (maximum)
-constexpr int kCandCap = 512;   // candidates ranked directly
+constexpr int kCandCap = 512;   // candidates ranked directly (maximum)
 
 // nb: a power of two <= kMedBins, so y * nb is exact and the map monotone
 __device__ __forceinline__ int med_bin(unsigned long long key, int nb) {
@@ -217,12 +217,18 @@ __device__ __forceinline__ int med_bin(unsigned long long key, int nb) {
   return b < nb - 1 ? b : nb - 1;
 }
 
+// Dynamic shared memory of the prep kernels, sized per launch from the
+// sort capacity (prep_smem_layout): [keys: cap][cand: candcap][hist: histcap].
+struct PrepShared;
+__device__ void prep_smem_setup(PrepShared& sm, unsigned char* dyn, int cap);
+
 struct PrepShared {
-  unsigned long long* keys;  // [cap] normalized dopplers (bit patterns, sign cleared), dynamic smem
-  double* xs;                // [cap] normalized azimuths, dynamic smem
+  unsigned long long* keys;  // [cap] normalized dopplers (bit patterns, sign cleared)
+  unsigned long long* cand;  // [candcap] candidates of the median bucket
+  unsigned int* hist;        // [histcap] bucket / radix counters (>= 256)
   int cap;                   // clusters up to this size are kept in shared memory
-  unsigned long long cand[kCandCap];
-  unsigned int hist[kMedBins];
+  int candcap;
+  int histcap;               // 2048: 11-bit radix digits, else 8-bit
   double red[32];
   double4 red4[32];
   unsigned long long sel[2];
@@ -230,6 +236,26 @@ struct PrepShared {
   unsigned int wsum[32];
   double4 stat;
 };
+
+__host__ __device__ inline int prep_histcap(int cap) {
+  if (cap >= 1024) return kMedBins;
+  int h = 256;
+  while (h < cap) h <<= 1;
+  return h;
+}
+__host__ __device__ inline int prep_candcap(int cap) { return cap < kCandCap ? cap : kCandCap; }
+__host__ __device__ inline size_t prep_dyn_bytes(int cap) {
+  return static_cast<size_t>(cap) * 8 + static_cast<size_t>(prep_candcap(cap)) * 8 +
+         static_cast<size_t>(prep_histcap(cap)) * 4;
+}
+__device__ void prep_smem_setup(PrepShared& sm, unsigned char* dyn, int cap) {
+  sm.cap = cap;
+  sm.candcap = prep_candcap(cap);
+  sm.histcap = prep_histcap(cap);
+  sm.keys = reinterpret_cast<unsigned long long*>(dyn);
+  sm.cand = sm.keys + cap;
+  sm.hist = reinterpret_cast<unsigned int*>(sm.cand + sm.candcap);
+}
 
 // The k-th and (k+1)-th smallest keys (k+1 only if `pair`), exact. Keys are
 // bucketed by value (a monotone map), the bucket holding rank k is collected
@@ -240,7 +266,7 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
   // about one bucket per point (small clusters scan few empty buckets), at
   // least one per thread
   int nb = nt;
-  while (nb < n && nb < kMedBins) nb <<= 1;
+  while (nb < n && nb < sm.histcap) nb <<= 1;
   for (int i = tid; i < nb; i += nt) sm.hist[i] = 0;
   if (tid == 0) sm.sh[2] = 0;
   __syncthreads();
@@ -279,9 +305,10 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
   const int bin = sm.sh[0];
   const int below = sm.sh[1];
   const int in_bin = static_cast<int>(sm.hist[bin]);
-  if (in_bin > kCandCap) {  // crowded bucket: exact radix select
-    v0 = block_radix_select(sm.keys, n, k, sm.hist, sm.sh);
-    if (pair) v1 = block_radix_select(sm.keys, n, k + 1, sm.hist, sm.sh);
+  if (in_bin > sm.candcap) {  // crowded bucket: exact radix select
+    const int bits = sm.histcap >= 2048 ? 11 : 8;
+    v0 = block_radix_select(sm.keys, n, k, sm.hist, sm.sh, bits);
+    if (pair) v1 = block_radix_select(sm.keys, n, k + 1, sm.hist, sm.sh, bits);
     return;
   }
   for (int i = tid; i < n; i += nt) {
@@ -419,10 +446,8 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
     p32[k] = make_float2(__double2float_rn(x), __double2float_rn(y));
     // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
     // std::sort's operator< treats them; every other value is >= +0)
-    if (in_smem) {
+    if (in_smem)
       sm.keys[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
-      sm.xs[k] = x;
-    }
   }
   if (threadIdx.x == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);  // pad to even
   if (threadIdx.x == 0 && norm != nullptr) {
@@ -477,9 +502,7 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
             double* __restrict__ norm, int cap) {
   __shared__ PrepShared sm;
   extern __shared__ __align__(16) unsigned char prep_dyn[];
-  sm.keys = reinterpret_cast<unsigned long long*>(prep_dyn);
-  sm.xs = reinterpret_cast<double*>(prep_dyn + 8 * cap);
-  sm.cap = cap;
+  prep_smem_setup(sm, prep_dyn, cap);
   prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
 }
 
@@ -563,20 +586,15 @@ __device__ __forceinline__ float tc_store_hyp(float* tile, int row, double x1, d
 // and its scoring tiles (kScorePPT points x TS groups each) are appended to
 // the size bucket they belong to, so the scoring kernel takes them
 // largest-first.
-__global__ void __launch_bounds__(kPrepThreads)
-prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
-                const double* __restrict__ az, const double* __restrict__ dop, double scale,
-                const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
-                float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
-                int32_t* __restrict__ upper, int4* __restrict__ tiles,
-                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc, int cap) {
-  __shared__ PrepShared sm;
-  extern __shared__ __align__(16) unsigned char prep_dyn[];
-  sm.keys = reinterpret_cast<unsigned long long*>(prep_dyn);
-  sm.xs = reinterpret_cast<double*>(prep_dyn + 8 * cap);
-  sm.cap = cap;
-  __shared__ int tile_pos[2];
-  const int c = blockIdx.x;
+__device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
+                              const int64_t* __restrict__ offsets, const double* __restrict__ az,
+                              const double* __restrict__ dop, double scale,
+                              const int32_t* __restrict__ keys, const ScoreGeom& g,
+                              uint64_t seed, double2* xy64, float2* __restrict__ xy32,
+                              double4* __restrict__ stat, float* __restrict__ hyp,
+                              int32_t* __restrict__ upper, int4* __restrict__ tiles,
+                              int32_t* __restrict__ tile_count, int64_t tile_cap,
+                              const TcOut& tc) {
   prep_cluster(sm, c, offsets, az, dop, scale, xy64, xy32, stat, nullptr);
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
@@ -593,9 +611,6 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       float* tile = pts + (k & ~(kTcN - 1)) * 8;
       if (k >= n) {
         tc_store_inert_point(tile, k & (kTcN - 1));
-      } else if (n <= sm.cap) {
-        tc_store_point(tile, k & (kTcN - 1), sm.xs[k],
-                       __longlong_as_double(static_cast<long long>(sm.keys[k])));
       } else {
         const double2 q = p64[k];
         tc_store_point(tile, k & (kTcN - 1), q.x, q.y);
@@ -608,14 +623,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       if (t < g.T) {
         int i, j;
         seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-        double2 p, q;
-        if (n <= sm.cap) {
-          p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
-          q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
-        } else {
-          p = p64[i];
-          q = p64[j];
-        }
+        const double2 p = p64[i], q = p64[j];
         t2 = tc_store_hyp(tile, t % kTcM, p.x, p.y, q.x, q.y, thr_hi);
       } else {
         tc_store_row(tile, t % kTcM, make_float4(0.f, 0.f, 0.f, 0.f),
@@ -638,14 +646,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     if (t < g.T) {
       int i, j;
       seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-      double2 p, q;
-      if (n <= sm.cap) {  // normalized points are still in shared memory (y >= +0)
-        p = make_double2(sm.xs[i], __longlong_as_double(static_cast<long long>(sm.keys[i])));
-        q = make_double2(sm.xs[j], __longlong_as_double(static_cast<long long>(sm.keys[j])));
-      } else {
-        p = p64[i];
-        q = p64[j];
-      }
+      const double2 p = p64[i], q = p64[j];  // written by this CTA before the barrier
       f = make_fast_from_seeds(p.x, p.y, q.x, q.y, thr_lo, thr_hi);
     }
     float* h = hc + (t >> 3) * 32 + (t & 7);
@@ -672,6 +673,332 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const int bk = tile_bucket(rem);
     for (int hb = threadIdx.x; hb < g.nhb; hb += blockDim.x)
       tiles[bk * tile_cap + tile_pos[1] + hb] =
+          make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
+  }
+}
+
+// One CTA per cluster (big_list == nullptr), or persistent CTAs working
+// through the list of clusters the warp kernel left for them
+// (big_ctl[0] = count, big_ctl[1] = claim counter).
+__global__ void __launch_bounds__(kPrepThreads)
+prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                const double* __restrict__ az, const double* __restrict__ dop, double scale,
+                const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
+                float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
+                int32_t* __restrict__ upper, int4* __restrict__ tiles,
+                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc, int cap,
+                const int32_t* __restrict__ big_list, int32_t* big_ctl) {
+  __shared__ PrepShared sm;
+  extern __shared__ __align__(16) unsigned char prep_dyn[];
+  prep_smem_setup(sm, prep_dyn, cap);
+  __shared__ int tile_pos[2];
+  __shared__ int s_idx;
+  if (big_list == nullptr) {
+    prep_hyp_body(sm, tile_pos, blockIdx.x, offsets, az, dop, scale, keys, g, seed, xy64, xy32,
+                  stat, hyp, upper, tiles, tile_count, tile_cap, tc);
+    return;
+  }
+  for (;;) {
+    if (threadIdx.x == 0) s_idx = atomicAdd(&big_ctl[1], 1);
+    __syncthreads();
+    const int i = s_idx;
+    if (i >= *reinterpret_cast<volatile int32_t*>(&big_ctl[0])) break;
+    prep_hyp_body(sm, tile_pos, big_list[i], offsets, az, dop, scale, keys, g, seed, xy64, xy32,
+                  stat, hyp, upper, tiles, tile_count, tile_cap, tc);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------ warp-per-cluster prep
+//
+// Clusters of up to kWarpCap points (the common case of imaging-radar
+// frames: thousands of clusters of ~50-350 points) are prepared by ONE warp
+// each, with warp shuffles and __syncwarp instead of block barriers: the
+// same normalize_cluster / median / MAD interval / hypothesis setup / unit
+// registration as prep_hyp_body, bit for bit. Larger clusters are appended
+// to a list for the CTA kernel.
+constexpr int kWarpCap = 512;
+constexpr int kWarpCand = 128;
+constexpr int kPrepWarps = 6;  // 6 x 7 KB of static shared memory per CTA
+
+struct WarpPrep {
+  unsigned long long keys[kWarpCap];
+  unsigned long long cand[kWarpCand];
+  unsigned int hist[kWarpCap];
+};
+
+__device__ __forceinline__ double warp_fmin(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_imin(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_umin64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  return v;
+}
+// inclusive prefix sum over the warp
+__device__ __forceinline__ unsigned int warp_scan(unsigned int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+// The bits of the first element equal to zero (Eigen's first-occurrence
+// minCoeff/maxCoeff for +-0), as first_zero().
+__device__ __forceinline__ double warp_first_zero(double v, const double* __restrict__ a, int n,
+                                                  int lane) {
+  if (v != 0.0) return v;
+  int first = INT_MAX;
+  for (int k = lane; k < n; k += 32)
+    if (a[k] == 0.0) first = k < first ? k : first;
+  return a[warp_imin(first)];
+}
+// Rank `k` among `bins` counters split into per-lane runs of `per`:
+// returns (bin, count below the bin) on every lane.
+__device__ __forceinline__ void warp_find_rank(const unsigned int* hist, int per, int k, int lane,
+                                               int& bin, int& below) {
+  unsigned int local = 0;
+  for (int q = 0; q < per; ++q) local += hist[lane * per + q];
+  const unsigned int incl = warp_scan(local, lane);
+  const unsigned int excl = incl - local;
+  const unsigned int kk = static_cast<unsigned int>(k);
+  const bool mine = kk >= excl && kk < incl;
+  int b = 0, c = 0;
+  if (mine) {
+    unsigned int cum = excl;
+    for (int q = 0; q < per; ++q) {
+      const unsigned int h = hist[lane * per + q];
+      if (kk < cum + h) {
+        b = lane * per + q;
+        c = static_cast<int>(cum);
+        break;
+      }
+      cum += h;
+    }
+  }
+  const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+  bin = __shfl_sync(0xffffffffu, b, src);
+  below = __shfl_sync(0xffffffffu, c, src);
+}
+// k-th smallest key, MSD radix select with 8-bit digits (fallback for a
+// crowded median bucket).
+__device__ unsigned long long warp_radix_select(WarpPrep& w, int n, int k, int lane) {
+  unsigned long long prefix = 0, mask = 0;
+#pragma unroll 1
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) w.hist[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long key = w.keys[i];
+      if ((key & mask) == prefix) atomicAdd(&w.hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    int digit, below;
+    warp_find_rank(w.hist, 8, k, lane, digit, below);
+    prefix |= static_cast<unsigned long long>(digit) << shift;
+    mask |= 0xFFull << shift;
+    k -= below;
+    __syncwarp();
+  }
+  return prefix;
+}
+// k-th and (k+1)-th smallest keys, exact (warp version of block_select_pair).
+__device__ void warp_select_pair(WarpPrep& w, int n, int k, bool pair, int lane,
+                                 unsigned long long& v0, unsigned long long& v1) {
+  int nb = 32;
+  while (nb < n) nb <<= 1;  // <= kWarpCap buckets, about one per point
+  for (int i = lane; i < nb; i += 32) w.hist[i] = 0;
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) atomicAdd(&w.hist[med_bin(w.keys[i], nb)], 1u);
+  __syncwarp();
+  int bin, below;
+  warp_find_rank(w.hist, nb >> 5, k, lane, bin, below);
+  const int in_bin = static_cast<int>(w.hist[bin]);
+  if (in_bin > kWarpCand) {
+    __syncwarp();
+    v0 = warp_radix_select(w, n, k, lane);
+    if (pair) v1 = warp_radix_select(w, n, k + 1, lane);
+    return;
+  }
+  int cnt = 0;  // compact the bucket's keys (order irrelevant)
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned long long key = i < n ? w.keys[i] : 0ull;
+    const bool hit = i < n && med_bin(key, nb) == bin;
+    const unsigned int m = __ballot_sync(0xffffffffu, hit);
+    if (hit) w.cand[cnt + __popc(m & ((1u << lane) - 1u))] = key;
+    cnt += __popc(m);
+  }
+  __syncwarp();
+  const int r0 = k - below;
+  const bool second_in_bin = pair && k + 1 < below + in_bin;
+  unsigned long long s0 = 0, s1 = 0;
+  bool f0 = false, f1 = false;
+  for (int i = lane; i < in_bin; i += 32) {
+    const unsigned long long ci = w.cand[i];
+    int less = 0, eq = 0;
+    for (int j = 0; j < in_bin; ++j) {
+      const unsigned long long cj = w.cand[j];
+      less += cj < ci;
+      eq += cj == ci;
+    }
+    if (r0 >= less && r0 < less + eq) {
+      s0 = ci;
+      f0 = true;
+    }
+    if (second_in_bin && r0 + 1 >= less && r0 + 1 < less + eq) {
+      s1 = ci;
+      f1 = true;
+    }
+  }
+  v0 = __shfl_sync(0xffffffffu, s0, __ffs(__ballot_sync(0xffffffffu, f0)) - 1);
+  if (pair) {
+    if (second_in_bin) {
+      v1 = __shfl_sync(0xffffffffu, s1, __ffs(__ballot_sync(0xffffffffu, f1)) - 1);
+    } else {  // the smallest key above the bucket
+      unsigned long long m = ~0ull;
+      for (int i = lane; i < n; i += 32) {
+        const unsigned long long key = w.keys[i];
+        if (med_bin(key, nb) > bin && key < m) m = key;
+      }
+      v1 = warp_umin64(m);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kPrepWarps * 32)
+prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                 const double* __restrict__ az, const double* __restrict__ dop, double scale,
+                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
+                 float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
+                 int32_t* __restrict__ upper, int4* __restrict__ tiles,
+                 int32_t* __restrict__ tile_count, int64_t tile_cap, int32_t* __restrict__ big_list,
+                 int32_t* big_ctl) {
+  __shared__ WarpPrep wp[kPrepWarps];
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kPrepWarps + (threadIdx.x >> 5);
+  if (c >= n_clusters) return;
+  WarpPrep& w = wp[threadIdx.x >> 5];
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  if (n > kWarpCap) {
+    if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
+    return;
+  }
+  // normalize_cluster (src/ransac.cpp:69-87)
+  double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
+  for (int k = lane; k < n; k += 32) {
+    const double a = az[b + k], d = dop[b + k];
+    lo0 = a < lo0 ? a : lo0;
+    hi0 = a > hi0 ? a : hi0;
+    lo1 = d < lo1 ? d : lo1;
+    hi1 = d > hi1 ? d : hi1;
+  }
+  lo0 = warp_first_zero(warp_fmin(lo0), az + b, n, lane);
+  hi0 = warp_first_zero(-warp_fmin(-hi0), az + b, n, lane);
+  lo1 = warp_first_zero(warp_fmin(lo1), dop + b, n, lane);
+  hi1 = warp_first_zero(-warp_fmin(-hi1), dop + b, n, lane);
+  const double s0 = __dsub_rn(hi0, lo0);
+  const double s1 = __dsub_rn(hi1, lo1);
+  float2* p32 = xy32 + xy32_base(offsets, c);
+  for (int k0 = lane; k0 < n; k0 += 64) {  // two points per lane and step
+    const int k1 = k0 + 32;
+    const double a0 = az[b + k0], d0 = dop[b + k0];
+    const double a1 = k1 < n ? az[b + k1] : 0.0, d1 = k1 < n ? dop[b + k1] : 0.0;
+    const double x0 = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(a0, lo0), s0);
+    const double y0 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d0, lo1), s1);
+    const double x1 = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(a1, lo0), s0);
+    const double y1 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d1, lo1), s1);
+    xy64[b + k0] = make_double2(x0, y0);
+    p32[k0] = make_float2(__double2float_rn(x0), __double2float_rn(y0));
+    w.keys[k0] = static_cast<unsigned long long>(__double_as_longlong(y0)) & ~(1ull << 63);
+    if (k1 < n) {
+      xy64[b + k1] = make_double2(x1, y1);
+      p32[k1] = make_float2(__double2float_rn(x1), __double2float_rn(y1));
+      w.keys[k1] = static_cast<unsigned long long>(__double_as_longlong(y1)) & ~(1ull << 63);
+    }
+  }
+  if (lane == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);
+  __syncwarp();
+  // median (ransac.hpp:53-70) and the MAD interval (see prep_cluster)
+  const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
+  unsigned long long v0 = 0, v1 = 0;
+  warp_select_pair(w, n, k0, (n & 1) == 0, lane, v0, v1);
+  const double d0 = __longlong_as_double(static_cast<long long>(v0));
+  const double med = (n & 1) ? d0
+                             : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))), 2.0);
+  double part = 0.0;
+  for (int k = lane; k < n; k += 32)
+    part += fabs(__dsub_rn(__longlong_as_double(static_cast<long long>(w.keys[k])), med));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  const double mid = scale * (part / n);
+  const double delta = (4.0 * n + 16.0) * 0x1p-53;
+  const double thr_lo = mid * (1.0 - delta), thr_hi = mid * (1.0 + delta);
+  if (lane == 0) stat[c] = make_double4(thr_lo, thr_hi, med, CUDART_NAN);
+  // hypotheses (as prep_hyp_body, FFMA2 layout) and zeroed counters
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double2* p64 = xy64 + b;  // written by this warp before __syncwarp
+  float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
+  int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
+  // two trials per lane and step: both seed pairs' loads are in flight
+  // before the first FP64 line is built
+  for (int t0 = lane; t0 < g.Tg * 8; t0 += 64) {
+    const int t1 = t0 + 32;
+    const bool a0 = t0 < g.T, a1 = t1 < g.T;
+    int i0 = 0, j0 = 0, i1 = 0, j1 = 0;
+    if (a0) seed_pair(seed, key, static_cast<uint32_t>(t0), static_cast<uint32_t>(n), i0, j0);
+    if (a1) seed_pair(seed, key, static_cast<uint32_t>(t1), static_cast<uint32_t>(n), i1, j1);
+    const double2 p0 = p64[i0], q0 = p64[j0], p1 = p64[i1], q1 = p64[j1];
+    const FastHyp f0 = a0 ? make_fast_from_seeds(p0.x, p0.y, q0.x, q0.y, thr_lo, thr_hi)
+                          : inert_fast();
+    const FastHyp f1 = a1 ? make_fast_from_seeds(p1.x, p1.y, q1.x, q1.y, thr_lo, thr_hi)
+                          : inert_fast();
+    float* h = hc + (t0 >> 3) * 32 + (t0 & 7);
+    h[0] = f0.A;
+    h[8] = f0.B;
+    h[16] = f0.C;
+    h[24] = -f0.t2hi;
+    uc[t0] = 0;
+    if (t1 < g.Tg * 8) {
+      h = hc + (t1 >> 3) * 32 + (t1 & 7);
+      h[0] = f1.A;
+      h[8] = f1.B;
+      h[16] = f1.C;
+      h[24] = -f1.t2hi;
+      uc[t1] = 0;
+    }
+  }
+  // scoring units of this cluster
+  const int full = n / kScorePPT, rem = n % kScorePPT;
+  int pos0 = 0, pos1 = 0;
+  if (lane == 0) {
+    pos0 = full ? atomicAdd(&tile_count[0], full * g.nhb) : 0;
+    pos1 = rem ? atomicAdd(&tile_count[tile_bucket(rem)], g.nhb) : 0;
+  }
+  pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+  pos1 = __shfl_sync(0xffffffffu, pos1, 0);
+  const int64_t base32 = xy32_base(offsets, c);
+  for (int i = lane; i < full * g.nhb; i += 32) {
+    const int pb = i / g.nhb, hb = i - pb * g.nhb;
+    tiles[pos0 + i] = make_int4(c, static_cast<int>(base32 + pb * kScorePPT), kScorePPT, hb * g.TS);
+  }
+  if (rem) {
+    const int bk = tile_bucket(rem);
+    for (int hb = lane; hb < g.nhb; hb += 32)
+      tiles[bk * tile_cap + pos1 + hb] =
           make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
   }
 }
@@ -1604,10 +1931,12 @@ CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env
   const int64_t avg = n_clusters ? n_points / n_clusters : 0;
   int t = avg < 384 ? (select ? 64 : 128) : 256;
   t = env_int(env, t);
-  t = t <= 64 ? 64 : (t <= 128 ? 128 : 256);
-  return {t, t * 8};
+  t = t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : 256));
+  int cap = std::max(512, t * 8);
+  if (!select) cap = env_int("RVK_PREP_CAP", cap);
+  cap = std::min(2048, std::max(256, cap));
+  return {t, cap};
 }
-size_t prep_dyn_bytes(int cap) { return static_cast<size_t>(cap) * 16; }
 
 void launch_prep(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
   if (f.n_clusters == 0) return;
@@ -1654,9 +1983,33 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
     cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
   }
   const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
+  const int64_t avg = f.n_points / f.n_clusters;
+  if (!s.tc && env_int("RVK_PREP_WARP", avg < 384 ? 1 : 0) != 0) {
+    // warp per cluster up to kWarpCap points; the rest by persistent CTAs
+    cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 2, st);
+    prep_warp_kernel<<<(f.n_clusters + kPrepWarps - 1) / kPrepWarps, kPrepWarps * 32, 0, st>>>(
+        f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, s.big_list,
+        s.big_ctl);
+    count_launch();
+    static int big_grid = 0;
+    if (big_grid == 0) {
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      big_grid = 2 * sms;
+    }
+    prep_hyp_kernel<<<std::min<int64_t>(big_grid, f.n_clusters), 256, prep_dyn_bytes(2048), st>>>(
+        f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, 2048,
+        s.big_list, s.big_ctl);
+    count_launch();
+    return;
+  }
   prep_hyp_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, sh.cap);
+      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, sh.cap,
+      nullptr, nullptr);
   count_launch();
 }
 

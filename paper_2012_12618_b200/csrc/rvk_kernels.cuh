@@ -81,6 +81,8 @@ struct Scratch {
   float* hyp = nullptr;      // [C*Tg*32] per group of 8: A[8] B[8] C[8] K[8]
   int4* tiles = nullptr;     // [kTileBuckets * tile_cap] scoring tile descriptors
   int32_t* tile_count = nullptr;  // [kTileBuckets + 1] tiles per bucket + claim counter (zeroed per call)
+  int32_t* big_list = nullptr;    // [C] clusters too large for the warp-per-cluster prep
+  int32_t* big_ctl = nullptr;     // [2] big_list count + claim counter (zeroed per call)
   int64_t tile_cap = 0;
   // tensor-core scoring
   float* tc_hyp = nullptr;     // [C][tc_blocks(T)][kTcHypFloats]: K-major operand tile
