@@ -423,13 +423,17 @@ def main():
     clk = clk.summary()
     sm_max = clk.get("sm_max_mhz") or 1965
     nominal = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "score_kernel_traffic.json")
+    # DRAM traffic and FMA-pipe activity of the same kernel from the committed
+    # ncu --set full capture of this configuration (profiles/score_kernel_ncu.json)
+    traffic, ncu_info = None, None
+    tpath = os.path.join(ROOT, "profiles", "score_kernel_ncu.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("bytes_per_launch")
+            ncu_info = json.load(open(tpath)).get("config%d" % args.config)
+            if ncu_info:
+                traffic = ncu_info.get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
-            traffic = None
+            ncu_info = None
     total_ms = sum(stage_ms)
     roofline = {"bound": "fp32", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
@@ -440,6 +444,7 @@ def main():
                 "nominal_peak": nominal,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals_per_launch,
                 "avg_launch_ms": score_ms, "traffic": traffic,
+                "ncu": ncu_info,
                 "share_of_step": stage_ms[2] / total_ms if total_ms else None,
                 "stage_ms_per_step": {"prep_hyp_setup": stage_ms[0] / n_iso,
                                       "score": stage_ms[2] / n_iso,
@@ -515,10 +520,28 @@ def main():
         e2e_evals = stream_run(args.e2e_steps)
         e2e_t = time.perf_counter() - t0
         fs.close()
+        # PCIe roofline of the e2e path: pinned H2D copy bandwidth measured
+        # here on a buffer of one step's input size
+        hbuf = torch.empty(h2d // 4 + 1, dtype=torch.float32).pin_memory()
+        dbuf = torch.empty_like(hbuf, device=dev)
+        for _ in range(3):
+            dbuf.copy_(hbuf, non_blocking=True)
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(10):
+            dbuf.copy_(hbuf, non_blocking=True)
+        eb.record()
+        eb.synchronize()
+        h2d_peak = 10 * hbuf.numel() * 4 / (ea.elapsed_time(eb) / 1e3) / 1e9
+        h2d_ach = h2d / (e2e_t / args.e2e_steps) / 1e9
         e2e = {"value": e2e_evals / e2e_t * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3 / args.e2e_steps,
                "api": "FrameStream / rvk_stream_submit+wait (pinned host buffers, "
                       "depth %d: H2D of step k+1 overlaps the kernels of step k)" % depth,
+               "roofline": {"bound": "pcie_h2d", "achieved": h2d_ach, "peak": h2d_peak,
+                            "unit": "GB/s", "frac": h2d_ach / h2d_peak,
+                            "peak_source": "in-run pinned H2D copy of one step's input bytes"},
                "sync_call": {"value": sync_evals / sync_t * world,
                              "p50_step_latency_ms": statistics.median(lat),
                              "api": "rvk_ransac_estimate (one synchronous call per step)"},

@@ -2022,7 +2022,8 @@ int score_grid(int64_t max_units) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, 0);
-    grid = sms * std::max(per_sm, 1);
+    per_sm = std::max(1, std::min(per_sm, env_int("RVK_SCORE_CTAS", per_sm)));
+    grid = sms * per_sm;
   }
   const int64_t warps_per_cta = kScoreThreads / 32;
   return static_cast<int>(

@@ -1,6 +1,6 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, smoke, bench (both arms, several configs),
-# ncu launch list and one --set full capture of the pipeline kernels.
+# One gpurun call: GPU parity tests, smoke, bench (both arms, configs 2/3/4),
+# ncu launch list and --set full captures of the pipeline kernels.
 # Usage: bash tools/gpu_round.sh [tag]
 TAG=${1:-r1}
 O=gpurun_out/$TAG
@@ -17,8 +17,10 @@ done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
     --log-file $O/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline \
     --streams 1 --e2e-steps 2 > $O/ncu_launch_bench.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"score_kernel|prep_hyp_kernel|select_kernel" -s 6 -c 3 \
-    -o $O/prof_pipe python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
-    --streams 1 --e2e-steps 1 > $O/ncu_pipe.log 2>&1
+for c in 2 3 4; do
+  timeout 900 ncu --set full --clock-control none --import-source on \
+      -k regex:"score_kernel|prep_hyp|prep_warp|select_kernel" -s 6 -c 4 \
+      -o $O/prof_c$c python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline \
+      --streams 1 --e2e-steps 1 --resident-frames 16 > $O/ncu_c$c.log 2>&1
+done
 echo done > $O/DONE
