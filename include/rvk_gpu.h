@@ -20,6 +20,13 @@
  *   rvk_seed_pairs     <- rvk::draw_seed_pair  src/ransac.cpp:111-123
  *   rvk_cluster_thresholds <- normalize_cluster + mad_threshold
  *                         (src/ransac.cpp:69-94, ransac.hpp:53-84)
+ *   rvk_stream_*          the per-frame loop of run_estimate
+ *                         (tools/rvk_main.cpp:125-149), pipelined
+ *   rvk_dbscan         <- rvk::dbscan          src/clustering.cpp:24-114
+ *   rvk_extract_clusters <- rvk::extract_clusters src/clustering.cpp:116-155
+ *   rvk_estimate_frame    one frame of run_estimate: dbscan -> extract_clusters
+ *                         -> gather -> run_ransac -> estimate_all
+ *                         (tools/rvk_main.cpp:128-141), all on the device
  *
  * The C++ layer paper_2012_12618_b200/csrc/rvk_dropin.cpp re-exports the
  * reference's own C++ signatures on top of these, so unchanged callers link
@@ -185,6 +192,45 @@ int rvk_stream_submit(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
                       rvk_estimate* out, int64_t* ticket);
 int rvk_stream_wait(rvk_frame_stream* s, int64_t ticket);
 int rvk_stream_destroy(rvk_frame_stream* s);
+
+/* ---- Clustering: the stage upstream of the path (tools/rvk_main.cpp:128-129) ----
+ * Mirrors rvk::ClusteringParams (include/rvk/clustering.hpp:13-17). */
+typedef struct rvk_clustering_params {
+  double eps;        /* neighbourhood radius, > 0 (default 2.0) */
+  int32_t min_pts;   /* neighbours incl. the point itself for a core point, >= 1 (default 3) */
+  int32_t features;  /* RVK_FEATURES_XY (default) or RVK_FEATURES_XYZ */
+} rvk_clustering_params;
+#define RVK_FEATURES_XY 0
+#define RVK_FEATURES_XYZ 1
+
+/* rvk::dbscan (src/clustering.cpp:24-114) on the device, bit-exact: x, y
+ * (and z for XYZ; may be NULL for XY) of n points -> labels[n] (cluster ids
+ * 0..k-1 in order of each cluster's smallest core index, or -1 = noise). */
+int rvk_dbscan(int64_t n, const double* x, const double* y, const double* z,
+               const rvk_clustering_params* params, int32_t* labels);
+
+/* rvk::extract_clusters (src/clustering.cpp:116-155): labels[n] rewritten in
+ * place (small clusters -> -1, survivors compacted in order); outputs the
+ * clusters as CSR: *n_clusters = m, offsets[m + 1] (capacity n + 1),
+ * point_indices[n] (members of cluster c at offsets[c] .. offsets[c+1], in
+ * ascending point order; entries past offsets[m] are unspecified). */
+int rvk_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
+                         int32_t* n_clusters, int64_t* offsets, int32_t* point_indices);
+
+/* One frame of run_estimate's loop (tools/rvk_main.cpp:128-141), all on the
+ * device: dbscan -> extract_clusters -> gather_cluster_points -> run_ransac
+ * -> estimate_all. Point arrays are SoA (z may be NULL for XY). Outputs are
+ * caller-allocated for the worst case: labels[n], offsets[n + 1],
+ * point_indices[n], mask[n] (CSR-aligned with point_indices), and per cluster
+ * (capacity n / min_cluster_size + 1) inlier_count, winning_trial, out
+ * (cluster_id = the compact cluster id, frame_id = frame_id). Errors as the
+ * reference's calls in that order (dbscan, extract_clusters, run_ransac). */
+int rvk_estimate_frame(int64_t frame_id, int64_t n, const double* x, const double* y,
+                       const double* z, const double* doppler, const double* azimuth,
+                       const rvk_clustering_params* cparams, int32_t min_cluster_size,
+                       const rvk_ransac_params* rparams, int32_t* labels, int32_t* n_clusters,
+                       int64_t* offsets, int32_t* point_indices, int32_t* inlier_count,
+                       int32_t* winning_trial, uint8_t* mask, rvk_estimate* out);
 
 /* Stage timing for benchmarking/profiling. When enabled, CUDA events bracket
  * every pipeline stage launch on its stream (0 = prep, 1 = hypothesis

@@ -94,7 +94,40 @@ class _Lib:
             raise CheckerError(st, msg().decode())
 
 
-class Oracle(_Lib):
+class _Clustering:
+    """dbscan / extract_clusters (src/clustering.cpp:24-155) through a checker
+    library that exports <prefix>dbscan and <prefix>extract_clusters."""
+
+    def dbscan(self, x, y, z=None, eps=2.0, min_pts=3, features=0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        z = None if z is None else np.ascontiguousarray(z, dtype=np.float64)
+        labels = np.zeros(x.size, np.int32)
+        f = self._fn("dbscan")
+        f.argtypes = [C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                      C.POINTER(C.c_double), C.c_double, C.c_int32, C.c_int32,
+                      C.POINTER(C.c_int32)]
+        self._check(f(x.size, _p(x, C.c_double), _p(y, C.c_double), _p(z, C.c_double), eps,
+                      min_pts, features, _p(labels, C.c_int32)))
+        return labels
+
+    def extract_clusters(self, labels, min_cluster_size=3):
+        """-> (labels rewritten, offsets[m+1], point_indices[offsets[m]])."""
+        labels = np.array(labels, dtype=np.int32)
+        n = labels.size
+        offsets = np.zeros(n + 2, np.int64)
+        pi = np.zeros(max(n, 1), np.int32)
+        m = C.c_int32(0)
+        f = self._fn("extract_clusters")
+        f.argtypes = [C.c_int64, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
+                      C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        self._check(f(n, _p(labels, C.c_int32), min_cluster_size, C.byref(m),
+                      _p(offsets, C.c_int64), _p(pi, C.c_int32)))
+        off = offsets[:m.value + 1].copy()
+        return labels, off, pi[:int(off[-1])].copy()
+
+
+class Oracle(_Lib, _Clustering):
     """The C restatement (oracle/rvk_oracle.c)."""
 
     prefix = "rvk_or_"
@@ -199,7 +232,7 @@ class Oracle(_Lib):
         return RansacResult(cnt, tr, mask), out
 
 
-class Reference(_Lib):
+class Reference(_Lib, _Clustering):
     """The unmodified reference (oracle/_ref/librvk_ref.so, via oracle/ref_capi.cpp)."""
 
     prefix = "rvk_ref_"

@@ -17,6 +17,7 @@
 //   count_trial_inliers     src/ransac.cpp:69-127
 //   rvk::generate_frame     src/scene.cpp:105-189 (workload synthesis)
 #include <rvk/baseline.hpp>
+#include <rvk/clustering.hpp>
 #include <rvk/ransac.hpp>
 #include <rvk/rng.hpp>
 #include <rvk/scene.hpp>
@@ -294,6 +295,45 @@ int rvk_ref_generate_frame(uint64_t seed, int32_t n_objects, const double* objec
     if (outlier_flag)
       for (const auto& t : scene.truth)
         for (int idx : t.outlier_indices) outlier_flag[idx] = 1;
+  });
+}
+
+// rvk::dbscan (src/clustering.cpp:24-114) on SoA points; features 0 = XY, 1 = XYZ.
+int rvk_ref_dbscan(int64_t n, const double* x, const double* y, const double* z, double eps,
+                   int32_t min_pts, int32_t features, int32_t* labels) {
+  return guarded([&] {
+    rvk::Frame frame;
+    frame.points.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      frame.points[static_cast<std::size_t>(i)].x = x[i];
+      frame.points[static_cast<std::size_t>(i)].y = y[i];
+      frame.points[static_cast<std::size_t>(i)].z = z ? z[i] : 0.0;
+    }
+    rvk::ClusteringParams cp;
+    cp.eps = eps;
+    cp.min_pts = min_pts;
+    cp.features = features ? rvk::ClusterFeatures::XYZ : rvk::ClusterFeatures::XY;
+    rvk::dbscan(frame, cp);
+    for (int64_t i = 0; i < n; ++i) labels[i] = frame.labels[static_cast<std::size_t>(i)];
+  });
+}
+
+// rvk::extract_clusters (src/clustering.cpp:116-155): labels in/out, CSR out.
+int rvk_ref_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
+                             int32_t* n_clusters, int64_t* offsets, int32_t* point_indices) {
+  return guarded([&] {
+    rvk::Frame frame;
+    frame.points.resize(static_cast<std::size_t>(n));
+    frame.labels.assign(labels, labels + n);
+    const auto clusters = rvk::extract_clusters(frame, min_cluster_size);
+    *n_clusters = static_cast<int32_t>(clusters.size());
+    offsets[0] = 0;
+    int64_t k = 0;
+    for (std::size_t c = 0; c < clusters.size(); ++c) {
+      for (int idx : clusters[c].point_indices) point_indices[k++] = idx;
+      offsets[c + 1] = k;
+    }
+    for (int64_t i = 0; i < n; ++i) labels[i] = frame.labels[static_cast<std::size_t>(i)];
   });
 }
 

@@ -380,3 +380,117 @@ int rvk_or_ransac_estimate_range(int64_t frame_id, int32_t n_clusters, const int
   }
   return RVK_OK;
 }
+
+/* ---- DBSCAN + extract_clusters (src/clustering.cpp) ---------------------
+ * Restated from the reference, O(n^2) neighbour tests like it. Any
+ * breadth-first order visits the same component, so the queue-based
+ * labelling here equals the reference's (:62-89) exactly. */
+
+/* squared_distance, clustering.cpp:11-20 (compiled -ffp-contract=off) */
+static double sq_dist(const double* x, const double* y, const double* z, int features, int64_t a,
+                      int64_t b) {
+  const double dx = x[a] - x[b];
+  const double dy = y[a] - y[b];
+  double d2 = dx * dx + dy * dy;
+  if (features) {
+    const double dz = z[a] - z[b];
+    d2 += dz * dz;
+  }
+  return d2;
+}
+
+int rvk_or_dbscan(int64_t n, const double* x, const double* y, const double* z, double eps,
+                  int32_t min_pts, int32_t features, int32_t* labels) {
+  if (!(eps > 0.0)) { /* clustering.cpp:25-27 */
+    snprintf(g_err, sizeof g_err, "dbscan: eps must be positive");
+    return 1;
+  }
+  if (min_pts < 1) { /* :28-30 */
+    snprintf(g_err, sizeof g_err, "dbscan: min_pts must be at least 1");
+    return 1;
+  }
+  for (int64_t i = 0; i < n; ++i) labels[i] = -1;
+  if (n == 0) return 0;
+  const double eps2 = eps * eps; /* :37 */
+  /* |N_eps(p)| including p itself (:39-60) */
+  char* core = (char*)calloc((size_t)n, 1);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t cnt = 0;
+    for (int64_t j = 0; j < n; ++j) cnt += sq_dist(x, y, z, features, i, j) <= eps2;
+    core[i] = cnt >= min_pts;
+  }
+  /* core-core components, ids in order of the smallest core index (:62-89) */
+  int64_t* queue = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int32_t next_id = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!core[i] || labels[i] != -1) continue;
+    const int32_t id = next_id++;
+    int64_t head = 0, tail = 0;
+    labels[i] = id;
+    queue[tail++] = i;
+    while (head < tail) {
+      const int64_t p = queue[head++];
+      for (int64_t q = 0; q < n; ++q)
+        if (core[q] && labels[q] == -1 && sq_dist(x, y, z, features, p, q) <= eps2) {
+          labels[q] = id;
+          queue[tail++] = q;
+        }
+    }
+  }
+  /* border points: nearest core neighbour, ties to the lowest index (:91-113) */
+  for (int64_t i = 0; i < n; ++i) {
+    if (core[i]) continue;
+    int64_t best = -1;
+    double best_d2 = 0.0;
+    for (int64_t q = 0; q < n; ++q) {
+      if (q == i || !core[q]) continue;
+      const double d2 = sq_dist(x, y, z, features, i, q);
+      if (d2 > eps2) continue;
+      if (best == -1 || d2 < best_d2 || (d2 == best_d2 && q < best)) {
+        best = q;
+        best_d2 = d2;
+      }
+    }
+    if (best != -1) labels[i] = labels[best];
+  }
+  free(queue);
+  free(core);
+  return 0;
+}
+
+/* extract_clusters (src/clustering.cpp:116-155) */
+int rvk_or_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
+                            int32_t* n_clusters, int64_t* offsets, int32_t* point_indices) {
+  if (min_cluster_size < 1) {
+    snprintf(g_err, sizeof g_err, "extract_clusters: min_cluster_size must be at least 1");
+    return 1;
+  }
+  int32_t max_label = -1;
+  for (int64_t i = 0; i < n; ++i) max_label = labels[i] > max_label ? labels[i] : max_label;
+  const int64_t k = (int64_t)max_label + 1;
+  int64_t* size = (int64_t*)calloc((size_t)(k > 0 ? k : 1), sizeof(int64_t));
+  int32_t* remap = (int32_t*)malloc(sizeof(int32_t) * (size_t)(k > 0 ? k : 1));
+  for (int64_t i = 0; i < n; ++i)
+    if (labels[i] >= 0) ++size[labels[i]];
+  int32_t m = 0;
+  offsets[0] = 0;
+  for (int64_t l = 0; l < k; ++l) {
+    remap[l] = -1;
+    if (size[l] < min_cluster_size) continue;
+    remap[l] = m;
+    offsets[m + 1] = offsets[m] + size[l];
+    ++m;
+  }
+  int64_t* fill = (int64_t*)calloc((size_t)(m > 0 ? m : 1), sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) { /* members in ascending point order */
+    if (labels[i] < 0) continue;
+    const int32_t c = remap[labels[i]];
+    labels[i] = c;
+    if (c >= 0) point_indices[offsets[c] + fill[c]++] = (int32_t)i;
+  }
+  *n_clusters = m;
+  free(fill);
+  free(remap);
+  free(size);
+  return 0;
+}

@@ -70,6 +70,13 @@ int rvk_or_ransac_estimate_range(int64_t frame_id, int32_t n_clusters, const int
                                  int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
                                  rvk_estimate* out);
 
+/* DBSCAN + extract_clusters (src/clustering.cpp:24-155), O(n^2) like the
+ * reference; features 0 = XY, 1 = XYZ (z may be NULL for XY). */
+int rvk_or_dbscan(int64_t n, const double* x, const double* y, const double* z, double eps,
+                  int32_t min_pts, int32_t features, int32_t* labels);
+int rvk_or_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
+                            int32_t* n_clusters, int64_t* offsets, int32_t* point_indices);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,12 @@ class RansacParamsC(C.Structure):
                 ("threshold_scale", C.c_double), ("rng_seed", C.c_uint64)]
 
 
+class ClusteringParamsC(C.Structure):
+    """rvk_clustering_params (include/rvk_gpu.h)."""
+
+    _fields_ = [("eps", C.c_double), ("min_pts", C.c_int32), ("features", C.c_int32)]
+
+
 class EstimateC(C.Structure):
     """rvk_estimate (include/rvk_gpu.h)."""
 
@@ -69,6 +75,10 @@ GPU_SIGNATURES = {
     "rvk_stream_submit": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "rvk_stream_wait": (C.c_int, [_P, _I64]),
     "rvk_stream_destroy": (C.c_int, [_P]),
+    "rvk_dbscan": (C.c_int, [_I64, _P, _P, _P, _P, _P]),
+    "rvk_extract_clusters": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
+    "rvk_estimate_frame": (C.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P,
+                                     _P, _P, _P, _P]),
     "rvk_profile_enable": (None, [_I32]),
     "rvk_profile_read": (C.c_int, [_P, _P, _I32]),
 }

@@ -85,11 +85,32 @@ class RadarPoint:
 
 @dataclass
 class Frame:
-    """rvk::Frame (include/rvk/types.hpp:35-40), struct-of-arrays."""
+    """rvk::Frame (include/rvk/types.hpp:35-40), struct-of-arrays: the
+    RadarPoint fields x, y, z, doppler, azimuth as columns, plus labels
+    once clustering has run."""
 
     frame_id: int = 0
     azimuth: np.ndarray = field(default_factory=lambda: np.zeros(0))
     doppler: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    x: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    y: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    z: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    labels: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+
+
+@dataclass
+class ClusteringParams:
+    """rvk::ClusteringParams (include/rvk/clustering.hpp:13-17)."""
+
+    eps: float = 2.0
+    min_pts: int = 3
+    features: str = "xy"  # "xy" | "xyz" (rvk::ClusterFeatures)
+
+    def c(self) -> N.ClusteringParamsC:
+        if self.features not in ("xy", "xyz"):
+            raise ValueError("dbscan: unknown feature space")
+        return N.ClusteringParamsC(float(self.eps), int(self.min_pts),
+                                   1 if self.features == "xyz" else 0)
 
 
 @dataclass
@@ -386,3 +407,84 @@ def draw_seed_pair(seed: int, cluster_id: int, trial: int, n: int):
                            rng_cluster_index=np.array([cluster_id], np.int32))
     i, j = pairs[0, trial]
     return int(i), int(j)
+
+
+# ------------------------------------------------------------- clustering
+
+def _f64(a, n=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.size != n:
+        raise ValueError("point arrays must have the same length")
+    return a
+
+
+def dbscan_points(x, y, z=None, params: ClusteringParams = ClusteringParams()) -> np.ndarray:
+    """rvk_dbscan on SoA coordinates -> labels (int32, -1 = noise)."""
+    x = _f64(x)
+    y = _f64(y, x.size)
+    z = None if z is None else _f64(z, x.size)
+    labels = np.zeros(x.size, np.int32)
+    p = params.c()
+    _check(N.gpu().rvk_dbscan(x.size, N.ptr(x), N.ptr(y), N.ptr(z), C.addressof(p),
+                              N.ptr(labels)))
+    return labels
+
+
+def extract_clusters_labels(labels, min_cluster_size: int = 3):
+    """rvk_extract_clusters -> (labels rewritten, offsets[m+1], point_indices)."""
+    labels = np.array(labels, dtype=np.int32)
+    n = labels.size
+    offsets = np.zeros(n + 2, np.int64)
+    pi = np.zeros(max(n, 1), np.int32)
+    m = C.c_int32(0)
+    _check(N.gpu().rvk_extract_clusters(n, N.ptr(labels), int(min_cluster_size), C.byref(m),
+                                        N.ptr(offsets), N.ptr(pi)))
+    off = offsets[:m.value + 1].copy()
+    return labels, off, pi[:int(off[-1])].copy()
+
+
+def dbscan(frame: Frame, params: ClusteringParams = ClusteringParams()) -> None:
+    """rvk::dbscan (src/clustering.cpp:24-114): fills frame.labels."""
+    z = frame.z if params.features == "xyz" else None
+    frame.labels = dbscan_points(frame.x, frame.y, z, params)
+
+
+def extract_clusters(frame: Frame, min_cluster_size: int = 3):
+    """rvk::extract_clusters (src/clustering.cpp:116-155): rewrites
+    frame.labels and returns the surviving clusters (ascending members)."""
+    if len(frame.labels) != len(frame.x):
+        raise ValueError("extract_clusters: frame labels missing; run dbscan first")
+    labels, off, pi = extract_clusters_labels(frame.labels, min_cluster_size)
+    frame.labels = labels
+    return [Cluster(c, pi[off[c]:off[c + 1]].copy()) for c in range(off.size - 1)]
+
+
+def estimate_frame(frame: Frame, cparams: ClusteringParams = ClusteringParams(),
+                   rparams: RansacParams = RansacParams(), min_cluster_size: int = 3):
+    """One frame of run_estimate (tools/rvk_main.cpp:128-141) on the device:
+    dbscan -> extract_clusters -> gather -> run_ransac -> estimate_all.
+    Returns (labels, offsets, point_indices, RansacResult, estimates)."""
+    x = _f64(frame.x)
+    n = x.size
+    y, dop, az = _f64(frame.y, n), _f64(frame.doppler, n), _f64(frame.azimuth, n)
+    z = _f64(frame.z, n) if cparams.features == "xyz" else None
+    cap = n // max(1, int(min_cluster_size)) + 1
+    labels = np.zeros(n, np.int32)
+    offsets = np.zeros(n + 2, np.int64)
+    pi = np.zeros(max(n, 1), np.int32)
+    cnt = np.zeros(cap, np.int32)
+    tr = np.zeros(cap, np.int32)
+    mask = np.zeros(max(n, 1), np.uint8)
+    est = np.zeros(cap, N.ESTIMATE_DTYPE)
+    m = C.c_int32(0)
+    cp, rp = cparams.c(), rparams.c()
+    _check(N.gpu().rvk_estimate_frame(
+        int(frame.frame_id), n, N.ptr(x), N.ptr(y), N.ptr(z), N.ptr(dop), N.ptr(az),
+        C.addressof(cp), int(min_cluster_size), C.addressof(rp), N.ptr(labels), C.byref(m),
+        N.ptr(offsets), N.ptr(pi), N.ptr(cnt), N.ptr(tr), N.ptr(mask), N.ptr(est)))
+    k = m.value
+    off = offsets[:k + 1].copy()
+    P = int(off[-1])
+    frame.labels = labels
+    return (labels, off, pi[:P].copy(), RansacResult(cnt[:k].copy(), tr[:k].copy(),
+                                                     mask[:P].copy()), est[:k].copy())

@@ -42,7 +42,7 @@ def _run(cmd):
 
 
 def build_gpu(force=False):
-    srcs = [os.path.join(CSRC, f) for f in ("rvk_kernels.cu", "rvk_capi.cu")]
+    srcs = [os.path.join(CSRC, f) for f in ("rvk_kernels.cu", "rvk_dbscan.cu", "rvk_capi.cu")]
     deps = srcs + [os.path.join(CSRC, f) for f in ("rvk_device.cuh", "rvk_kernels.cuh")] + \
         [os.path.join(INCLUDE, "rvk_gpu.h")]
     out = os.path.join(LIB, "librvk_gpu.so")

@@ -100,6 +100,8 @@ struct Workspace {
 struct Context {
   int device = -1;
   cudaStream_t stream = nullptr;
+  DevBuf db, frame, labels;  // clustering scratch, frame points, labels
+  HostBuf stage_frame;
   DevBuf in;       // offsets | az | dop | ids | keys | order (one H2D)
   DevBuf out;      // count | trial | est | mask (one D2H)
   HostBuf stage_in, stage_out;
@@ -506,6 +508,43 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
                  us(t1, t2), us(t2, t3), us(t3, t4), us(t0, t4));
   }
   return RVK_OK;
+}
+
+// ---- clustering + the whole frame path ----
+int validate_clustering(const rvk_clustering_params* p) {
+  if (p == nullptr) return fail(RVK_EINVAL, "dbscan: params must not be null");
+  if (!(p->eps > 0.0)) return fail(RVK_EINVAL, "dbscan: eps must be positive");
+  if (p->min_pts < 1) return fail(RVK_EINVAL, "dbscan: min_pts must be at least 1");
+  if (p->features != RVK_FEATURES_XY && p->features != RVK_FEATURES_XYZ)
+    return fail(RVK_EINVAL, "dbscan: unknown feature space");
+  return RVK_OK;
+}
+
+// Frame points (x | y | [z] | [doppler | azimuth]) to the device, one H2D.
+struct FramePts {
+  double *x, *y, *z, *dop, *az;
+};
+FramePts upload_points(Context& ctx, int64_t n, const double* x, const double* y, const double* z,
+                       const double* dop, const double* az) {
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  const int cols = 2 + (z ? 1 : 0) + (dop ? 1 : 0) + (az ? 1 : 0);
+  char* h = static_cast<char*>(ctx.stage_frame.get(bytes * cols));
+  double* d = ctx.frame.get<double>(static_cast<size_t>(n) * cols);
+  FramePts f{};
+  int col = 0;
+  auto put = [&](const double* src, double** dst) {
+    if (src == nullptr) return;
+    std::memcpy(h + bytes * col, src, bytes);
+    *dst = d + static_cast<size_t>(n) * col;
+    ++col;
+  };
+  put(x, &f.x);
+  put(y, &f.y);
+  put(z, &f.z);
+  put(dop, &f.dop);
+  put(az, &f.az);
+  RVK_CUDA(cudaMemcpyAsync(d, h, bytes * cols, cudaMemcpyHostToDevice, ctx.stream));
+  return f;
 }
 
 // ---- pipelined frame stream (rvk_stream_*) ----
@@ -931,6 +970,160 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
       if (c) cudaStreamDestroy(c);
     delete s;
     return rc;
+  });
+}
+
+int rvk_dbscan(int64_t n, const double* x, const double* y, const double* z,
+               const rvk_clustering_params* params, int32_t* labels) {
+  return guarded([&]() -> int {
+    const int st = validate_clustering(params);
+    if (st != RVK_OK) return st;
+    if (n < 0) return fail(RVK_EINVAL, "dbscan: negative point count");
+    if (n == 0) return RVK_OK;
+    if (n >= (int64_t{1} << 31)) return fail(RVK_EINVAL, "dbscan: too many points");
+    const bool xyz = params->features == RVK_FEATURES_XYZ;
+    if (x == nullptr || y == nullptr || (xyz && z == nullptr) || labels == nullptr)
+      return fail(RVK_EINVAL, "dbscan: null point arrays");
+    Context& ctx = context();
+    const FramePts f = upload_points(ctx, n, x, y, xyz ? z : nullptr, nullptr, nullptr);
+    const DbscanLayout L = dbscan_layout(n, xyz);
+    char* ws = ctx.db.get<char>(L.total);
+    int32_t* d_labels = ctx.labels.get<int32_t>(static_cast<size_t>(n));
+    launch_dbscan(n, f.x, f.y, f.z, params->eps, params->min_pts, L, ws, d_labels, ctx.stream);
+    check_launch();
+    int32_t* h = static_cast<int32_t*>(ctx.stage_out.get(sizeof(int32_t) * n));
+    RVK_CUDA(cudaMemcpyAsync(h, d_labels, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(labels, h, sizeof(int32_t) * n);
+    return RVK_OK;
+  });
+}
+
+int rvk_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
+                         int32_t* n_clusters, int64_t* offsets, int32_t* point_indices) {
+  return guarded([&]() -> int {
+    if (min_cluster_size < 1)
+      return fail(RVK_EINVAL, "extract_clusters: min_cluster_size must be at least 1");
+    if (n < 0 || n >= (int64_t{1} << 31)) return fail(RVK_EINVAL, "extract_clusters: bad size");
+    if (n_clusters) *n_clusters = 0;
+    if (offsets) offsets[0] = 0;
+    if (n == 0) return RVK_OK;
+    if (labels == nullptr || n_clusters == nullptr || offsets == nullptr ||
+        point_indices == nullptr)
+      return fail(RVK_EINVAL, "extract_clusters: null arrays");
+    int32_t max_label = -1;
+    for (int64_t i = 0; i < n; ++i) max_label = std::max(max_label, labels[i]);
+    if (max_label < 0) return RVK_OK;
+    const int64_t k = static_cast<int64_t>(max_label) + 1;
+    Context& ctx = context();
+    const int64_t cap = std::max(n, k);
+    const DbscanLayout L = dbscan_layout(cap, false);
+    char* ws = ctx.db.get<char>(L.total);
+    // device block: labels[n] | offsets[k+1] | point_indices[n] | count
+    const size_t o_off = align_up(sizeof(int32_t) * n);
+    const size_t o_pi = align_up(o_off + sizeof(int64_t) * (k + 1));
+    const size_t o_m = align_up(o_pi + sizeof(int32_t) * n);
+    const size_t total = o_m + 256;
+    char* d = ctx.out.get<char>(total);
+    char* h = static_cast<char*>(ctx.stage_out.get(total));
+    std::memcpy(h, labels, sizeof(int32_t) * n);
+    RVK_CUDA(cudaMemcpyAsync(d, h, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx.stream));
+    launch_extract(n, reinterpret_cast<int32_t*>(d), static_cast<int32_t>(k), min_cluster_size, L,
+                   ws, reinterpret_cast<int64_t*>(d + o_off), reinterpret_cast<int32_t*>(d + o_pi),
+                   reinterpret_cast<int32_t*>(d + o_m), ctx.stream);
+    check_launch();
+    RVK_CUDA(cudaMemcpyAsync(h, d, total, cudaMemcpyDeviceToHost, ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    const int32_t m = *reinterpret_cast<int32_t*>(h + o_m);
+    *n_clusters = m;
+    std::memcpy(labels, h, sizeof(int32_t) * n);
+    std::memcpy(offsets, h + o_off, sizeof(int64_t) * (m + 1));
+    std::memcpy(point_indices, h + o_pi, sizeof(int32_t) * offsets[m]);
+    return RVK_OK;
+  });
+}
+
+int rvk_estimate_frame(int64_t frame_id, int64_t n, const double* x, const double* y,
+                       const double* z, const double* doppler, const double* azimuth,
+                       const rvk_clustering_params* cparams, int32_t min_cluster_size,
+                       const rvk_ransac_params* rparams, int32_t* labels, int32_t* n_clusters,
+                       int64_t* offsets, int32_t* point_indices, int32_t* inlier_count,
+                       int32_t* winning_trial, uint8_t* mask, rvk_estimate* out) {
+  return guarded([&]() -> int {
+    int st = validate_clustering(cparams);
+    if (st != RVK_OK) return st;
+    if (min_cluster_size < 1)
+      return fail(RVK_EINVAL, "extract_clusters: min_cluster_size must be at least 1");
+    st = validate_params(rparams, "run_ransac");
+    if (st != RVK_OK) return st;
+    if (n < 0 || n >= (int64_t{1} << 31)) return fail(RVK_EINVAL, "dbscan: bad point count");
+    if (n_clusters) *n_clusters = 0;
+    if (offsets) offsets[0] = 0;
+    if (n == 0) return RVK_OK;
+    const bool xyz = cparams->features == RVK_FEATURES_XYZ;
+    if (x == nullptr || y == nullptr || (xyz && z == nullptr) || doppler == nullptr ||
+        azimuth == nullptr || labels == nullptr || n_clusters == nullptr || offsets == nullptr ||
+        point_indices == nullptr)
+      return fail(RVK_EINVAL, "estimate_frame: null arrays");
+    Context& ctx = context();
+    const FramePts f = upload_points(ctx, n, x, y, xyz ? z : nullptr, doppler, azimuth);
+    const DbscanLayout L = dbscan_layout(n, xyz);
+    char* ws = ctx.db.get<char>(L.total);
+    // device: labels[n] | offsets[n+1] | point_indices[n] | m | gaz[n] | gdop[n]
+    const size_t o_off = align_up(sizeof(int32_t) * n);
+    const size_t o_pi = align_up(o_off + sizeof(int64_t) * (n + 1));
+    const size_t o_m = align_up(o_pi + sizeof(int32_t) * n);
+    const size_t o_gaz = align_up(o_m + 256);
+    const size_t o_gdop = align_up(o_gaz + sizeof(double) * n);
+    const size_t total = align_up(o_gdop + sizeof(double) * n);
+    char* d = ctx.labels.get<char>(total);
+    int32_t* d_labels = reinterpret_cast<int32_t*>(d);
+    int64_t* d_off = reinterpret_cast<int64_t*>(d + o_off);
+    int32_t* d_pi = reinterpret_cast<int32_t*>(d + o_pi);
+    launch_dbscan(n, f.x, f.y, f.z, cparams->eps, cparams->min_pts, L, ws, d_labels, ctx.stream);
+    launch_extract(n, d_labels, static_cast<int32_t>(n), min_cluster_size, L, ws, d_off, d_pi,
+                   reinterpret_cast<int32_t*>(d + o_m), ctx.stream);
+    check_launch();
+    // the cluster count and offsets decide the launch shapes: one sync
+    char* h = static_cast<char*>(ctx.stage_out.get(o_m + 256));
+    RVK_CUDA(cudaMemcpyAsync(h, d, o_m + 256, cudaMemcpyDeviceToHost, ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    const int32_t m = *reinterpret_cast<int32_t*>(h + o_m);
+    *n_clusters = m;
+    std::memcpy(labels, h, sizeof(int32_t) * n);
+    std::memcpy(offsets, h + o_off, sizeof(int64_t) * (m + 1));
+    const int64_t P = offsets[m];
+    std::memcpy(point_indices, h + o_pi, sizeof(int32_t) * P);
+    if (m == 0) return RVK_OK;
+    st = validate_offsets(m, offsets, kMinClusterSize, "run_ransac");  // ransac.cpp:147-156
+    if (st != RVK_OK) return st;
+    double* gaz = reinterpret_cast<double*>(d + o_gaz);
+    double* gdop = reinterpret_cast<double*>(d + o_gdop);
+    launch_gather(P, d_pi, f.az, f.dop, gaz, gdop, ctx.stream);
+    FrameDev fd;
+    fd.n_clusters = m;
+    fd.n_points = P;
+    fd.offsets = d_off;
+    fd.azimuth = gaz;
+    fd.doppler = gdop;
+    fd.frame_id = frame_id;  // keys / cluster ids: positional = the compact ids
+    Scratch scr = scratch(ctx.workspace(ctx.stream), m, P, rparams->max_trials);
+    const OutLayout OL(m, P);
+    char* dout = ctx.out.get<char>(OL.total);
+    Outputs o;
+    o.inlier_count = reinterpret_cast<int32_t*>(dout + OL.o_cnt);
+    o.winning_trial = reinterpret_cast<int32_t*>(dout + OL.o_tr);
+    o.est = reinterpret_cast<rvk_estimate*>(dout + OL.o_est);
+    o.mask = reinterpret_cast<uint8_t*>(dout + OL.o_mask);
+    run_pipeline(fd, *rparams, scr, o, ctx.stream);
+    char* hout = static_cast<char*>(ctx.stage_out.get(OL.total));
+    RVK_CUDA(cudaMemcpyAsync(hout, dout, OL.total, cudaMemcpyDeviceToHost, ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (inlier_count) std::memcpy(inlier_count, hout + OL.o_cnt, sizeof(int32_t) * m);
+    if (winning_trial) std::memcpy(winning_trial, hout + OL.o_tr, sizeof(int32_t) * m);
+    if (out) std::memcpy(out, hout + OL.o_est, sizeof(rvk_estimate) * m);
+    if (mask) std::memcpy(mask, hout + OL.o_mask, P);
+    return RVK_OK;
   });
 }
 

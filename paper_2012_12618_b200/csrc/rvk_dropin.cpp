@@ -7,6 +7,10 @@
 //                                                   const std::vector<Cluster>&,
 //                                                   const std::vector<InlierMask>&, int workers)
 //       -- include/rvk/velocity.hpp:123-125, replaces src/velocity.cpp:92-121
+//   void rvk::dbscan(Frame&, const ClusteringParams&)
+//       -- include/rvk/clustering.hpp:24, replaces src/clustering.cpp:24-114
+//   std::vector<Cluster> rvk::extract_clusters(Frame&, int)
+//       -- include/rvk/clustering.hpp:31, replaces src/clustering.cpp:116-155
 //
 // with the reference's exact signatures, compiled against the reference's
 // public headers (proj/include/rvk) and Eigen. Both marshal into the CSR
@@ -19,6 +23,7 @@
 // reference's ransac.o / velocity.o (objcopy --weaken-symbol) and link this
 // library; every other reference symbol (primitives, sequential baselines,
 // gather, combine_masks) stays the reference's own.
+#include <rvk/clustering.hpp>
 #include <rvk/ransac.hpp>
 #include <rvk/types.hpp>
 #include <rvk/velocity.hpp>
@@ -122,6 +127,46 @@ std::vector<VelocityEstimate> estimate_all(const Frame& frame, const std::vector
     v.heading = e.has_heading ? std::optional<double>(e.heading) : std::nullopt;
     v.inlier_count = e.inlier_count;
     v.condition_ok = e.condition_ok != 0;
+  }
+  return out;
+}
+
+void dbscan(Frame& frame, const ClusteringParams& params) {
+  const int64_t n = static_cast<int64_t>(frame.points.size());
+  std::vector<double> x(static_cast<std::size_t>(n)), y(x.size()), z(x.size());
+  for (std::size_t i = 0; i < x.size(); ++i) {
+    x[i] = frame.points[i].x;
+    y[i] = frame.points[i].y;
+    z[i] = frame.points[i].z;
+  }
+  const rvk_clustering_params p{params.eps, params.min_pts,
+                                params.features == ClusterFeatures::XYZ ? RVK_FEATURES_XYZ
+                                                                        : RVK_FEATURES_XY};
+  std::vector<int32_t> labels(x.size());
+  const int st = rvk_dbscan(n, x.data(), y.data(), z.data(), &p, labels.data());
+  if (st != RVK_OK) rethrow(st);  // clustering.cpp:25-30, before labels change
+  frame.labels.assign(labels.begin(), labels.end());
+}
+
+std::vector<Cluster> extract_clusters(Frame& frame, int min_cluster_size) {
+  if (min_cluster_size < 1)  // clustering.cpp:117-119
+    throw std::invalid_argument("extract_clusters: min_cluster_size must be at least 1");
+  if (frame.labels.size() != frame.points.size())  // :120-122
+    throw std::invalid_argument("extract_clusters: frame labels missing; run dbscan first");
+  const int64_t n = static_cast<int64_t>(frame.labels.size());
+  std::vector<int32_t> labels(frame.labels.begin(), frame.labels.end());
+  std::vector<int64_t> offsets(static_cast<std::size_t>(n) + 2, 0);
+  std::vector<int32_t> pi(static_cast<std::size_t>(n) + 1);
+  int32_t m = 0;
+  const int st = rvk_extract_clusters(n, labels.data(), min_cluster_size, &m, offsets.data(),
+                                      pi.data());
+  if (st != RVK_OK) rethrow(st);
+  frame.labels.assign(labels.begin(), labels.end());
+  std::vector<Cluster> out(static_cast<std::size_t>(m));
+  for (int32_t c = 0; c < m; ++c) {
+    out[static_cast<std::size_t>(c)].cluster_id = c;
+    out[static_cast<std::size_t>(c)].point_indices.assign(pi.begin() + offsets[c],
+                                                          pi.begin() + offsets[c + 1]);
   }
   return out;
 }

@@ -129,4 +129,25 @@ void launch_exact_counts(const FrameDev& f, const rvk_ransac_params& p, const Sc
 void launch_seed_pairs(const FrameDev& f, const rvk_ransac_params& p, int32_t* pairs,
                        cudaStream_t st);
 
+// ---- clustering (rvk_dbscan.cu): dbscan + extract_clusters
+struct DbscanLayout {
+  int table_bits = 0;
+  size_t o_keys = 0, o_idx = 0, o_skeys = 0, o_sidx = 0, o_sx = 0, o_sy = 0, o_sz = 0;
+  size_t o_cstart = 0, o_cend = 0, o_core = 0, o_parent = 0, o_root = 0, o_rep = 0, o_rank = 0;
+  size_t o_count = 0, o_keep = 0, o_kept = 0, o_start = 0, o_small = 0, o_cub = 0;
+  size_t cub_bytes = 0, total = 0;
+};
+DbscanLayout dbscan_layout(int64_t n, bool xyz);
+// rvk::dbscan on device arrays x, y (z or null for XY) -> labels[n].
+void launch_dbscan(int64_t n, const double* x, const double* y, const double* z, double eps,
+                   int min_pts, const DbscanLayout& L, char* ws, int32_t* labels, cudaStream_t st);
+// rvk::extract_clusters on device labels (rewritten in place); labels < n_labels_max.
+// offsets[m+1], point_indices[n] (kept members first, ascending per cluster), *d_n_clusters = m.
+void launch_extract(int64_t n, int32_t* labels, int32_t n_labels_max, int min_size,
+                    const DbscanLayout& L, char* ws, int64_t* offsets, int32_t* point_indices,
+                    int32_t* d_n_clusters, cudaStream_t st);
+// Gathers azimuth/doppler of the clusters' members (gather_cluster_points).
+void launch_gather(int64_t p, const int32_t* point_indices, const double* az, const double* dop,
+                   double* gaz, double* gdop, cudaStream_t st);
+
 }  // namespace rvk_gpu

@@ -37,6 +37,8 @@ class Workload:
     threshold_scale: float = 1.0
     rng_seed: int = 0
     meta: dict = field(default_factory=dict)
+    x: np.ndarray = field(default_factory=lambda: np.zeros(0))  # float64 [P], m (frame order)
+    y: np.ndarray = field(default_factory=lambda: np.zeros(0))
 
     @property
     def n_clusters(self) -> int:
@@ -74,12 +76,12 @@ def generate(seed: int, objects: np.ndarray, offset_range=(2.0, 5.0)):
 
 
 def _frame(name, seed, objects, max_trials, threshold_scale=1.0, rng_seed=0, **meta):
-    _, _, d, a, flag = generate(seed, objects)
+    x, y, d, a, flag = generate(seed, objects)
     sizes = objects[:, 6].astype(np.int64)
     offsets = np.zeros(sizes.size + 1, np.int64)
     np.cumsum(sizes, out=offsets[1:])
     return Workload(name, offsets, a, d, flag, objects[:, 4:6].copy(), max_trials,
-                    threshold_scale, rng_seed, dict(scene_seed=seed, **meta))
+                    threshold_scale, rng_seed, dict(scene_seed=seed, **meta), x, y)
 
 
 def _velocities(seed: int, k: int, lo=3.0, hi=18.0):

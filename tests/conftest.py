@@ -92,6 +92,20 @@ def golden_scene():
 
 
 @pytest.fixture(scope="session")
+def golden_dbscan():
+    d = np.load(os.path.join(GOLDEN, "dbscan.npz"))
+    out = []
+    for i, name in enumerate(d["names"]):
+        eps, mp, feat, mcs = d[f"{i}/params"]
+        out.append(dict(name=str(name), x=d[f"{i}/x"], y=d[f"{i}/y"],
+                        z=d[f"{i}/z"] if f"{i}/z" in d else None, eps=float(eps),
+                        min_pts=int(mp), features=int(feat), min_cluster_size=int(mcs),
+                        labels=d[f"{i}/labels"], extracted=d[f"{i}/extracted"],
+                        offsets=d[f"{i}/offsets"], point_indices=d[f"{i}/point_indices"]))
+    return out
+
+
+@pytest.fixture(scope="session")
 def gpu_lib():
     """The CUDA library on a real device (the GPU tests' entry point)."""
     _ensure_built()

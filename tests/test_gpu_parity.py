@@ -259,7 +259,8 @@ def _run_binary(name, extra=()):
 
 def test_reference_unit_suites_against_dropin(gpu_lib):
     """The reference's own gtest suites (test_ransac, test_baseline,
-    test_velocity, ...) linked against the GPU drop-in.
+    test_velocity, test_clustering, ...) linked against the GPU drop-in
+    (run_ransac, estimate_all, dbscan and extract_clusters on the device).
 
     Excluded: SequentialLsq.ExactlyMatchesParallelEstimates
     (test_baseline.cpp:84-110) asserts that the reference's two CPU LSQ
@@ -274,7 +275,8 @@ def test_reference_unit_suites_against_dropin(gpu_lib):
 
 def test_reference_acceptance_against_dropin(gpu_lib):
     """Acceptance C1, C2, C3 (1000 frames), C5-C7 of the reference against the
-    GPU drop-in. C4 (CPU thread-scaling trend) is about the CPU engine and is
+    GPU drop-in (C7: the reference's brute-force DBSCAN oracle vs rvk::dbscan,
+    now the device grid-hash DBSCAN). C4 (CPU thread-scaling trend) is about the CPU engine and is
     excluded."""
     code, log = _run_binary("rvk_dropin_acceptance", ["--gtest_filter=-C4ScalingTrend"])
     assert code == 0, log[-4000:]
