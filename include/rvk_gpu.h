@@ -24,6 +24,7 @@
  *                         (tools/rvk_main.cpp:125-149), pipelined
  *   rvk_dbscan         <- rvk::dbscan          src/clustering.cpp:24-114
  *   rvk_extract_clusters <- rvk::extract_clusters src/clustering.cpp:116-155
+ *   rvk_combine_masks  <- rvk::combine_masks  src/ransac.cpp:217-242
  *   rvk_estimate_frame    one frame of run_estimate: dbscan -> extract_clusters
  *                         -> gather -> run_ransac -> estimate_all
  *                         (tools/rvk_main.cpp:128-141), all on the device
@@ -231,6 +232,16 @@ int rvk_estimate_frame(int64_t frame_id, int64_t n, const double* x, const doubl
                        const rvk_ransac_params* rparams, int32_t* labels, int32_t* n_clusters,
                        int64_t* offsets, int32_t* point_indices, int32_t* inlier_count,
                        int32_t* winning_trial, uint8_t* mask, rvk_estimate* out);
+
+/* rvk::combine_masks (src/ransac.cpp:217-242): the frame-level union of the
+ * cluster masks. labels[n] = Frame::labels; masks are CSR: mask k has
+ * cluster_id mask_ids[k] and bytes masks[mask_offsets[k] .. mask_offsets[k+1]].
+ * result[n]: point i is set iff its label is >= 0, a mask with that
+ * cluster_id exists (the first such mask if ids repeat) and that mask is set
+ * at i's position among the points of its label in ascending frame order.
+ * n_masks == 0 gives all zeros. */
+int rvk_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks, const int32_t* mask_ids,
+                      const int64_t* mask_offsets, const uint8_t* masks, uint8_t* result);
 
 /* Stage timing for benchmarking/profiling. When enabled, CUDA events bracket
  * every pipeline stage launch on its stream (0 = prep, 1 = hypothesis

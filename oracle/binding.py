@@ -127,6 +127,23 @@ class _Clustering:
         return labels, off, pi[:int(off[-1])].copy()
 
 
+def _combine(self, labels, mask_ids, mask_offsets, masks):
+    labels = np.ascontiguousarray(labels, np.int32)
+    ids = np.ascontiguousarray(mask_ids, np.int32)
+    off = np.ascontiguousarray(mask_offsets, np.int64)
+    m = np.ascontiguousarray(masks, np.uint8)
+    out = np.zeros(labels.size, np.uint8)
+    f = self._fn("combine_masks")
+    f.argtypes = [C.c_int64, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
+                  C.POINTER(C.c_int64), C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)]
+    self._check(f(labels.size, _p(labels, C.c_int32), ids.size, _p(ids, C.c_int32),
+                  _p(off, C.c_int64), _p(m, C.c_uint8), _p(out, C.c_uint8)))
+    return out
+
+
+_Clustering.combine_masks = _combine
+
+
 class Oracle(_Lib, _Clustering):
     """The C restatement (oracle/rvk_oracle.c)."""
 

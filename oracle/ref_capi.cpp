@@ -337,4 +337,25 @@ int rvk_ref_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_siz
   });
 }
 
+// rvk::combine_masks (src/ransac.cpp:217-242): frame labels + CSR masks.
+int rvk_ref_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
+                          const int32_t* mask_ids, const int64_t* mask_offsets,
+                          const uint8_t* masks, uint8_t* result) {
+  return guarded([&] {
+    rvk::Frame frame;
+    frame.points.resize(static_cast<std::size_t>(n));
+    frame.labels.assign(labels, labels + n);
+    std::vector<rvk::InlierMask> ms(static_cast<std::size_t>(n_masks));
+    for (int32_t k = 0; k < n_masks; ++k) {
+      auto& m = ms[static_cast<std::size_t>(k)];
+      m.cluster_id = mask_ids[k];
+      const int64_t len = mask_offsets[k + 1] - mask_offsets[k];
+      m.mask = rvk::BoolArray::Constant(len, false);
+      for (int64_t q = 0; q < len; ++q) m.mask(q) = masks[mask_offsets[k] + q] != 0;
+    }
+    const rvk::BoolArray r = rvk::combine_masks(frame, ms);
+    for (int64_t i = 0; i < n; ++i) result[i] = r(i) ? 1 : 0;
+  });
+}
+
 }  // extern "C"

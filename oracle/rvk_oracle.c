@@ -494,3 +494,33 @@ int rvk_or_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size
   free(size);
   return 0;
 }
+
+/* combine_masks (src/ransac.cpp:217-242): a point's position within its
+ * label counts the earlier points of that label (:227-239); the first mask
+ * with a given cluster_id wins (unordered_map::emplace, :223-226). */
+int rvk_or_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
+                         const int32_t* mask_ids, const int64_t* mask_offsets,
+                         const uint8_t* masks, uint8_t* result) {
+  for (int64_t i = 0; i < n; ++i) result[i] = 0;
+  if (n_masks == 0) return 0;
+  int32_t max_label = -1;
+  for (int64_t i = 0; i < n; ++i) max_label = labels[i] > max_label ? labels[i] : max_label;
+  if (max_label < 0) return 0;
+  int64_t* seen = (int64_t*)calloc((size_t)max_label + 1, sizeof(int64_t));
+  int32_t* by_id = (int32_t*)malloc(sizeof(int32_t) * ((size_t)max_label + 1));
+  for (int32_t l = 0; l <= max_label; ++l) by_id[l] = -1;
+  for (int32_t k = 0; k < n_masks; ++k)
+    if (mask_ids[k] >= 0 && mask_ids[k] <= max_label && by_id[mask_ids[k]] < 0)
+      by_id[mask_ids[k]] = k;
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t l = labels[i];
+    if (l < 0) continue;
+    const int64_t pos = seen[l]++;
+    const int32_t k = by_id[l];
+    if (k >= 0 && pos < mask_offsets[k + 1] - mask_offsets[k])
+      result[i] = masks[mask_offsets[k] + pos] ? 1 : 0;
+  }
+  free(by_id);
+  free(seen);
+  return 0;
+}

@@ -77,6 +77,11 @@ int rvk_or_dbscan(int64_t n, const double* x, const double* y, const double* z, 
 int rvk_or_extract_clusters(int64_t n, int32_t* labels, int32_t min_cluster_size,
                             int32_t* n_clusters, int64_t* offsets, int32_t* point_indices);
 
+/* combine_masks (src/ransac.cpp:217-242): frame labels + CSR masks. */
+int rvk_or_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
+                         const int32_t* mask_ids, const int64_t* mask_offsets,
+                         const uint8_t* masks, uint8_t* result);
+
 #ifdef __cplusplus
 }
 #endif

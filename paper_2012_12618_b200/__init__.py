@@ -7,7 +7,8 @@ Kernels live in csrc/ and are reached through the C-ABI include/rvk_gpu.h;
 this package is the Python mirror of the reference API on top of it.
 """
 from .api import (ClusterTooSmall, Cluster, ClusteringParams, DeviceError, Frame,  # noqa: F401
-                  FrameStream, InlierMask, RansacParams, dbscan, dbscan_points, estimate_frame,
+                  FrameStream, InlierMask, RansacParams, combine_masks, combine_masks_labels,
+                  dbscan, dbscan_points, estimate_frame,
                   extract_clusters, extract_clusters_labels,
                   RansacResult, VelocityEstimate, clusters_to_csr, cluster_thresholds_csr,
                   draw_seed_pair, estimate_all, estimate_all_csr, gather_cluster_points,
@@ -16,7 +17,8 @@ from .api import (ClusterTooSmall, Cluster, ClusteringParams, DeviceError, Frame
 
 __all__ = [
     "ClusterTooSmall", "Cluster", "ClusteringParams", "DeviceError", "Frame", "FrameStream",
-    "InlierMask", "RansacParams", "dbscan", "dbscan_points", "estimate_frame", "extract_clusters",
+    "InlierMask", "RansacParams", "combine_masks", "combine_masks_labels", "dbscan",
+    "dbscan_points", "estimate_frame", "extract_clusters",
     "extract_clusters_labels",
     "RansacResult", "VelocityEstimate", "clusters_to_csr", "cluster_thresholds_csr",
     "draw_seed_pair", "estimate_all", "estimate_all_csr", "gather_cluster_points",

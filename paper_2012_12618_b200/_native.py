@@ -79,6 +79,7 @@ GPU_SIGNATURES = {
     "rvk_extract_clusters": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
     "rvk_estimate_frame": (C.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _P, _P,
                                      _P, _P, _P, _P]),
+    "rvk_combine_masks": (C.c_int, [_I64, _P, _I32, _P, _P, _P, _P]),
     "rvk_profile_enable": (None, [_I32]),
     "rvk_profile_read": (C.c_int, [_P, _P, _I32]),
 }

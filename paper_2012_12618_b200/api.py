@@ -488,3 +488,31 @@ def estimate_frame(frame: Frame, cparams: ClusteringParams = ClusteringParams(),
     frame.labels = labels
     return (labels, off, pi[:P].copy(), RansacResult(cnt[:k].copy(), tr[:k].copy(),
                                                      mask[:P].copy()), est[:k].copy())
+
+
+def combine_masks_labels(labels, mask_ids, mask_offsets, masks) -> np.ndarray:
+    """rvk_combine_masks: frame labels + CSR masks -> uint8 [n]."""
+    labels = np.ascontiguousarray(labels, np.int32)
+    ids = np.ascontiguousarray(mask_ids, np.int32)
+    off = np.ascontiguousarray(mask_offsets, np.int64)
+    m = np.ascontiguousarray(masks, np.uint8)
+    if off.size != ids.size + 1:
+        raise ValueError("combine_masks: mask_offsets must have n_masks + 1 entries")
+    out = np.zeros(labels.size, np.uint8)
+    _check(N.gpu().rvk_combine_masks(labels.size, N.ptr(labels), ids.size, N.ptr(ids),
+                                     N.ptr(off), N.ptr(m), N.ptr(out)))
+    return out
+
+
+def combine_masks(frame: Frame, masks: Sequence[InlierMask]) -> np.ndarray:
+    """rvk::combine_masks (src/ransac.cpp:217-242) -> bool [n points]."""
+    n = len(frame.x) if len(frame.x) else len(frame.azimuth)
+    if not masks or len(frame.labels) != n:
+        return np.zeros(n, bool)
+    ids = np.array([m.cluster_id for m in masks], np.int32)
+    sizes = np.array([len(m.mask) for m in masks], np.int64)
+    off = np.zeros(len(masks) + 1, np.int64)
+    np.cumsum(sizes, out=off[1:])
+    flat = np.concatenate([np.asarray(m.mask, np.uint8) for m in masks]) if off[-1] else \
+        np.zeros(0, np.uint8)
+    return combine_masks_labels(frame.labels, ids, off, flat).astype(bool)

@@ -1127,6 +1127,60 @@ int rvk_estimate_frame(int64_t frame_id, int64_t n, const double* x, const doubl
   });
 }
 
+int rvk_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks, const int32_t* mask_ids,
+                      const int64_t* mask_offsets, const uint8_t* masks, uint8_t* result) {
+  return guarded([&]() -> int {
+    if (n < 0 || n >= (int64_t{1} << 31) || n_masks < 0)
+      return fail(RVK_EINVAL, "combine_masks: bad sizes");
+    if (n == 0) return RVK_OK;
+    if (result == nullptr) return fail(RVK_EINVAL, "combine_masks: null result");
+    if (n_masks == 0 || labels == nullptr) {  // src/ransac.cpp:220-222
+      std::memset(result, 0, static_cast<size_t>(n));
+      return RVK_OK;
+    }
+    if (mask_ids == nullptr || mask_offsets == nullptr)
+      return fail(RVK_EINVAL, "combine_masks: null mask arrays");
+    const int64_t P = mask_offsets[n_masks];
+    // ids sorted ascending, the lowest mask index first among equal ids
+    std::vector<int32_t> order(static_cast<size_t>(n_masks));
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return mask_ids[a] < mask_ids[b]; });
+    Context& ctx = context();
+    const size_t o_ids = align_up(sizeof(int32_t) * n);
+    const size_t o_of = align_up(o_ids + sizeof(int32_t) * n_masks);
+    const size_t o_off = align_up(o_of + sizeof(int32_t) * n_masks);
+    const size_t o_m = align_up(o_off + sizeof(int64_t) * (n_masks + 1));
+    const size_t o_res = align_up(o_m + static_cast<size_t>(P));
+    const size_t total = align_up(o_res + static_cast<size_t>(n));
+    char* h = static_cast<char*>(ctx.stage_in.get(total));
+    char* d = ctx.in.get<char>(total);
+    std::memcpy(h, labels, sizeof(int32_t) * n);
+    int32_t* hid = reinterpret_cast<int32_t*>(h + o_ids);
+    int32_t* hof = reinterpret_cast<int32_t*>(h + o_of);
+    for (int32_t k = 0; k < n_masks; ++k) {
+      hid[k] = mask_ids[order[static_cast<size_t>(k)]];
+      hof[k] = order[static_cast<size_t>(k)];
+    }
+    std::memcpy(h + o_off, mask_offsets, sizeof(int64_t) * (n_masks + 1));
+    if (P > 0) std::memcpy(h + o_m, masks, static_cast<size_t>(P));
+    RVK_CUDA(cudaMemcpyAsync(d, h, o_res, cudaMemcpyHostToDevice, ctx.stream));
+    const DbscanLayout L = dbscan_layout(n, false);
+    char* ws = ctx.db.get<char>(L.total);
+    launch_combine_masks(n, reinterpret_cast<int32_t*>(d), n_masks,
+                         reinterpret_cast<int32_t*>(d + o_ids), reinterpret_cast<int32_t*>(d + o_of),
+                         reinterpret_cast<int64_t*>(d + o_off),
+                         reinterpret_cast<uint8_t*>(d + o_m), L, ws,
+                         reinterpret_cast<uint8_t*>(d + o_res), ctx.stream);
+    check_launch();
+    RVK_CUDA(cudaMemcpyAsync(h + o_res, d + o_res, static_cast<size_t>(n), cudaMemcpyDeviceToHost,
+                             ctx.stream));
+    RVK_CUDA(cudaStreamSynchronize(ctx.stream));
+    std::memcpy(result, h + o_res, static_cast<size_t>(n));
+    return RVK_OK;
+  });
+}
+
 void rvk_profile_enable(int32_t on) { g_prof.on = on != 0; }
 
 int rvk_profile_read(double* ms, int64_t* launches, int32_t n_stages) {

@@ -324,9 +324,80 @@ __global__ void gather_kernel(int64_t p, const int32_t* __restrict__ pi,
   gdop[k] = dop[i];
 }
 
+// ---- combine_masks (src/ransac.cpp:217-242)
+__global__ void cm_keys(int64_t n, const int32_t* __restrict__ labels, uint32_t* __restrict__ key,
+                        int32_t* __restrict__ idx) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t l = labels[i];
+  key[i] = l >= 0 ? static_cast<uint32_t>(l) : 0xFFFFFFFFu;
+  idx[i] = static_cast<int32_t>(i);
+}
+// run starts of the sorted labels: s where the label changes, else 0 (max-scanned)
+__global__ void cm_bounds(int64_t n, const uint32_t* __restrict__ skey, int32_t* __restrict__ b) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  b[s] = (s == 0 || skey[s - 1] != skey[s]) ? static_cast<int32_t>(s) : 0;
+}
+// Point sidx[s]: position within its label = s - run start; its mask = the
+// first mask whose cluster_id equals the label (ids sorted on the host with
+// the lowest mask index first, as unordered_map::emplace keeps the first).
+__global__ void cm_apply(int64_t n, const uint32_t* __restrict__ skey,
+                         const int32_t* __restrict__ sidx, const int32_t* __restrict__ run,
+                         int32_t n_masks, const int32_t* __restrict__ ids_sorted,
+                         const int32_t* __restrict__ mask_of, const int64_t* __restrict__ moff,
+                         const uint8_t* __restrict__ masks, uint8_t* __restrict__ result) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t k = skey[s];
+  uint8_t v = 0;
+  if (k != 0xFFFFFFFFu) {
+    const int32_t label = static_cast<int32_t>(k);
+    int lo = 0, hi = n_masks;  // first id >= label
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (ids_sorted[mid] < label) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n_masks && ids_sorted[lo] == label) {
+      const int32_t m = mask_of[lo];
+      const int64_t pos = s - run[s];
+      if (pos < moff[m + 1] - moff[m]) v = masks[moff[m] + pos];
+    }
+  }
+  result[sidx[s]] = v;
+}
+
 unsigned blocks(int64_t n) { return static_cast<unsigned>((n + kDbThreads - 1) / kDbThreads); }
 
 }  // namespace
+
+void launch_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
+                          const int32_t* ids_sorted, const int32_t* mask_of,
+                          const int64_t* moff, const uint8_t* masks, const DbscanLayout& L,
+                          char* ws, uint8_t* result, cudaStream_t st) {
+  if (n <= 0) return;
+  auto P = [&](size_t o) { return ws + o; };
+  uint32_t* key = reinterpret_cast<uint32_t*>(P(L.o_keys));
+  int32_t* idx = reinterpret_cast<int32_t*>(P(L.o_idx));
+  uint32_t* skey = reinterpret_cast<uint32_t*>(P(L.o_skeys));
+  int32_t* sidx = reinterpret_cast<int32_t*>(P(L.o_sidx));
+  int32_t* bnd = reinterpret_cast<int32_t*>(P(L.o_rep));
+  int32_t* run = reinterpret_cast<int32_t*>(P(L.o_rank));
+  void* cub_tmp = P(L.o_cub);
+  cm_keys<<<blocks(n), kDbThreads, 0, st>>>(n, labels, key, idx);
+  count_launch();
+  size_t cb = L.cub_bytes;
+  cub::DeviceRadixSort::SortPairs(cub_tmp, cb, key, skey, idx, sidx, static_cast<int>(n), 0, 32,
+                                  st);
+  cm_bounds<<<blocks(n), kDbThreads, 0, st>>>(n, skey, bnd);
+  count_launch();
+  cb = L.cub_bytes;
+  cub::DeviceScan::InclusiveScan(cub_tmp, cb, bnd, run, cub::Max(), static_cast<int>(n), st);
+  cm_apply<<<blocks(n), kDbThreads, 0, st>>>(n, skey, sidx, run, n_masks, ids_sorted, mask_of,
+                                             moff, masks, result);
+  count_launch();
+}
 
 void launch_gather(int64_t p, const int32_t* point_indices, const double* az, const double* dop,
                    double* gaz, double* gdop, cudaStream_t st) {
@@ -355,6 +426,10 @@ DbscanLayout dbscan_layout(int64_t n, bool xyz) {
   b = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const int32_t*>(nullptr),
                                 static_cast<int64_t*>(nullptr), static_cast<int>(n));
+  cub_bytes = b > cub_bytes ? b : cub_bytes;
+  b = 0;
+  cub::DeviceScan::InclusiveScan(nullptr, b, static_cast<const int32_t*>(nullptr),
+                                 static_cast<int32_t*>(nullptr), cub::Max(), static_cast<int>(n));
   cub_bytes = b > cub_bytes ? b : cub_bytes;
   auto take = [&](size_t bytes) {
     const size_t o = L.total;

@@ -7,6 +7,8 @@
 //                                                   const std::vector<Cluster>&,
 //                                                   const std::vector<InlierMask>&, int workers)
 //       -- include/rvk/velocity.hpp:123-125, replaces src/velocity.cpp:92-121
+//   BoolArray rvk::combine_masks(const Frame&, const std::vector<InlierMask>&)
+//       -- include/rvk/ransac.hpp:140, replaces src/ransac.cpp:217-242
 //   void rvk::dbscan(Frame&, const ClusteringParams&)
 //       -- include/rvk/clustering.hpp:24, replaces src/clustering.cpp:24-114
 //   std::vector<Cluster> rvk::extract_clusters(Frame&, int)
@@ -169,6 +171,29 @@ std::vector<Cluster> extract_clusters(Frame& frame, int min_cluster_size) {
                                                           pi.begin() + offsets[c + 1]);
   }
   return out;
+}
+
+BoolArray combine_masks(const Frame& frame, const std::vector<InlierMask>& masks) {
+  const int64_t n = static_cast<int64_t>(frame.points.size());
+  BoolArray result = BoolArray::Constant(n, false);
+  if (masks.empty() || frame.labels.size() != frame.points.size()) return result;  // :220-222
+  std::vector<int32_t> ids(masks.size());
+  std::vector<int64_t> off(masks.size() + 1, 0);
+  for (std::size_t k = 0; k < masks.size(); ++k) {
+    ids[k] = masks[k].cluster_id;
+    off[k + 1] = off[k] + masks[k].mask.size();
+  }
+  std::vector<uint8_t> flat(static_cast<std::size_t>(off.back()));
+  for (std::size_t k = 0; k < masks.size(); ++k)
+    for (Eigen::Index q = 0; q < masks[k].mask.size(); ++q)
+      flat[static_cast<std::size_t>(off[k] + q)] = masks[k].mask(q) ? 1 : 0;
+  std::vector<int32_t> labels(frame.labels.begin(), frame.labels.end());
+  std::vector<uint8_t> out(static_cast<std::size_t>(n));
+  const int st = rvk_combine_masks(n, labels.data(), static_cast<int32_t>(masks.size()),
+                                   ids.data(), off.data(), flat.data(), out.data());
+  if (st != RVK_OK) rethrow(st);
+  for (int64_t i = 0; i < n; ++i) result(i) = out[static_cast<std::size_t>(i)] != 0;
+  return result;
 }
 
 }  // namespace rvk

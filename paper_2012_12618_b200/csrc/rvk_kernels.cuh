@@ -146,6 +146,12 @@ void launch_dbscan(int64_t n, const double* x, const double* y, const double* z,
 void launch_extract(int64_t n, int32_t* labels, int32_t n_labels_max, int min_size,
                     const DbscanLayout& L, char* ws, int64_t* offsets, int32_t* point_indices,
                     int32_t* d_n_clusters, cudaStream_t st);
+// rvk::combine_masks: result[n] from frame labels and CSR masks (ids sorted
+// ascending with the first mask index per id in mask_of).
+void launch_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
+                          const int32_t* ids_sorted, const int32_t* mask_of,
+                          const int64_t* moff, const uint8_t* masks, const DbscanLayout& L,
+                          char* ws, uint8_t* result, cudaStream_t st);
 // Gathers azimuth/doppler of the clusters' members (gather_cluster_points).
 void launch_gather(int64_t p, const int32_t* point_indices, const double* az, const double* dop,
                    double* gaz, double* gdop, cudaStream_t st);

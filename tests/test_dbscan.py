@@ -153,3 +153,46 @@ def test_gpu_estimate_frame_matches_reference_pipeline(gpu_lib, reference):
         np.testing.assert_array_equal(res.winning_trial, r.winning_trial)
         np.testing.assert_array_equal(res.inlier_count, r.inlier_count)
         assert_estimates_close(est, e, label=f"frame {s}")
+
+
+# ------------------------------------------------------------ combine_masks
+
+def _random_masks(rng):
+    n = int(rng.integers(0, 300))
+    labels = rng.integers(-1, 8, n).astype(np.int32)
+    m = int(rng.integers(0, 10))
+    ids = rng.integers(-1, 9, m).astype(np.int32)  # duplicates and unknown ids too
+    sizes = rng.integers(0, 60, m)
+    off = np.zeros(m + 1, np.int64)
+    np.cumsum(sizes, out=off[1:])
+    masks = rng.integers(0, 2, int(off[-1])).astype(np.uint8)
+    return labels, ids, off, masks
+
+
+def test_oracle_combine_masks_live_against_reference(oracle, reference):
+    rng = np.random.default_rng(21)
+    for _ in range(200):
+        args = _random_masks(rng)
+        np.testing.assert_array_equal(oracle.combine_masks(*args), reference.combine_masks(*args))
+
+
+@pytest.mark.gpu
+def test_gpu_combine_masks_vs_oracle(gpu_lib, oracle):
+    import paper_2012_12618_b200 as rvk
+    rng = np.random.default_rng(22)
+    for k in range(200):
+        args = _random_masks(rng)
+        np.testing.assert_array_equal(rvk.combine_masks_labels(*args), oracle.combine_masks(*args),
+                                      err_msg=f"case {k}")
+    # frame-level: the masks of the device pipeline on a clustered frame
+    from paper_2012_12618_b200 import workloads as W
+    w = W.automotive(seed=5, n_clusters=30)
+    fr = rvk.Frame(frame_id=0, x=w.x, y=w.y, doppler=w.doppler, azimuth=w.azimuth)
+    labels, off, pi, res, _ = rvk.estimate_frame(fr, rvk.ClusteringParams(2.0, 3),
+                                                 rvk.RansacParams(256, 1.0, 1))
+    ids = np.arange(off.size - 1, dtype=np.int32)
+    got = rvk.combine_masks_labels(labels, ids, off, res.mask)
+    want = np.zeros(labels.size, np.uint8)
+    want[pi] = res.mask  # members in ascending order == the label ranks
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(got, oracle.combine_masks(labels, ids, off, res.mask))
