@@ -359,6 +359,29 @@ class Reference(_Lib, _Clustering):
             C.c_void_p(out.ctypes.data)))
         return RansacResult(cnt, tr, mask), out
 
+    def write_frames(self, path, frames):
+        """frames: list of (frame_id, x, y, z, doppler, azimuth) -> the reference's CSV."""
+        ids = np.array([f[0] for f in frames], np.int64)
+        sizes = [len(f[1]) for f in frames]
+        off = np.zeros(len(frames) + 1, np.int64)
+        np.cumsum(sizes, out=off[1:])
+        cols = [np.ascontiguousarray(np.concatenate([f[k] for f in frames]) if frames
+                                     else np.zeros(0), np.float64) for k in range(1, 6)]
+        f = self._fn("write_frames")
+        f.argtypes = [C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)] + \
+            [C.POINTER(C.c_double)] * 5 + [C.c_char_p]
+        self._check(f(len(frames), _p(ids, C.c_int64), _p(off, C.c_int64),
+                      *[_p(c, C.c_double) for c in cols], path.encode()))
+
+    def run_estimate_csv(self, frames_path, out_path, mode="parallel", eps=2.0, min_pts=3,
+                         max_trials=256, threshold_scale=1.0, seed=0):
+        f = self._fn("run_estimate_csv")
+        f.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                      C.c_double, C.c_uint64]
+        self._check(f(frames_path.encode(), out_path.encode(),
+                      0 if mode == "parallel" else 2, eps, min_pts, max_trials, threshold_scale,
+                      seed))
+
     def generate_frame(self, seed, objects, offset_range=(2.0, 5.0)):
         objects = np.ascontiguousarray(objects, np.float64).reshape(-1, 10)
         p = int(objects[:, 6].sum())

@@ -18,6 +18,7 @@
 //   rvk::generate_frame     src/scene.cpp:105-189 (workload synthesis)
 #include <rvk/baseline.hpp>
 #include <rvk/clustering.hpp>
+#include <rvk/frame_io.hpp>
 #include <rvk/ransac.hpp>
 #include <rvk/rng.hpp>
 #include <rvk/scene.hpp>
@@ -355,6 +356,66 @@ int rvk_ref_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks,
     }
     const rvk::BoolArray r = rvk::combine_masks(frame, ms);
     for (int64_t i = 0; i < n; ++i) result[i] = r(i) ? 1 : 0;
+  });
+}
+
+// The body of run_estimate (tools/rvk_main.cpp:104-158) without CLI11:
+// read_frames -> per frame dbscan, extract_clusters, gather, run_ransac +
+// estimate_all (mode 0 "parallel") or all_true_masks + estimate_all (mode 2
+// "lsq-only") -> write_estimates. Per-frame errors are skipped like the CLI.
+int rvk_ref_run_estimate_csv(const char* frames_path, const char* out_path, int32_t mode,
+                             double eps, int32_t min_pts, int32_t max_trials,
+                             double threshold_scale, uint64_t seed) {
+  return guarded([&] {
+    rvk::ClusteringParams cp;
+    cp.eps = eps;
+    cp.min_pts = min_pts;
+    rvk::RansacParams rp;
+    rp.max_trials = max_trials;
+    rp.threshold_scale = threshold_scale;
+    rp.rng_seed = seed;
+    std::vector<rvk::Frame> frames = rvk::read_frames(frames_path);
+    std::vector<rvk::VelocityEstimate> all;
+    for (rvk::Frame& frame : frames) {
+      try {
+        rvk::dbscan(frame, cp);
+        const auto clusters = rvk::extract_clusters(frame);
+        if (clusters.empty()) continue;
+        const auto pts = rvk::gather_cluster_points(frame, clusters);
+        std::vector<rvk::VelocityEstimate> est;
+        if (mode == 0) {
+          const auto masks = rvk::run_ransac(pts, rp, 0);
+          est = rvk::estimate_all(frame, clusters, masks, 0);
+        } else {
+          est = rvk::estimate_all(frame, clusters, rvk::all_true_masks(clusters), 0);
+        }
+        all.insert(all.end(), est.begin(), est.end());
+      } catch (const std::exception&) {
+      }
+    }
+    rvk::write_estimates(all, out_path);
+  });
+}
+
+// rvk::write_frames (src/frame_io.cpp:141-156) of one frame of SoA points.
+int rvk_ref_write_frames(int32_t n_frames, const int64_t* frame_ids, const int64_t* offsets,
+                         const double* x, const double* y, const double* z, const double* dop,
+                         const double* az, const char* path) {
+  return guarded([&] {
+    std::vector<rvk::Frame> frames(static_cast<std::size_t>(n_frames));
+    for (int32_t f = 0; f < n_frames; ++f) {
+      frames[static_cast<std::size_t>(f)].frame_id = frame_ids[f];
+      for (int64_t i = offsets[f]; i < offsets[f + 1]; ++i) {
+        rvk::RadarPoint p;
+        p.x = x[i];
+        p.y = y[i];
+        p.z = z[i];
+        p.doppler = dop[i];
+        p.azimuth = az[i];
+        frames[static_cast<std::size_t>(f)].points.push_back(p);
+      }
+    }
+    rvk::write_frames(frames, path);
   });
 }
 

@@ -5,6 +5,8 @@
 * lib/librvk_gpu.so   nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3
                       csrc/rvk_kernels.cu csrc/rvk_capi.cu      (C-ABI, include/rvk_gpu.h)
 * lib/librvk_scene.so gcc csrc/rvk_scene.c                      (host workload generator)
+* lib/rvk_gpu          g++ csrc/rvk_cli.cpp: the reference CLI's `estimate` command
+                      (frame CSV in, estimate CSV out) on the device path.
 * lib/librvk_dropin.so g++ csrc/rvk_dropin.cpp against the Eigen stand-in: the
                       reference's C++ API (rvk::run_ransac, rvk::estimate_all, ...)
                       re-exported over the C-ABI.
@@ -83,9 +85,20 @@ def build_dropin(force=False):
     return out
 
 
+def build_cli(force=False):
+    """lib/rvk_gpu: the reference CLI's `estimate` command on the device path."""
+    src = os.path.join(CSRC, "rvk_cli.cpp")
+    out = os.path.join(LIB, "rvk_gpu")
+    if force or _stale(out, [src, os.path.join(INCLUDE, "rvk_gpu.h")]):
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", INCLUDE, "-o", out, src,
+              "-L", LIB, "-lrvk_gpu", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build(force=False):
     os.makedirs(LIB, exist_ok=True)
-    return [build_gpu(force), build_probe(force), build_scene(force), build_dropin(force)]
+    return [build_gpu(force), build_probe(force), build_scene(force), build_dropin(force),
+            build_cli(force)]
 
 
 if __name__ == "__main__":
