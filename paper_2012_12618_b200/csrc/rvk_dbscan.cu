@@ -184,8 +184,43 @@ __global__ void db_parent_init(int64_t n, const int32_t* __restrict__ sidx,
   parent[i] = core[s] ? i : -1;
 }
 
+// Hooking: every core point points at its smallest core eps-neighbour (or
+// itself). Every pointer is a core-core edge and points to a smaller index,
+// so this is already a union-find forest of the graph; the union pass then
+// only has to merge the local trees.
+__global__ void db_hook(int64_t n, Pts p, double inv_cs, uint32_t mask, double eps2,
+                        const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
+                        const int32_t* __restrict__ sidx, const uint8_t* __restrict__ core,
+                        int32_t* __restrict__ parent) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n || !core[s]) return;
+  const int32_t i = sidx[s];
+  int32_t m = i;
+  Nbr nb;
+  neighbour_buckets(p, s, inv_cs, mask, nb);
+  for (int q = 0; q < nb.cnt; ++q) {
+    const int32_t e = cend[nb.key[q]];
+    for (int32_t t = cstart[nb.key[q]]; t < e; ++t) {
+      if (!core[t]) continue;
+      const int32_t j = sidx[t];
+      if (j < m && sq_dist(p, s, t) <= eps2) m = j;
+    }
+  }
+  parent[i] = m;
+}
+
+// Pointer jumping after hooking: every core point hangs directly under its
+// tree's root, so the union pass recognises same-tree edges with one load.
+__global__ void db_compress(int64_t n, int32_t* parent) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || parent[i] < 0) return;
+  parent[i] = uf_find(parent, static_cast<int32_t>(i));
+}
+
 // Core-core eps edges: each edge once (from the endpoint with the larger
-// sorted position), skipped when both ends already share a root.
+// sorted position). An edge whose far end already hangs directly under this
+// point's current root is skipped with one load; otherwise both roots are
+// found and linked.
 __global__ void db_union(int64_t n, Pts p, double inv_cs, uint32_t mask, double eps2,
                          const int32_t* __restrict__ cstart, const int32_t* __restrict__ cend,
                          const int32_t* __restrict__ sidx, const uint8_t* __restrict__ core,
@@ -193,15 +228,24 @@ __global__ void db_union(int64_t n, Pts p, double inv_cs, uint32_t mask, double 
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= n || !core[s]) return;
   const int32_t i = sidx[s];
+  int32_t r = uf_find(parent, i);
   Nbr nb;
   neighbour_buckets(p, s, inv_cs, mask, nb);
   for (int q = 0; q < nb.cnt; ++q) {
-    const int32_t e = cend[nb.key[q]];
-    for (int32_t t = cstart[nb.key[q]]; t < e; ++t) {
-      if (t >= s || !core[t]) continue;
-      if (sq_dist(p, s, t) > eps2) continue;
+    const int32_t b = cstart[nb.key[q]];
+    const int32_t e = min(cend[nb.key[q]], static_cast<int32_t>(s));  // edges to t < s
+    for (int32_t t = b; t < e; ++t) {
+      if (!core[t]) continue;
       const int32_t j = sidx[t];
-      if (uf_find(parent, i) != uf_find(parent, j)) uf_union(parent, i, j);
+      // a possibly stale (L1) read is enough to prove j is in i's tree:
+      // parents only ever move within a component
+      const int32_t pj = __ldca(parent + j);
+      if (pj == r || j == r) continue;
+      if (sq_dist(p, s, t) > eps2) continue;
+      const int32_t rj = uf_find(parent, j);
+      if (rj == r) continue;
+      uf_union(parent, r, rj);
+      r = uf_find(parent, i);
     }
   }
 }
@@ -501,6 +545,11 @@ void launch_dbscan(int64_t n, const double* x, const double* y, const double* z,
   db_core<<<blocks(n), kDbThreads, 0, st>>>(n, p, inv_cs, mask, eps2, min_pts, cstart, cend, core);
   count_launch();
   db_parent_init<<<blocks(n), kDbThreads, 0, st>>>(n, sidx, core, parent);
+  count_launch();
+  db_hook<<<blocks(n), kDbThreads, 0, st>>>(n, p, inv_cs, mask, eps2, cstart, cend, sidx, core,
+                                            parent);
+  count_launch();
+  db_compress<<<blocks(n), kDbThreads, 0, st>>>(n, parent);
   count_launch();
   db_union<<<blocks(n), kDbThreads, 0, st>>>(n, p, inv_cs, mask, eps2, cstart, cend, sidx, core,
                                              parent);
