@@ -283,8 +283,14 @@ def main():
     world, rank, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU (ranks beyond the device count share devices: only
+        # for functional runs of the multi-rank path on a smaller box)
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        backend = os.environ.get("RVK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -407,10 +413,11 @@ def main():
             frame_lat.append(a.elapsed_time(b_))
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        rdev = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([elapsed], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-        tot = torch.tensor([evals, clusters], device=dev, dtype=torch.float64)
+        tot = torch.tensor([evals, clusters], device=rdev, dtype=torch.float64)
         dist.all_reduce(tot)
         evals_all, clusters_all = float(tot[0]), float(tot[1])
     else:
@@ -454,99 +461,121 @@ def main():
                             "%d-stream timed region (overlapping other stages)" % (n_iso, S),
                 "live_avg_launch_ms": live_ms[2] / max(1, live_n[2])}
 
+    # ---- e2e through the public host API (pinned host buffers, H2D + D2H per
+    # step), on every rank at once
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def reduce_max_sum(t, n):
+        if world == 1:
+            return t, n
+        import torch.distributed as dist
+        rdev = dev if dist.get_backend() == "nccl" else "cpu"
+        v = torch.tensor([t], device=rdev, dtype=torch.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        c = torch.tensor([float(n)], device=rdev, dtype=torch.float64)
+        dist.all_reduce(c)
+        return float(v.item()), float(c.item())
+
+    hb = []
+    for j in range(min(n_batches, 8)):
+        fr = frames[j * B:(j + 1) * B]
+        off, az, dop, keys = batch(fr)
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        hb.append((pin(off), pin(az), pin(dop), pin(keys)))
+    C_ = hb[0][0].size - 1
+    P_ = int(hb[0][0][-1])
+    o_cnt = torch.zeros(Cmax, dtype=torch.int32).pin_memory().numpy()
+    o_tr = torch.zeros(Cmax, dtype=torch.int32).pin_memory().numpy()
+    o_mask = torch.zeros(Pmax, dtype=torch.uint8).pin_memory().numpy()
+    o_est = np.zeros(Cmax, _native.ESTIMATE_DTYPE)
+
+    def e2e_step(j):
+        off, az, dop, keys = hb[j % len(hb)]
+        st = lib.rvk_ransac_estimate(0, off.size - 1, off.ctypes.data, az.ctypes.data,
+                                     dop.ctypes.data, None, C.addressof(pc), keys.ctypes.data,
+                                     o_cnt.ctypes.data, o_tr.ctypes.data, o_mask.ctypes.data,
+                                     o_est.ctypes.data)
+        if st != 0:
+            raise RuntimeError(lib.rvk_last_error().decode())
+        return int(off[-1]) * p.max_trials
+
+    for j in range(3):
+        e2e_step(j)
+    lat = []
+    sync_evals = 0
+    barrier()
+    t0 = time.perf_counter()
+    for j in range(args.e2e_steps):
+        t1 = time.perf_counter()
+        sync_evals += e2e_step(j)
+        lat.append((time.perf_counter() - t1) * 1e3)
+    sync_t = time.perf_counter() - t0
+    h2d = (C_ + 1) * 8 + 2 * P_ * 8 + 2 * C_ * 4  # offsets, az, dop, keys, cluster ids
+    d2h = C_ * 4 * 2 + C_ * 48 + P_               # counts, trials, estimates, mask
+
+    # pipelined frame stream (rvk_stream_*): each step's H2D, kernels and
+    # D2H, up to `depth` steps in flight; pinned inputs and outputs
+    depth = 3
+    pin_np = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    outsets = [(pin_np(np.zeros(Cmax, np.int32)), pin_np(np.zeros(Cmax, np.int32)),
+                pin_np(np.zeros(Pmax, np.uint8)), np.zeros(Cmax, _native.ESTIMATE_DTYPE))
+               for _ in range(depth)]
+    fs = rvk.FrameStream(p, depth=depth)
+
+    def stream_run(n):
+        tickets, ev = [], 0
+        for j in range(n):
+            off, az, dop, keys = hb[j % len(hb)]
+            nc, npt = off.size - 1, int(off[-1])
+            o = outsets[j % depth]
+            tickets.append(fs.submit(off, az, dop, frame_id=j, rng_cluster_index=keys,
+                                     out=(o[0][:nc], o[1][:nc], o[2][:npt], o[3][:nc])))
+            ev += npt * p.max_trials
+        for t in tickets:
+            fs.wait(t)
+        return ev
+
+    stream_run(len(hb) + depth)  # every batch through every slot: buffers sized
+    barrier()  # all ranks stream concurrently; the job time is the slowest rank's
+    t0 = time.perf_counter()
+    e2e_evals = stream_run(args.e2e_steps)
+    e2e_t = time.perf_counter() - t0
+    fs.close()
+    e2e_t, e2e_evals = reduce_max_sum(e2e_t, e2e_evals)
+    sync_t, sync_evals = reduce_max_sum(sync_t, sync_evals)
+    # PCIe roofline of the e2e path: pinned H2D copy bandwidth measured
+    # here on a buffer of one step's input size
+    hbuf = torch.empty(h2d // 4 + 1, dtype=torch.float32).pin_memory()
+    dbuf = torch.empty_like(hbuf, device=dev)
+    for _ in range(3):
+        dbuf.copy_(hbuf, non_blocking=True)
+    torch.cuda.synchronize()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record()
+    for _ in range(10):
+        dbuf.copy_(hbuf, non_blocking=True)
+    eb.record()
+    eb.synchronize()
+    h2d_peak = 10 * hbuf.numel() * 4 / (ea.elapsed_time(eb) / 1e3) / 1e9
+    h2d_ach = h2d / (e2e_t / args.e2e_steps) / 1e9
+    e2e = {"value": e2e_evals / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3 / args.e2e_steps,
+           "api": "FrameStream / rvk_stream_submit+wait (pinned host buffers, "
+                  "depth %d: H2D of step k+1 overlaps the kernels of step k)" % depth,
+           "roofline": {"bound": "pcie_h2d", "achieved": h2d_ach, "peak": h2d_peak,
+                        "unit": "GB/s", "frac": h2d_ach / h2d_peak,
+                        "peak_source": "in-run pinned H2D copy of one step's input bytes"},
+           "sync_call": {"value": sync_evals / sync_t,
+                         "p50_step_latency_ms": statistics.median(lat),
+                         "api": "rvk_ransac_estimate (one synchronous call per step)"},
+           "note": "all %d ranks concurrently: evals summed over ranks / the slowest rank's "
+                   "wall time" % world}
+
     result = None
     if rank == 0:
-        # ---- e2e through the public host API (pinned host buffers, H2D + D2H per step)
-        hb = []
-        for j in range(min(n_batches, 8)):
-            fr = frames[j * B:(j + 1) * B]
-            off, az, dop, keys = batch(fr)
-            pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
-            hb.append((pin(off), pin(az), pin(dop), pin(keys)))
-        C_ = hb[0][0].size - 1
-        P_ = int(hb[0][0][-1])
-        o_cnt = torch.zeros(Cmax, dtype=torch.int32).pin_memory().numpy()
-        o_tr = torch.zeros(Cmax, dtype=torch.int32).pin_memory().numpy()
-        o_mask = torch.zeros(Pmax, dtype=torch.uint8).pin_memory().numpy()
-        o_est = np.zeros(Cmax, _native.ESTIMATE_DTYPE)
-
-        def e2e_step(j):
-            off, az, dop, keys = hb[j % len(hb)]
-            st = lib.rvk_ransac_estimate(0, off.size - 1, off.ctypes.data, az.ctypes.data,
-                                         dop.ctypes.data, None, C.addressof(pc), keys.ctypes.data,
-                                         o_cnt.ctypes.data, o_tr.ctypes.data, o_mask.ctypes.data,
-                                         o_est.ctypes.data)
-            if st != 0:
-                raise RuntimeError(lib.rvk_last_error().decode())
-            return int(off[-1]) * p.max_trials
-
-        for j in range(3):
-            e2e_step(j)
-        lat = []
-        sync_evals = 0
-        t0 = time.perf_counter()
-        for j in range(args.e2e_steps):
-            t1 = time.perf_counter()
-            sync_evals += e2e_step(j)
-            lat.append((time.perf_counter() - t1) * 1e3)
-        sync_t = time.perf_counter() - t0
-        h2d = (C_ + 1) * 8 + 2 * P_ * 8 + 2 * C_ * 4  # offsets, az, dop, keys, cluster ids
-        d2h = C_ * 4 * 2 + C_ * 48 + P_               # counts, trials, estimates, mask
-
-        # pipelined frame stream (rvk_stream_*): each step's H2D, kernels and
-        # D2H, up to `depth` steps in flight; pinned inputs and outputs
-        depth = 3
-        pin_np = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
-        outsets = [(pin_np(np.zeros(Cmax, np.int32)), pin_np(np.zeros(Cmax, np.int32)),
-                    pin_np(np.zeros(Pmax, np.uint8)), np.zeros(Cmax, _native.ESTIMATE_DTYPE))
-                   for _ in range(depth)]
-        fs = rvk.FrameStream(p, depth=depth)
-
-        def stream_run(n):
-            tickets, ev = [], 0
-            for j in range(n):
-                off, az, dop, keys = hb[j % len(hb)]
-                nc, npt = off.size - 1, int(off[-1])
-                o = outsets[j % depth]
-                tickets.append(fs.submit(off, az, dop, frame_id=j, rng_cluster_index=keys,
-                                         out=(o[0][:nc], o[1][:nc], o[2][:npt], o[3][:nc])))
-                ev += npt * p.max_trials
-            for t in tickets:
-                fs.wait(t)
-            return ev
-
-        stream_run(len(hb) + depth)  # every batch through every slot: buffers sized
-        t0 = time.perf_counter()
-        e2e_evals = stream_run(args.e2e_steps)
-        e2e_t = time.perf_counter() - t0
-        fs.close()
-        # PCIe roofline of the e2e path: pinned H2D copy bandwidth measured
-        # here on a buffer of one step's input size
-        hbuf = torch.empty(h2d // 4 + 1, dtype=torch.float32).pin_memory()
-        dbuf = torch.empty_like(hbuf, device=dev)
-        for _ in range(3):
-            dbuf.copy_(hbuf, non_blocking=True)
-        torch.cuda.synchronize()
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record()
-        for _ in range(10):
-            dbuf.copy_(hbuf, non_blocking=True)
-        eb.record()
-        eb.synchronize()
-        h2d_peak = 10 * hbuf.numel() * 4 / (ea.elapsed_time(eb) / 1e3) / 1e9
-        h2d_ach = h2d / (e2e_t / args.e2e_steps) / 1e9
-        e2e = {"value": e2e_evals / e2e_t * world, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3 / args.e2e_steps,
-               "api": "FrameStream / rvk_stream_submit+wait (pinned host buffers, "
-                      "depth %d: H2D of step k+1 overlaps the kernels of step k)" % depth,
-               "roofline": {"bound": "pcie_h2d", "achieved": h2d_ach, "peak": h2d_peak,
-                            "unit": "GB/s", "frac": h2d_ach / h2d_peak,
-                            "peak_source": "in-run pinned H2D copy of one step's input bytes"},
-               "sync_call": {"value": sync_evals / sync_t * world,
-                             "p50_step_latency_ms": statistics.median(lat),
-                             "api": "rvk_ransac_estimate (one synchronous call per step)"},
-               "note": "rank-0 e2e rate x n_gpus" if world > 1 else "single rank"}
-
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             checker, kind, workers = cpu_checker(os.cpu_count() or 1)

@@ -101,6 +101,22 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
           }
         }
         ++i;
+      } else if (V == 5) {
+        // diagonal pairing, no broadcast operand: v = (x1, x2, y1, y2);
+        // FFMA2 lanes = (hyp 2k, point 1) + (hyp 2k+1, point 2), then swapped
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+        const float2 Xs = make_float2(v.y, v.x), Ys = make_float2(v.w, v.z);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 ea = __ffma2_rn(h.A[q], X, __ffma2_rn(h.B[q], Y, h.C[q]));
+          float2 eb = __ffma2_rn(h.A[q], Xs, __ffma2_rn(h.B[q], Ys, h.C[q]));
+          ea = __ffma2_rn(ea, ea, h.T[q]);
+          eb = __ffma2_rn(eb, eb, h.T[q]);
+          cnt[2 * q] += __float_as_uint(ea.x) >> 31;
+          cnt[2 * q + 1] += __float_as_uint(ea.y) >> 31;
+          cnt[2 * q] += __float_as_uint(eb.x) >> 31;
+          cnt[2 * q + 1] += __float_as_uint(eb.y) >> 31;
+        }
       } else {
         // v = (x1, x2, y1, y2)
         const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
@@ -176,9 +192,9 @@ int main() {
     for (size_t i = 0; i < h.size(); ++i) h[i] = make_float4(0.1f * (i % 7), 0.2f, 0.3f * (i % 3), 0.4f);
     CK(cudaMemcpyToSymbol(g_pts, h.data(), h.size() * sizeof(float4)));
   }
-  run<4, 256, 2, 2>(sms, peak, du);
-  run<4, 256, 3, 2>(sms, peak, du);
-  run<4, 128, 6, 2>(sms, peak, du);
+  run<5, 256, 2, 2>(sms, peak, du);
+  run<5, 256, 3, 2>(sms, peak, du);
+  run<5, 256, 2, 4>(sms, peak, du);
   run<0, 256, 2, 2>(sms, peak, du);
   run<3, 256, 3, 1>(sms, peak, du);
   run<3, 256, 2, 1>(sms, peak, du);
