@@ -1925,11 +1925,12 @@ int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
 }
-// Measured on B200 (profiles/r1d_summary.md): prep wants 128 threads for
-// clusters of ~200 points and 256 above ~400; select wants 64 for ~200 points.
+// Measured on B200 (profiles/r1d_summary.md, r1e): prep wants 128 threads for
+// clusters of ~200 points and 256 above ~400; select 64 for ~200 points, 128
+// for ~600.
 CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env, bool select) {
   const int64_t avg = n_clusters ? n_points / n_clusters : 0;
-  int t = avg < 384 ? (select ? 64 : 128) : 256;
+  int t = select ? (avg < 384 ? 64 : (avg < 1024 ? 128 : 256)) : (avg < 384 ? 128 : 256);
   t = env_int(env, t);
   t = t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : 256));
   int cap = std::max(512, t * 8);
