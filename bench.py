@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--frames-per-step", type=int, default=8)
+    ap.add_argument("--frames-per-step", type=int, default=16)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--resident-frames", type=int, default=96)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
