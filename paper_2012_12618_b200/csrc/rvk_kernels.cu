@@ -374,6 +374,19 @@ __device__ __forceinline__ int64_t xy32_base(const int64_t* offsets, int c) {
   return ((offsets[c] + 1) & ~int64_t{1}) + 2 * static_cast<int64_t>(c);
 }
 
+// xy32 holds each cluster's points two at a time as (x_2q, x_2q+1, y_2q,
+// y_2q+1): one float4 = two points with x and y already paired for the
+// scoring loop's FFMA2 (two points x one hypothesis per instruction).
+__device__ __forceinline__ void xy32_put(float2* base, int k, float x, float y) {
+  float* f = reinterpret_cast<float*>(base) + (k >> 1) * 4 + (k & 1);
+  f[0] = x;
+  f[2] = y;
+}
+__device__ __forceinline__ float2 xy32_get(const float2* base, int k) {
+  const float* f = reinterpret_cast<const float*>(base) + (k >> 1) * 4 + (k & 1);
+  return make_float2(f[0], f[2]);
+}
+
 // Per cluster (one CTA): normalize_cluster (src/ransac.cpp:69-87), the median
 // of the normalized dopplers (ransac.hpp:53-70, exact selection), and the MAD
 // corridor as a guaranteed interval. Leaves stat in sm.stat for the caller.
@@ -443,13 +456,13 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
-    p32[k] = make_float2(__double2float_rn(x), __double2float_rn(y));
+    xy32_put(p32, k, __double2float_rn(x), __double2float_rn(y));
     // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
     // std::sort's operator< treats them; every other value is >= +0)
     if (in_smem)
       sm.keys[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
   }
-  if (threadIdx.x == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);  // pad to even
+  if (threadIdx.x == 0 && (n & 1)) xy32_put(p32, n, 0.f, kPadY);  // pad to even
   if (threadIdx.x == 0 && norm != nullptr) {
     norm[4 * c + 0] = lo0;
     norm[4 * c + 1] = lo1;
@@ -922,15 +935,15 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const double x1 = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(a1, lo0), s0);
     const double y1 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d1, lo1), s1);
     xy64[b + k0] = make_double2(x0, y0);
-    p32[k0] = make_float2(__double2float_rn(x0), __double2float_rn(y0));
+    xy32_put(p32, k0, __double2float_rn(x0), __double2float_rn(y0));
     w.keys[k0] = static_cast<unsigned long long>(__double_as_longlong(y0)) & ~(1ull << 63);
     if (k1 < n) {
       xy64[b + k1] = make_double2(x1, y1);
-      p32[k1] = make_float2(__double2float_rn(x1), __double2float_rn(y1));
+      xy32_put(p32, k1, __double2float_rn(x1), __double2float_rn(y1));
       w.keys[k1] = static_cast<unsigned long long>(__double_as_longlong(y1)) & ~(1ull << 63);
     }
   }
-  if (lane == 0 && (n & 1)) p32[n] = make_float2(0.f, kPadY);
+  if (lane == 0 && (n & 1)) xy32_put(p32, n, 0.f, kPadY);
   __syncwarp();
   // median (ransac.hpp:53-70) and the MAD interval (see prep_cluster)
   const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
@@ -1146,7 +1159,8 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     // 1. this unit's hypotheses: lane j holds group d.w + j (A, B, C, K x 8)
     const int gi = d.w + lane;
     const bool active = gi < g.Tg;
-    float2 A[kNH / 2], B[kNH / 2], Cc[kNH / 2], T2[kNH / 2];
+    float A[kNH], B[kNH];
+    float2 Cc[kNH], T2[kNH];
     {
       const float4* hp = reinterpret_cast<const float4*>(
           hyp + (static_cast<int64_t>(d.x) * g.Tg + (active ? gi : d.w)) * 32);
@@ -1154,14 +1168,16 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
       for (int h = 0; h < 2; ++h) {
         const float4 a = __ldg(hp + h), bb = __ldg(hp + 2 + h), cc = __ldg(hp + 4 + h),
                      kk = __ldg(hp + 6 + h);
-        A[2 * h] = make_float2(a.x, a.y);
-        A[2 * h + 1] = make_float2(a.z, a.w);
-        B[2 * h] = make_float2(bb.x, bb.y);
-        B[2 * h + 1] = make_float2(bb.z, bb.w);
-        Cc[2 * h] = make_float2(cc.x, cc.y);
-        Cc[2 * h + 1] = make_float2(cc.z, cc.w);
-        T2[2 * h] = make_float2(kk.x, kk.y);
-        T2[2 * h + 1] = make_float2(kk.z, kk.w);
+        A[4 * h] = a.x, A[4 * h + 1] = a.y, A[4 * h + 2] = a.z, A[4 * h + 3] = a.w;
+        B[4 * h] = bb.x, B[4 * h + 1] = bb.y, B[4 * h + 2] = bb.z, B[4 * h + 3] = bb.w;
+        Cc[4 * h] = make_float2(cc.x, cc.x);
+        Cc[4 * h + 1] = make_float2(cc.y, cc.y);
+        Cc[4 * h + 2] = make_float2(cc.z, cc.z);
+        Cc[4 * h + 3] = make_float2(cc.w, cc.w);
+        T2[4 * h] = make_float2(kk.x, kk.x);
+        T2[4 * h + 1] = make_float2(kk.y, kk.y);
+        T2[4 * h + 2] = make_float2(kk.z, kk.z);
+        T2[4 * h + 3] = make_float2(kk.w, kk.w);
       }
     }
     // 2. the next unit (claimed one unit ago): descriptor + point prefetch,
@@ -1182,19 +1198,16 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     uint32_t cnt[kNH];
 #pragma unroll
     for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+    // v = (x_2q, x_2q+1, y_2q, y_2q+1): per hypothesis 3 FFMA2 over the two
+    // points (e = A x + (B y + C); g = e^2 - t2hi) and two sign bits
     auto score_pair = [&](const float4& v) {
+      const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
 #pragma unroll
-      for (int pr = 0; pr < kNH / 2; ++pr) {
-        float2 e0 = __ffma2_rn(A[pr], make_float2(v.x, v.x),
-                               __ffma2_rn(B[pr], make_float2(v.y, v.y), Cc[pr]));
-        float2 e1 = __ffma2_rn(A[pr], make_float2(v.z, v.z),
-                               __ffma2_rn(B[pr], make_float2(v.w, v.w), Cc[pr]));
-        e0 = __ffma2_rn(e0, e0, T2[pr]);
-        e1 = __ffma2_rn(e1, e1, T2[pr]);
-        cnt[2 * pr] += __float_as_uint(e0.x) >> 31;
-        cnt[2 * pr + 1] += __float_as_uint(e0.y) >> 31;
-        cnt[2 * pr] += __float_as_uint(e1.x) >> 31;
-        cnt[2 * pr + 1] += __float_as_uint(e1.y) >> 31;
+      for (int h = 0; h < kNH; ++h) {
+        float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
+                              __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
+        e = __ffma2_rn(e, e, T2[h]);
+        cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
       }
     };
     // 4. broadcast LDS.128 (two points), two float4 per iteration, one ahead
@@ -1522,7 +1535,7 @@ __device__ int warp_exact_count(const ExactHyp& H, int n, const float2* __restri
   int cnt = 0;
   bool und = false;
   for (int k = threadIdx.x & 31; k < n; k += 32) {
-    const int d = classify(H, k, p32[k], p64, thr_lo, thr_hi);
+    const int d = classify(H, k, xy32_get(p32, k), p64, thr_lo, thr_hi);
     cnt += d == kIn;
     und |= d == kUndecided;
   }
@@ -1754,7 +1767,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
       for (int u = 0; u < 4; ++u) {
         const int k = k0 + u * nt;
         if (k < n) {
-          pp[u] = p32[k];
+          pp[u] = xy32_get(p32, k);
           if (refit) {
             pa[u] = caz[k];
             pd[u] = cdop[k];
