@@ -1089,6 +1089,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // hypothesis loads) is covered by the other warps of the SM sub-partition.
 // Counts are upper bounds (guard band, see make_fast) and accumulate over
 // units with integer atomics (order-free, deterministic).
+// per warp two slots of (kScorePPT / 2 + 2) float4
+constexpr size_t kScoreSmemBytes =
+    static_cast<size_t>(kScoreThreads / 32) * 2 * (kScorePPT / 2 + 2) * sizeof(float4);
+
 // Unit index (LPT order) -> descriptor: binary search of the bucket starts.
 __device__ __forceinline__ int4 unit_desc(const int* bstart, const int4* __restrict__ tiles,
                                           int64_t tile_cap, int u) {
@@ -1122,7 +1126,8 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
   constexpr int kSlot = kScorePPT / 2 + 2;  // float4 per slot (+2: read-ahead slack)
   __shared__ int bstart[kTileBuckets + 1];
   // two point slots per warp: the current unit's and the next unit's (prefetch)
-  __shared__ __align__(16) float4 pts_s[kScoreThreads / 32][2][kSlot];
+  extern __shared__ __align__(16) float4 pts_dyn[];
+  auto pts_s = reinterpret_cast<float4(*)[2][kSlot]>(pts_dyn);
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 32) {  // exclusive prefix of the bucket sizes
     int carry = 0;
@@ -2035,7 +2040,10 @@ int score_grid(int64_t max_units) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads, 0);
+    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kScoreSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads,
+                                                  kScoreSmemBytes);
     per_sm = std::max(1, std::min(per_sm, env_int("RVK_SCORE_CTAS", per_sm)));
     grid = sms * per_sm;
   }
@@ -2070,7 +2078,8 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   }
   const ScoreGeom g = score_geom(p.max_trials);
   const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
-  score_kernel<<<score_grid(max_units), kScoreThreads, 0, st>>>(s.tile_count, s.tiles, s.tile_cap,
+  score_kernel<<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
+      s.tile_count, s.tiles, s.tile_cap,
                                                                 s.xy32, s.hyp, g, s.upper);
   count_launch();
 }

@@ -29,8 +29,8 @@ struct FrameDev {
 // against up to kScorePPT of its points.
 constexpr int kScoreThreads = 256;
 constexpr int kUnitGroups = 32;                   // groups of 8 hypotheses per unit (one per lane)
-constexpr int kScorePPT = 256;                    // points per scoring unit (max)
-constexpr int kTileBuckets = kScorePPT / 4 + 1;   // 0: full units; 1..64: by size, descending
+constexpr int kScorePPT = 512;                    // points per scoring unit (max)
+constexpr int kTileBuckets = kScorePPT / 4 + 1;   // 0: full units; 1..128: by size, descending
 
 struct ScoreGeom {
   int T = 0;    // max_trials
