@@ -64,8 +64,17 @@ __device__ __forceinline__ T block_reduce(T v, Op op, T* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   T r = red[0];
-  for (int w = 1; w < nw; ++w) r = op(r, red[w]);
-  return r;
+  if (nw <= 4) {  // few partials: every thread combines them (no extra barrier)
+    for (int w = 1; w < nw; ++w) r = op(r, red[w]);
+    return r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // one thread combines the warp partials, same order
+    for (int w = 1; w < nw; ++w) r = op(r, red[w]);
+    red[0] = r;
+  }
+  __syncthreads();
+  return red[0];
 }
 
 struct SumI {
@@ -218,14 +227,22 @@ __device__ __forceinline__ int med_bin(unsigned long long key, int nb) {
 }
 
 // Dynamic shared memory of the prep kernels, sized per launch from the
-// sort capacity (prep_smem_layout): [keys: cap][cand: candcap][hist: histcap].
-struct PrepShared;
-__device__ void prep_smem_setup(PrepShared& sm, unsigned char* dyn, int cap);
+// sort capacity (prep_dyn_bytes): [keys: cap][cand: candcap][hist: histcap].
+// Addressed from the extern symbol (not through stored pointers) so every
+// access compiles to LDS/STS rather than generic loads.
+extern __shared__ __align__(16) unsigned char prep_dyn[];
 
 struct PrepShared {
-  unsigned long long* keys;  // [cap] normalized dopplers (bit patterns, sign cleared)
-  unsigned long long* cand;  // [candcap] candidates of the median bucket
-  unsigned int* hist;        // [histcap] bucket / radix counters (>= 256)
+  // [cap] normalized dopplers (bit patterns, sign cleared)
+  __device__ unsigned long long* keys() const {
+    return reinterpret_cast<unsigned long long*>(prep_dyn);
+  }
+  // [candcap] candidates of the median bucket
+  __device__ unsigned long long* cand() const { return keys() + cap; }
+  // [histcap] bucket / radix counters (>= 256)
+  __device__ unsigned int* hist() const {
+    return reinterpret_cast<unsigned int*>(keys() + cap + candcap);
+  }
   int cap;                   // clusters up to this size are kept in shared memory
   int candcap;
   int histcap;               // 2048: 11-bit radix digits, else 8-bit
@@ -248,34 +265,43 @@ __host__ __device__ inline size_t prep_dyn_bytes(int cap) {
   return static_cast<size_t>(cap) * 8 + static_cast<size_t>(prep_candcap(cap)) * 8 +
          static_cast<size_t>(prep_histcap(cap)) * 4;
 }
-__device__ void prep_smem_setup(PrepShared& sm, unsigned char* dyn, int cap) {
-  sm.cap = cap;
-  sm.candcap = prep_candcap(cap);
-  sm.histcap = prep_histcap(cap);
-  sm.keys = reinterpret_cast<unsigned long long*>(dyn);
-  sm.cand = sm.keys + cap;
-  sm.hist = reinterpret_cast<unsigned int*>(sm.cand + sm.candcap);
+__device__ void prep_smem_setup(PrepShared& sm, int cap) {
+  if (threadIdx.x == 0) {
+    sm.cap = cap;
+    sm.candcap = prep_candcap(cap);
+    sm.histcap = prep_histcap(cap);
+  }
+  __syncthreads();
+}
+
+// Median buckets of a cluster of n points: about one per point (small
+// clusters scan few empty buckets), at least one per thread; a power of two.
+__device__ __forceinline__ int med_buckets(int n, int histcap) {
+  int nb = blockDim.x;
+  while (nb < n && nb < histcap) nb <<= 1;
+  return nb;
 }
 
 // The k-th and (k+1)-th smallest keys (k+1 only if `pair`), exact. Keys are
 // bucketed by value (a monotone map), the bucket holding rank k is collected
 // and ranked directly; a crowded bucket falls back to the radix select.
-__device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
+// On entry sm.hist()[0, nb) holds the bucket histogram of the n keys
+// (built by prep_cluster's normalize pass) and sm.sh[2] == 0.
+__device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair, int nb,
                                   unsigned long long& v0, unsigned long long& v1) {
   const int nt = blockDim.x, tid = threadIdx.x;
-  // about one bucket per point (small clusters scan few empty buckets), at
-  // least one per thread
-  int nb = nt;
-  while (nb < n && nb < sm.histcap) nb <<= 1;
-  for (int i = tid; i < nb; i += nt) sm.hist[i] = 0;
-  if (tid == 0) sm.sh[2] = 0;
-  __syncthreads();
-  for (int i = tid; i < n; i += nt) atomicAdd(&sm.hist[med_bin(sm.keys[i], nb)], 1u);
-  __syncthreads();
   // bin holding rank k: thread j owns bins [j*per, (j+1)*per)
-  const int per = nb / nt;  // both powers of two, nb >= nt
+  const int per = nb >> (31 - __clz(nt));  // both powers of two, nb >= nt
   unsigned int local = 0;
-  for (int q = 0; q < per; ++q) local += sm.hist[tid * per + q];
+  if (per >= 4) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(sm.hist() + tid * per);
+    for (int q = 0; q < (per >> 2); ++q) {
+      const uint4 u = h4[q];
+      local += u.x + u.y + u.z + u.w;
+    }
+  } else {
+    for (int q = 0; q < per; ++q) local += sm.hist()[tid * per + q];
+  }
   const int lane = tid & 31, warp = tid >> 5;
   unsigned int incl = local;
 #pragma unroll
@@ -292,7 +318,7 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
   if (kk >= excl && kk < excl + local) {
     unsigned int cum = excl;
     for (int q = 0; q < per; ++q) {
-      const unsigned int h = sm.hist[tid * per + q];
+      const unsigned int h = sm.hist()[tid * per + q];
       if (kk < cum + h) {
         sm.sh[0] = tid * per + q;          // bin
         sm.sh[1] = static_cast<int>(cum);  // keys below the bin
@@ -304,25 +330,25 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
   __syncthreads();
   const int bin = sm.sh[0];
   const int below = sm.sh[1];
-  const int in_bin = static_cast<int>(sm.hist[bin]);
+  const int in_bin = static_cast<int>(sm.hist()[bin]);
   if (in_bin > sm.candcap) {  // crowded bucket: exact radix select
     const int bits = sm.histcap >= 2048 ? 11 : 8;
-    v0 = block_radix_select(sm.keys, n, k, sm.hist, sm.sh, bits);
-    if (pair) v1 = block_radix_select(sm.keys, n, k + 1, sm.hist, sm.sh, bits);
+    v0 = block_radix_select(sm.keys(), n, k, sm.hist(), sm.sh, bits);
+    if (pair) v1 = block_radix_select(sm.keys(), n, k + 1, sm.hist(), sm.sh, bits);
     return;
   }
   for (int i = tid; i < n; i += nt) {
-    const unsigned long long key = sm.keys[i];
-    if (med_bin(key, nb) == bin) sm.cand[atomicAdd(reinterpret_cast<unsigned int*>(&sm.sh[2]), 1u)] = key;
+    const unsigned long long key = sm.keys()[i];
+    if (med_bin(key, nb) == bin) sm.cand()[atomicAdd(reinterpret_cast<unsigned int*>(&sm.sh[2]), 1u)] = key;
   }
   const bool second_in_bin = pair && k + 1 < below + in_bin;
   __syncthreads();
   const int r0 = k - below;
   for (int i = tid; i < in_bin; i += nt) {
-    const unsigned long long ci = sm.cand[i];
+    const unsigned long long ci = sm.cand()[i];
     int less = 0, eq = 0;
     for (int j = 0; j < in_bin; ++j) {
-      const unsigned long long cj = sm.cand[j];
+      const unsigned long long cj = sm.cand()[j];
       less += cj < ci;
       eq += cj == ci;
     }
@@ -333,7 +359,7 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
     // the (k+1)-th is the smallest key above the bin
     unsigned long long m = ~0ull;
     for (int i = tid; i < n; i += nt) {
-      const unsigned long long key = sm.keys[i];
+      const unsigned long long key = sm.keys()[i];
       if (med_bin(key, nb) > bin && key < m) m = key;
     }
 #pragma unroll
@@ -342,11 +368,11 @@ __device__ void block_select_pair(PrepShared& sm, int n, int k, bool pair,
       m = u < m ? u : m;
     }
     __syncthreads();
-    if (lane == 0) sm.cand[warp] = m;  // cand[] reads are done
+    if (lane == 0) sm.cand()[warp] = m;  // cand[] reads are done
     __syncthreads();
     if (tid == 0) {
-      unsigned long long r = sm.cand[0];
-      for (int w = 1; w < (nt >> 5); ++w) r = sm.cand[w] < r ? sm.cand[w] : r;
+      unsigned long long r = sm.cand()[0];
+      for (int w = 1; w < (nt >> 5); ++w) r = sm.cand()[w] < r ? sm.cand()[w] : r;
       sm.sel[1] = r;
     }
   }
@@ -409,6 +435,8 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
 
+  const bool in_smem = n <= sm.cap;
+  const int nb = med_buckets(n, sm.histcap);
   double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double a = az[b + k], d = dop[b + k];
@@ -417,29 +445,46 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
     lo1 = d < lo1 ? d : lo1;
     hi1 = d > hi1 ? d : hi1;
   }
-  {  // one fused block reduction of (min az, -max az, min dop, -max dop)
-    double4 v = make_double4(lo0, -hi0, lo1, -hi1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      v.x = fmin(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
-      v.y = fmin(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
-      v.z = fmin(v.z, __shfl_xor_sync(0xffffffffu, v.z, o));
-      v.w = fmin(v.w, __shfl_xor_sync(0xffffffffu, v.w, o));
+  {  // (min az, max az, min dop, max dop): per-thread partials go to the
+     // keys area (free until the normalize pass below; cap >= 512 keeps it
+     // >= 32 B per thread), warp 0 combines them. No partial is NaN (the
+     // loop above never takes one), so plain compares are exact.
+    double4* part = reinterpret_cast<double4*>(prep_dyn);
+    part[threadIdx.x] = make_double4(lo0, hi0, lo1, hi1);
+    if (in_smem) {  // median buckets, filled by the normalize pass
+      uint4* h4 = reinterpret_cast<uint4*>(sm.hist());
+      for (int i = threadIdx.x; i < (nb >> 2); i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+      if (threadIdx.x == 0) sm.sh[2] = 0;
     }
-    if ((threadIdx.x & 31) == 0) sm.red4[threadIdx.x >> 5] = v;
     __syncthreads();
-    v = sm.red4[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      const double4 u = sm.red4[w];
-      v.x = fmin(v.x, u.x);
-      v.y = fmin(v.y, u.y);
-      v.z = fmin(v.z, u.z);
-      v.w = fmin(v.w, u.w);
+    if (threadIdx.x < 32) {
+      double4 v = part[threadIdx.x];
+      for (int i = threadIdx.x + 32; i < (int)blockDim.x; i += 32) {
+        const double4 u = part[i];
+        v.x = u.x < v.x ? u.x : v.x;
+        v.y = u.y > v.y ? u.y : v.y;
+        v.z = u.z < v.z ? u.z : v.z;
+        v.w = u.w > v.w ? u.w : v.w;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ux = __shfl_xor_sync(0xffffffffu, v.x, o);
+        const double uy = __shfl_xor_sync(0xffffffffu, v.y, o);
+        const double uz = __shfl_xor_sync(0xffffffffu, v.z, o);
+        const double uw = __shfl_xor_sync(0xffffffffu, v.w, o);
+        v.x = ux < v.x ? ux : v.x;
+        v.y = uy > v.y ? uy : v.y;
+        v.z = uz < v.z ? uz : v.z;
+        v.w = uw > v.w ? uw : v.w;
+      }
+      if (threadIdx.x == 0) sm.red4[0] = v;
     }
+    __syncthreads();
+    const double4 v = sm.red4[0];
     lo0 = v.x;
-    hi0 = -v.y;
+    hi0 = v.y;
     lo1 = v.z;
-    hi1 = -v.w;
+    hi1 = v.w;
   }
   // Eigen's minCoeff/maxCoeff keep the FIRST extreme in index order; values
   // that compare equal differ in bits only for +-0, so an extreme equal to
@@ -450,17 +495,21 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
   hi1 = first_zero(hi1, dop + b, n, sm.red);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
-  const bool in_smem = n <= sm.cap;
   float2* p32 = xy32 + xy32_base(offsets, c);
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
     xy64[b + k] = make_double2(x, y);
     xy32_put(p32, k, __double2float_rn(x), __double2float_rn(y));
-    // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
-    // std::sort's operator< treats them; every other value is >= +0)
-    if (in_smem)
-      sm.keys[k] = static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
+    if (in_smem) {
+      // key: bit pattern with the sign cleared (-0.0 sorts with +0.0, as
+      // std::sort's operator< treats them; every other value is >= +0),
+      // counted into its median bucket right away
+      const unsigned long long key =
+          static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
+      sm.keys()[k] = key;
+      atomicAdd(&sm.hist()[med_bin(key, nb)], 1u);
+    }
   }
   if (threadIdx.x == 0 && (n & 1)) xy32_put(p32, n, 0.f, kPadY);  // pad to even
   if (threadIdx.x == 0 && norm != nullptr) {
@@ -476,24 +525,24 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
     // k-th order statistics (median of the sorted copy, ransac.hpp:60-69).
     const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
     unsigned long long v0 = 0, v1 = 0;
-    block_select_pair(sm, n, k0, (n & 1) == 0, v0, v1);
+    block_select_pair(sm, n, k0, (n & 1) == 0, nb, v0, v1);
     const double d0 = __longlong_as_double(static_cast<long long>(v0));
     med = (n & 1) ? d0
                   : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))), 2.0);
   } else {
     const double2* cxy = xy64 + b;
     if (n & 1) {
-      med = block_select_y(cxy, n, n / 2, sm.hist, &sm.sel[0], &sm.sh[0]);
+      med = block_select_y(cxy, n, n / 2, sm.hist(), &sm.sel[0], &sm.sh[0]);
     } else {
-      const double lo = block_select_y(cxy, n, n / 2 - 1, sm.hist, &sm.sel[0], &sm.sh[0]);
-      const double hi = block_select_y(cxy, n, n / 2, sm.hist, &sm.sel[0], &sm.sh[0]);
+      const double lo = block_select_y(cxy, n, n / 2 - 1, sm.hist(), &sm.sel[0], &sm.sh[0]);
+      const double hi = block_select_y(cxy, n, n / 2, sm.hist(), &sm.sel[0], &sm.sh[0]);
       med = __ddiv_rn(__dadd_rn(lo, hi), 2.0);
     }
   }
 
   double part = 0.0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const double y = in_smem ? __longlong_as_double(static_cast<long long>(sm.keys[k]))
+    const double y = in_smem ? __longlong_as_double(static_cast<long long>(sm.keys()[k]))
                              : xy64[b + k].y;
     part += fabs(__dsub_rn(y, med));
   }
@@ -514,8 +563,7 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
             double2* xy64, float2* __restrict__ xy32, double4* __restrict__ stat,
             double* __restrict__ norm, int cap) {
   __shared__ PrepShared sm;
-  extern __shared__ __align__(16) unsigned char prep_dyn[];
-  prep_smem_setup(sm, prep_dyn, cap);
+  prep_smem_setup(sm, cap);
   prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
 }
 
@@ -693,7 +741,7 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
 // One CTA per cluster (big_list == nullptr), or persistent CTAs working
 // through the list of clusters the warp kernel left for them
 // (big_ctl[0] = count, big_ctl[1] = claim counter).
-__global__ void __launch_bounds__(kPrepThreads)
+__global__ void __launch_bounds__(kPrepThreads, 4)
 prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 const double* __restrict__ az, const double* __restrict__ dop, double scale,
                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
@@ -702,8 +750,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc, int cap,
                 const int32_t* __restrict__ big_list, int32_t* big_ctl) {
   __shared__ PrepShared sm;
-  extern __shared__ __align__(16) unsigned char prep_dyn[];
-  prep_smem_setup(sm, prep_dyn, cap);
+  prep_smem_setup(sm, cap);
   __shared__ int tile_pos[2];
   __shared__ int s_idx;
   if (big_list == nullptr) {
@@ -1953,7 +2000,9 @@ CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env
   t = t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : 256));
   int cap = std::max(512, t * 8);
   if (!select) cap = env_int("RVK_PREP_CAP", cap);
-  cap = std::min(2048, std::max(256, cap));
+  // >= 512: prep_cluster's reduction scratch; multiple of 32: 16-byte
+  // aligned histogram
+  cap = std::min(2048, std::max(512, cap)) & ~31;
   return {t, cap};
 }
 

@@ -12,3 +12,6 @@ for r in 1 2; do
   done
 done
 cp paper_2012_12618_b200/lib/ab/_orig.so paper_2012_12618_b200/lib/librvk_gpu.so
+if [ -n "$AB_TESTS" ]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log
+fi
