@@ -787,10 +787,20 @@ struct WarpPrep {
   unsigned int hist[kWarpCap];
 };
 
-__device__ __forceinline__ double warp_fmin(double v) {
+// Warp-wide (min, max, min, max) of non-NaN partials: plain compares (no
+// fmin NaN handling), the four butterflies interleaved.
+__device__ __forceinline__ void warp_minmax2(double& lo0, double& hi0, double& lo1, double& hi1) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double a = __shfl_xor_sync(0xffffffffu, lo0, o);
+    const double b = __shfl_xor_sync(0xffffffffu, hi0, o);
+    const double c = __shfl_xor_sync(0xffffffffu, lo1, o);
+    const double d = __shfl_xor_sync(0xffffffffu, hi1, o);
+    lo0 = a < lo0 ? a : lo0;
+    hi0 = b > hi0 ? b : hi0;
+    lo1 = c < lo1 ? c : lo1;
+    hi1 = d > hi1 ? d : hi1;
+  }
 }
 __device__ __forceinline__ int warp_imin(int v) {
 #pragma unroll
@@ -874,14 +884,9 @@ __device__ unsigned long long warp_radix_select(WarpPrep& w, int n, int k, int l
   return prefix;
 }
 // k-th and (k+1)-th smallest keys, exact (warp version of block_select_pair).
-__device__ void warp_select_pair(WarpPrep& w, int n, int k, bool pair, int lane,
+// On entry w.hist[0, nb) holds the bucket histogram of the n keys.
+__device__ void warp_select_pair(WarpPrep& w, int n, int k, bool pair, int nb, int lane,
                                  unsigned long long& v0, unsigned long long& v1) {
-  int nb = 32;
-  while (nb < n) nb <<= 1;  // <= kWarpCap buckets, about one per point
-  for (int i = lane; i < nb; i += 32) w.hist[i] = 0;
-  __syncwarp();
-  for (int i = lane; i < n; i += 32) atomicAdd(&w.hist[med_bin(w.keys[i], nb)], 1u);
-  __syncwarp();
   int bin, below;
   warp_find_rank(w.hist, nb >> 5, k, lane, bin, below);
   const int in_bin = static_cast<int>(w.hist[bin]);
@@ -957,6 +962,11 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
     return;
   }
+  // median buckets (<= kWarpCap, about one per point), zeroed here and
+  // filled by the normalize pass
+  int nb = 32;
+  while (nb < n) nb <<= 1;
+  for (int i = lane; i < nb; i += 32) w.hist[i] = 0;
   // normalize_cluster (src/ransac.cpp:69-87)
   double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
   for (int k = lane; k < n; k += 32) {
@@ -966,10 +976,11 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     lo1 = d < lo1 ? d : lo1;
     hi1 = d > hi1 ? d : hi1;
   }
-  lo0 = warp_first_zero(warp_fmin(lo0), az + b, n, lane);
-  hi0 = warp_first_zero(-warp_fmin(-hi0), az + b, n, lane);
-  lo1 = warp_first_zero(warp_fmin(lo1), dop + b, n, lane);
-  hi1 = warp_first_zero(-warp_fmin(-hi1), dop + b, n, lane);
+  warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
+  lo0 = warp_first_zero(lo0, az + b, n, lane);
+  hi0 = warp_first_zero(hi0, az + b, n, lane);
+  lo1 = warp_first_zero(lo1, dop + b, n, lane);
+  hi1 = warp_first_zero(hi1, dop + b, n, lane);
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   float2* p32 = xy32 + xy32_base(offsets, c);
@@ -983,11 +994,17 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const double y1 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d1, lo1), s1);
     xy64[b + k0] = make_double2(x0, y0);
     xy32_put(p32, k0, __double2float_rn(x0), __double2float_rn(y0));
-    w.keys[k0] = static_cast<unsigned long long>(__double_as_longlong(y0)) & ~(1ull << 63);
+    const unsigned long long key0 =
+        static_cast<unsigned long long>(__double_as_longlong(y0)) & ~(1ull << 63);
+    w.keys[k0] = key0;
+    atomicAdd(&w.hist[med_bin(key0, nb)], 1u);
     if (k1 < n) {
       xy64[b + k1] = make_double2(x1, y1);
       xy32_put(p32, k1, __double2float_rn(x1), __double2float_rn(y1));
-      w.keys[k1] = static_cast<unsigned long long>(__double_as_longlong(y1)) & ~(1ull << 63);
+      const unsigned long long key1 =
+          static_cast<unsigned long long>(__double_as_longlong(y1)) & ~(1ull << 63);
+      w.keys[k1] = key1;
+      atomicAdd(&w.hist[med_bin(key1, nb)], 1u);
     }
   }
   if (lane == 0 && (n & 1)) xy32_put(p32, n, 0.f, kPadY);
@@ -995,7 +1012,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   // median (ransac.hpp:53-70) and the MAD interval (see prep_cluster)
   const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
   unsigned long long v0 = 0, v1 = 0;
-  warp_select_pair(w, n, k0, (n & 1) == 0, lane, v0, v1);
+  warp_select_pair(w, n, k0, (n & 1) == 0, nb, lane, v0, v1);
   const double d0 = __longlong_as_double(static_cast<long long>(v0));
   const double med = (n & 1) ? d0
                              : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))), 2.0);

@@ -34,6 +34,7 @@ __device__ __forceinline__ void init_h(Hy& h, uint32_t base) {
 // V=0: per point, per pair: B-step, A-step, square (production shape)
 // V=1: per point pair: all B-steps, then all A-steps, then squares
 // V=2: point-pair packing: smem float4 (x1,x2,y1,y2); hypothesis scalars
+// V=6..8: V=2 with some FFMA2 steps as scalar FFMA (measured slower, mb4)
 __device__ float4 g_pts[64][kPts / 2];  // V=4: points in global memory (L1-cached broadcast)
 
 template <int V, int TH, int MINB, int UNR>
@@ -117,6 +118,36 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
           cnt[2 * q] += __float_as_uint(eb.x) >> 31;
           cnt[2 * q + 1] += __float_as_uint(eb.y) >> 31;
         }
+      } else if (V >= 6) {
+        // V=6: as V=2 but the square step as two scalar FFMA
+        // V=7: as V=2 but the B step as two scalar FFMA
+        // V=8: all scalar FFMA (3 per eval)
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float a = hh ? h.A[q].y : h.A[q].x, b = hh ? h.B[q].y : h.B[q].x;
+            const float c = hh ? h.C[q].y : h.C[q].x, t = hh ? h.T[q].y : h.T[q].x;
+            float2 e, g;
+            if (V == 8) {
+              e.x = __fmaf_rn(X.x, a, __fmaf_rn(Y.x, b, c));
+              e.y = __fmaf_rn(X.y, a, __fmaf_rn(Y.y, b, c));
+            } else if (V == 7) {
+              const float2 u = make_float2(__fmaf_rn(Y.x, b, c), __fmaf_rn(Y.y, b, c));
+              e = __ffma2_rn(X, make_float2(a, a), u);
+            } else {
+              e = __ffma2_rn(X, make_float2(a, a), __ffma2_rn(Y, make_float2(b, b), make_float2(c, c)));
+            }
+            if (V == 7) {
+              g = __ffma2_rn(e, e, make_float2(t, t));
+            } else {
+              g.x = __fmaf_rn(e.x, e.x, t);
+              g.y = __fmaf_rn(e.y, e.y, t);
+            }
+            cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+          }
+        }
       } else {
         // v = (x1, x2, y1, y2)
         const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
@@ -192,21 +223,13 @@ int main() {
     for (size_t i = 0; i < h.size(); ++i) h[i] = make_float4(0.1f * (i % 7), 0.2f, 0.3f * (i % 3), 0.4f);
     CK(cudaMemcpyToSymbol(g_pts, h.data(), h.size() * sizeof(float4)));
   }
-  run<5, 256, 2, 2>(sms, peak, du);
-  run<5, 256, 3, 2>(sms, peak, du);
-  run<5, 256, 2, 4>(sms, peak, du);
-  run<0, 256, 2, 2>(sms, peak, du);
-  run<3, 256, 3, 1>(sms, peak, du);
-  run<3, 256, 2, 1>(sms, peak, du);
-  run<3, 128, 6, 1>(sms, peak, du);
-  run<0, 256, 3, 2>(sms, peak, du);
-  run<0, 256, 2, 4>(sms, peak, du);
-  run<0, 128, 6, 2>(sms, peak, du);
-  run<0, 128, 4, 1>(sms, peak, du);
-  run<1, 256, 2, 2>(sms, peak, du);
-  run<1, 256, 3, 1>(sms, peak, du);
   run<2, 256, 2, 2>(sms, peak, du);
-  run<2, 256, 3, 2>(sms, peak, du);
   run<2, 128, 4, 2>(sms, peak, du);
+  run<6, 256, 2, 2>(sms, peak, du);
+  run<6, 128, 4, 2>(sms, peak, du);
+  run<7, 256, 2, 2>(sms, peak, du);
+  run<7, 128, 4, 2>(sms, peak, du);
+  run<8, 256, 2, 2>(sms, peak, du);
+  run<8, 128, 4, 2>(sms, peak, du);
   return 0;
 }
