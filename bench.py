@@ -554,12 +554,15 @@ def main():
         dbuf.copy_(hbuf, non_blocking=True)
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ea.record()
-    for _ in range(10):
-        dbuf.copy_(hbuf, non_blocking=True)
-    eb.record()
-    eb.synchronize()
-    h2d_peak = 10 * hbuf.numel() * 4 / (ea.elapsed_time(eb) / 1e3) / 1e9
+    best_ms = float("inf")
+    for _ in range(5):  # best of 5 bursts of 10 copies (the link's rate varies run to run)
+        ea.record()
+        for _ in range(10):
+            dbuf.copy_(hbuf, non_blocking=True)
+        eb.record()
+        eb.synchronize()
+        best_ms = min(best_ms, ea.elapsed_time(eb))
+    h2d_peak = 10 * hbuf.numel() * 4 / (best_ms / 1e3) / 1e9
     h2d_ach = h2d / (e2e_t / args.e2e_steps) / 1e9
     e2e = {"value": e2e_evals / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_t * 1e3 / args.e2e_steps,

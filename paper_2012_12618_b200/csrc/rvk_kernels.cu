@@ -1279,20 +1279,21 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
         cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
       }
     };
-    // 4. broadcast LDS.128 (two points), two float4 per iteration, one ahead
+    // 4. broadcast LDS.128 (two points each), four float4 per iteration
+    //    (the other warps of the sub-partition cover the LDS latency)
     const float4* cp = pts_s[tid >> 5][buf];
     const int m2 = (d.z + 1) >> 1;
-    float4 v0 = cp[0], v1 = cp[1];
     int q2 = 0;
 #pragma unroll 1
-    for (; q2 + 2 <= m2; q2 += 2) {
-      const float4 v2 = cp[q2 + 2], v3 = cp[q2 + 3];
+    for (; q2 + 4 <= m2; q2 += 4) {
+      const float4 v0 = cp[q2], v1 = cp[q2 + 1], v2 = cp[q2 + 2], v3 = cp[q2 + 3];
       score_pair(v0);
       score_pair(v1);
-      v0 = v2;
-      v1 = v3;
+      score_pair(v2);
+      score_pair(v3);
     }
-    if (q2 < m2) score_pair(v0);
+#pragma unroll 1
+    for (; q2 < m2; ++q2) score_pair(cp[q2]);
     if (active) {
       int32_t* up = upper + (static_cast<int64_t>(d.x) * g.Tg + gi) * 8;
 #pragma unroll
