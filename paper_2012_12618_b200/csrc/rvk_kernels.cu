@@ -1827,14 +1827,14 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
     RefitAcc acc;
     bool und = false;
     const int nt = blockDim.x;
-    // four points per thread and step, every load issued before the first
+    // two points per thread and step, every load issued before the first
     // use (the loop is latency-bound: few points per thread, one CTA per
-    // cluster)
-    for (int k0 = threadIdx.x; k0 < n; k0 += 4 * nt) {
-      float2 pp[4];
-      double pa[4], pd[4];
+    // cluster; four deep costs more in spills than it hides, measured)
+    for (int k0 = threadIdx.x; k0 < n; k0 += 2 * nt) {
+      float2 pp[2];
+      double pa[2], pd[2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 2; ++u) {
         const int k = k0 + u * nt;
         if (k < n) {
           pp[u] = xy32_get(p32, k);
@@ -1845,7 +1845,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 2; ++u) {
         const int k = k0 + u * nt;
         if (k >= n) break;
         const int d = H.L.degenerate ? kOut : classify(H, k, pp[u], p64, thr_lo, thr_hi);
