@@ -702,7 +702,8 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
     return;
   }
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
-  for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) {
+  // hyp == nullptr: hyp_kernel builds the hypotheses and zeroes the counters
+  for (int t = threadIdx.x; hyp != nullptr && t < g.Tg * 8; t += blockDim.x) {
     FastHyp f = inert_fast();
     if (t < g.T) {
       int i, j;
@@ -1031,8 +1032,8 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
   // two trials per lane and step: both seed pairs' loads are in flight
-  // before the first FP64 line is built
-  for (int t0 = lane; t0 < g.Tg * 8; t0 += 64) {
+  // before the first FP64 line is built (hyp == nullptr: hyp_kernel does it)
+  for (int t0 = lane; hyp != nullptr && t0 < g.Tg * 8; t0 += 64) {
     const int t1 = t0 + 32;
     const bool a0 = t0 < g.T, a1 = t1 < g.T;
     int i0 = 0, j0 = 0, i1 = 0, j1 = 0;
@@ -1078,6 +1079,39 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       tiles[bk * tile_cap + pos1 + hb] =
           make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
   }
+}
+
+// Every trial's FP32 fast-pass hypothesis and zeroed counter, one thread per
+// trial over all clusters (after the prep kernels have written xy64 and the
+// threshold interval): the same seed pair, FP64 line and coefficients as
+// prep_hyp_body, without the per-cluster kernel's barriers in its way.
+__global__ void __launch_bounds__(256)
+hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+           const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed,
+           const double2* __restrict__ xy64, const double4* __restrict__ stat,
+           float* __restrict__ hyp, int32_t* __restrict__ upper) {
+  const int tg8 = g.Tg * 8;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(n_clusters) * tg8) return;
+  const int c = static_cast<int>(idx / tg8);
+  const int t = static_cast<int>(idx - static_cast<int64_t>(c) * tg8);
+  FastHyp f = inert_fast();
+  if (t < g.T) {
+    const int64_t b = offsets[c];
+    const int n = static_cast<int>(offsets[c + 1] - b);
+    const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+    const double4 st = stat[c];
+    int i, j;
+    seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+    const double2 p = xy64[b + i], q = xy64[b + j];
+    f = make_fast_from_seeds(p.x, p.y, q.x, q.y, st.x, st.y);
+  }
+  float* h = hyp + static_cast<int64_t>(c) * g.Tg * 32 + (t >> 3) * 32 + (t & 7);
+  h[0] = f.A;
+  h[8] = f.B;
+  h[16] = f.C;
+  h[24] = -f.t2hi;  // K: the squared compare's bound
+  upper[idx] = 0;   // rows of Tg * 8 counters, cluster-major
 }
 
 // The exact reference threshold (left-to-right MAD sum), one warp per
@@ -2045,6 +2079,16 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
 // MMA of 128 x 256 x 8 keeps the tensor pipe busy ~470 cycles, so the tensor
 // path caps near 70 evals/cycle/SM while its epilogue still needs one ALU
 // instruction per eval (profiles/r1c_summary.md). RVK_SCORE=tc selects it.
+// Hypotheses inside the per-cluster prep kernels (default) or in their own
+// one-thread-per-trial kernel (RVK_HYP_KERNEL=1). Measured on B200
+// (gpurun_out/hk1): the split is slower -- config 2 prep + hypotheses 0.094
+// -> 0.108 ms -- because inside the prep kernels the hypothesis loop fills
+// the issue slots the latency-bound median phases of the other CTAs leave.
+bool hyp_kernel_enabled() {
+  static const bool v = env_int("RVK_HYP_KERNEL", 0) != 0;
+  return v;
+}
+
 bool score_uses_tc() {
   static const bool v = [] {
     const char* e = std::getenv("RVK_SCORE");
@@ -2070,13 +2114,24 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
   }
   const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
   const int64_t avg = f.n_points / f.n_clusters;
+  // hypotheses by hyp_kernel (one thread per trial) instead of inside the
+  // per-cluster prep kernels
+  const bool split = !s.tc && hyp_kernel_enabled();
+  float* prep_hyp_out = split ? nullptr : s.hyp;
+  auto launch_hyps = [&]() {
+    if (!split) return;
+    const int64_t total = static_cast<int64_t>(f.n_clusters) * g.Tg * 8;
+    hyp_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        f.n_clusters, f.offsets, f.keys, g, p.rng_seed, s.xy64, s.stat, s.hyp, s.upper);
+    count_launch();
+  };
   if (!s.tc && env_int("RVK_PREP_WARP", avg < 384 ? 1 : 0) != 0) {
     // warp per cluster up to kWarpCap points; the rest by persistent CTAs
     cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 2, st);
     prep_warp_kernel<<<(f.n_clusters + kPrepWarps - 1) / kPrepWarps, kPrepWarps * 32, 0, st>>>(
         f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, s.big_list,
-        s.big_ctl);
+        s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap,
+        s.big_list, s.big_ctl);
     count_launch();
     static int big_grid = 0;
     if (big_grid == 0) {
@@ -2087,16 +2142,18 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
     }
     prep_hyp_kernel<<<std::min<int64_t>(big_grid, f.n_clusters), 256, prep_dyn_bytes(2048), st>>>(
         f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, 2048,
-        s.big_list, s.big_ctl);
+        s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
+        2048, s.big_list, s.big_ctl);
     count_launch();
+    launch_hyps();
     return;
   }
   prep_hyp_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, tc, sh.cap,
-      nullptr, nullptr);
+      s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
+      sh.cap, nullptr, nullptr);
   count_launch();
+  launch_hyps();
 }
 
 namespace {

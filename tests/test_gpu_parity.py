@@ -35,8 +35,8 @@ def test_native_library_is_the_cuda_one(gpu_lib):
     off = np.array([0, 5], np.int64)
     rvk.run_ransac_csr(off, np.linspace(0, 1, 5), np.linspace(1, 2, 5), rvk.RansacParams(8))
     # prep (one CTA per cluster, or warp-per-cluster + persistent CTAs for
-    # the large clusters), score, select
-    assert gpu_lib.rvk_kernel_launches() in (3, 4)
+    # the large clusters), hypotheses (unless RVK_HYP_KERNEL=0), score, select
+    assert gpu_lib.rvk_kernel_launches() in (3, 4, 5)
 
 
 def test_seed_pairs_vs_oracle(gpu_lib, oracle):
@@ -330,12 +330,16 @@ def est_dtype():
 @pytest.mark.parametrize("env", [{"RVK_SCORE": "tc"},
                                  {"RVK_PREP_THREADS": "256", "RVK_SELECT_THREADS": "256"},
                                  {"RVK_PREP_THREADS": "64", "RVK_SELECT_THREADS": "64"},
-                                 {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0"}],
-                         ids=["tensor_core_scoring", "cta256", "cta64", "warp_prep", "cta_prep"])
+                                 {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0"},
+                                 {"RVK_HYP_KERNEL": "1"},
+                                 {"RVK_HYP_KERNEL": "1", "RVK_PREP_WARP": "1"}],
+                         ids=["tensor_core_scoring", "cta256", "cta64", "warp_prep", "cta_prep",
+                              "hyp_kernel", "hyp_kernel_warp_prep"])
 def test_alternative_kernel_shapes_parity(gpu_lib, env):
     """Every kernel variant must give the same bytes: the tcgen05 scoring
-    kernel (RVK_SCORE=tc), the per-cluster CTA shapes of prep/select and the
-    warp-per-cluster prep (normally chosen from the mean cluster size). The golden, C3 and
+    kernel (RVK_SCORE=tc), the per-cluster CTA shapes of prep/select, the
+    warp-per-cluster prep (normally chosen from the mean cluster size) and the
+    separate one-thread-per-trial hypothesis kernel (RVK_HYP_KERNEL=1). The golden, C3 and
     full-size parity tests re-run in a child process with the variant
     selected (selections are read once per process)."""
     r = subprocess.run(
