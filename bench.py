@@ -40,6 +40,7 @@ sys.path.insert(0, ROOT)
 METRIC = "hypothesis_point_evals_per_sec"
 UNIT = "evals/s"
 FLOP_PER_EVAL = 4  # 1 mul + 2 add + 1 div (ref form) == 2 FMA (affine form)
+HW_FLOP_PER_EVAL = 6  # executed: 3 FMA per eval (affine form + squared corridor compare)
 
 
 def parse():
@@ -450,6 +451,11 @@ def main():
                 "frac_of_nominal": achieved / nominal,
                 "nominal_peak": nominal,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals_per_launch,
+                # what the FP32 pipe executes: 3 FMA (6 FLOP) per eval (A*x + (B*y + C),
+                # then e*e - t2hi), two evals per FFMA2; the north star's
+                # "FP32-pipe utilisation" is this fraction (ncu: fma_pipe_active_pct)
+                "hw_flop_per_eval": HW_FLOP_PER_EVAL,
+                "hw_frac": achieved * HW_FLOP_PER_EVAL / FLOP_PER_EVAL / peak,
                 "avg_launch_ms": score_ms, "traffic": traffic,
                 "ncu": ncu_info,
                 "share_of_step": stage_ms[2] / total_ms if total_ms else None,
