@@ -1217,6 +1217,19 @@ __device__ __forceinline__ void stage_points(float4* slot, const float2* __restr
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// The same staging through the TMA engine: one 1-D bulk copy issued by lane 0,
+// completion (bytes) tracked on the slot's mbarrier.
+__device__ __forceinline__ void stage_points_bulk(float4* slot, uint64_t* bar,
+                                                  const float2* __restrict__ xy32, int4 d,
+                                                  int lane) {
+  if (lane == 0) {
+    const uint32_t bytes = static_cast<uint32_t>((d.z + 1) >> 1) * 16u;
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(slot, xy32 + d.y, bytes, bar);
+  }
+}
+
+template <bool kBulk>
 __global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
@@ -1226,7 +1239,14 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
   // two point slots per warp: the current unit's and the next unit's (prefetch)
   extern __shared__ __align__(16) float4 pts_dyn[];
   auto pts_s = reinterpret_cast<float4(*)[2][kSlot]>(pts_dyn);
+  __shared__ __align__(8) uint64_t slot_bar[kScoreThreads / 32][2];  // kBulk: per slot
   const int tid = threadIdx.x, lane = tid & 31;
+  if (kBulk && lane == 0) {
+    mbar_init(&slot_bar[tid >> 5][0], 1);
+    mbar_init(&slot_bar[tid >> 5][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t phase = 0;  // kBulk: parity bit per slot (bit b = slot b)
   if (tid < 32) {  // exclusive prefix of the bucket sizes
     int carry = 0;
     for (int b0 = 0; b0 < kTileBuckets; b0 += 32) {
@@ -1255,7 +1275,8 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
   int buf = 0;
   if (u < total) {
     d = unit_desc(bstart, tiles, tile_cap, u);
-    stage_points(pts_s[tid >> 5][0], xy32, d, lane);
+    if (kBulk) stage_points_bulk(pts_s[tid >> 5][0], &slot_bar[tid >> 5][0], xy32, d, lane);
+    else stage_points(pts_s[tid >> 5][0], xy32, d, lane);
   }
 #pragma unroll 1
   while (u < total) {
@@ -1289,13 +1310,21 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     int4 dn = make_int4(0, 0, 0, 0);
     if (u_next < total) {
       dn = unit_desc(bstart, tiles, tile_cap, u_next);
-      stage_points(pts_s[tid >> 5][buf ^ 1], xy32, dn, lane);
-    } else {
+      if (kBulk)  // the slot was last read one unit ago (the warp is converged)
+        stage_points_bulk(pts_s[tid >> 5][buf ^ 1], &slot_bar[tid >> 5][buf ^ 1], xy32, dn, lane);
+      else
+        stage_points(pts_s[tid >> 5][buf ^ 1], xy32, dn, lane);
+    } else if (!kBulk) {
       asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
     }
     if (lane == 0) un = atomicAdd(next, 1);
-    // 3. this unit's points have landed (all but the newest group)
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    // 3. this unit's points have landed
+    if (kBulk) {
+      mbar_wait(&slot_bar[tid >> 5][buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    } else {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // all but the newest group
+    }
     __syncwarp();
 
     uint32_t cnt[kNH];
@@ -2089,6 +2118,16 @@ bool hyp_kernel_enabled() {
   return v;
 }
 
+// Point staging of score_kernel: TMA bulk copies with an mbarrier per slot
+// (default) or per-lane cp.async (RVK_SCORE_STAGE=lanes).
+bool score_uses_bulk() {
+  static const bool v = [] {
+    const char* e = std::getenv("RVK_SCORE_STAGE");
+    return !(e && std::strcmp(e, "lanes") == 0);
+  }();
+  return v;
+}
+
 bool score_uses_tc() {
   static const bool v = [] {
     const char* e = std::getenv("RVK_SCORE");
@@ -2164,9 +2203,10 @@ int score_grid(int64_t max_units) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kScoreSmemBytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads,
+    for (auto k : {score_kernel<true>, score_kernel<false>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(kScoreSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<true>, kScoreThreads,
                                                   kScoreSmemBytes);
     per_sm = std::max(1, std::min(per_sm, env_int("RVK_SCORE_CTAS", per_sm)));
     grid = sms * per_sm;
@@ -2202,9 +2242,12 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   }
   const ScoreGeom g = score_geom(p.max_trials);
   const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
-  score_kernel<<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
-      s.tile_count, s.tiles, s.tile_cap,
-                                                                s.xy32, s.hyp, g, s.upper);
+  if (score_uses_bulk())
+    score_kernel<true><<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
+        s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+  else
+    score_kernel<false><<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
+        s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
   count_launch();
 }
 

@@ -332,9 +332,10 @@ def est_dtype():
                                  {"RVK_PREP_THREADS": "64", "RVK_SELECT_THREADS": "64"},
                                  {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0"},
                                  {"RVK_HYP_KERNEL": "1"},
-                                 {"RVK_HYP_KERNEL": "1", "RVK_PREP_WARP": "1"}],
+                                 {"RVK_HYP_KERNEL": "1", "RVK_PREP_WARP": "1"},
+                                 {"RVK_SCORE_STAGE": "lanes"}],
                          ids=["tensor_core_scoring", "cta256", "cta64", "warp_prep", "cta_prep",
-                              "hyp_kernel", "hyp_kernel_warp_prep"])
+                              "hyp_kernel", "hyp_kernel_warp_prep", "cp_async_staging"])
 def test_alternative_kernel_shapes_parity(gpu_lib, env):
     """Every kernel variant must give the same bytes: the tcgen05 scoring
     kernel (RVK_SCORE=tc), the per-cluster CTA shapes of prep/select, the
