@@ -2007,6 +2007,172 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   }
 }
 
+// ------------------------------------------------ warp-per-cluster select
+//
+// The same exact winner / mask / refit as select_kernel with ONE warp per
+// cluster and no block barriers (imaging-radar frames: thousands of clusters
+// of a few hundred points, where select_kernel's CTAs spend their time in
+// barrier and latency chains). Candidates are found 32 trials at a time
+// with a ballot over the upper bounds.
+constexpr int kSelectWarps = 4;
+
+__device__ __forceinline__ RefitAcc warp_reduce_refit(RefitAcc a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a.g00 += __shfl_xor_sync(0xffffffffu, a.g00, o);
+    a.g01 += __shfl_xor_sync(0xffffffffu, a.g01, o);
+    a.g11 += __shfl_xor_sync(0xffffffffu, a.g11, o);
+    a.b0 += __shfl_xor_sync(0xffffffffu, a.b0, o);
+    a.b1 += __shfl_xor_sync(0xffffffffu, a.b1, o);
+    a.ds += __shfl_xor_sync(0xffffffffu, a.ds, o);
+    a.nin += __shfl_xor_sync(0xffffffffu, a.nin, o);
+    a.first = min(a.first, __shfl_xor_sync(0xffffffffu, a.first, o));
+  }
+  return a;
+}
+
+__global__ void __launch_bounds__(kSelectWarps * 32)
+select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                   const double* __restrict__ az, const double* __restrict__ dop,
+                   const int32_t* __restrict__ keys, const int32_t* __restrict__ cluster_ids,
+                   int64_t frame_id, const double2* __restrict__ xy64,
+                   const float2* __restrict__ xy32, const double4* __restrict__ stat,
+                   double scale, const int32_t* __restrict__ upper, int T, uint64_t seed,
+                   int32_t* __restrict__ out_count, int32_t* __restrict__ out_trial,
+                   uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kSelectWarps + (threadIdx.x >> 5);
+  if (c >= n_clusters) return;
+  const int64_t b = offsets[c];
+  const int n = static_cast<int>(offsets[c + 1] - b);
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double4 st = stat[c];
+  double thr_lo = st.x, thr_hi = st.y;
+  const float2* p32 = xy32 + xy32_base(offsets, c);
+  const double2* p64 = xy64 + b;
+  const double* caz = az + b;
+  const double* cdop = dop + b;
+  uint8_t* cmask = mask + b;
+  const int32_t* U = upper + static_cast<int64_t>(c) * ((T + 7) / 8) * 8;
+  const bool refit = est != nullptr;
+
+  auto go_exact = [&]() {  // the exact sequential threshold (rare)
+    double t = 0.0;
+    if (lane == 0) t = exact_threshold(p64, n, st.z, scale);
+    thr_lo = thr_hi = __shfl_sync(0xffffffffu, t, 0);
+  };
+  // one pass for trial t: mask + exact count + refit sums (false: undecided)
+  auto pass = [&](int t, int& count, RefitAcc& total) -> bool {
+    const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
+    RefitAcc acc;
+    bool und = false;
+    for (int k0 = lane; k0 < n; k0 += 64) {
+      float2 pp[2];
+      double pa[2], pd[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + 32 * u;
+        if (k < n) {
+          pp[u] = xy32_get(p32, k);
+          if (refit) {
+            pa[u] = caz[k];
+            pd[u] = cdop[k];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = k0 + 32 * u;
+        if (k >= n) break;
+        const int d = H.L.degenerate ? kOut : classify(H, k, pp[u], p64, thr_lo, thr_hi);
+        und |= d == kUndecided;
+        cmask[k] = d == kIn ? 1 : 0;
+        if (d == kIn) {
+          if (refit) acc.add(k, pa[u], pd[u]);
+          else ++acc.nin;
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, und)) return false;
+    total = warp_reduce_refit(acc);
+    count = total.nin;
+    return true;
+  };
+
+  // 1. trial with the largest upper bound (lowest index on ties)
+  unsigned long long v = 0;
+  {
+    const int4* U4 = reinterpret_cast<const int4*>(U);
+    for (int q = lane; 4 * q < T; q += 32) {
+      const int4 w = U4[q];
+      const int t = 4 * q;
+      v = MaxU64()(v, pack_best(w.x, t));
+      if (t + 1 < T) v = MaxU64()(v, pack_best(w.y, t + 1));
+      if (t + 2 < T) v = MaxU64()(v, pack_best(w.z, t + 2));
+      if (t + 3 < T) v = MaxU64()(v, pack_best(w.w, t + 3));
+    }
+  }
+  v = warp_reduce(v, MaxU64());
+  const int t0 = unpack_trial(v);
+  const int u0 = unpack_count(v);
+
+  // 2. its exact count, mask and refit sums in one pass
+  int e0 = 0;
+  RefitAcc tot;
+  if (!pass(t0, e0, tot)) {
+    go_exact();
+    pass(t0, e0, tot);
+  }
+  unsigned long long best = pack_best(e0, t0);
+
+  // 3. verify the trials that could still win (none when u0 == e0); the
+  //    candidates of 32 trials at a time by ballot
+  if (u0 > e0) {
+    for (int round = 0; round < 2; ++round) {
+      bool need_exact = false;
+      for (int tb = 0; tb < T; tb += 32) {
+        const int tl = tb + lane;
+        const int u = tl < T ? U[tl] : -1;
+        unsigned cand = __ballot_sync(
+            0xffffffffu, tl < T && tl != t0 && !(u < e0 || (u == e0 && tl > t0)));
+        while (cand) {
+          const int t = tb + __ffs(cand) - 1;
+          cand &= cand - 1;
+          const ExactHyp H =
+              make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
+          bool und;
+          const int e = warp_exact_count(H, n, p32, p64, thr_lo, thr_hi, &und);
+          if (und) need_exact = true;
+          else best = MaxU64()(best, pack_best(e, t));
+        }
+      }
+      if (need_exact && round == 0) {
+        go_exact();  // redo every candidate (and t0) with the exact threshold
+        pass(t0, e0, tot);
+        best = pack_best(e0, t0);
+        continue;
+      }
+      break;
+    }
+  }
+  const int win = unpack_trial(best);
+  const int win_count = unpack_count(best);
+
+  // 4. another trial won: its mask and refit sums
+  if (win != t0) {
+    int cnt;
+    if (!pass(win, cnt, tot)) {
+      go_exact();
+      pass(win, cnt, tot);
+    }
+  }
+  if (lane == 0) {
+    if (out_count) out_count[c] = win_count;
+    if (out_trial) out_trial[c] = win;
+    if (refit) finish_refit(tot, caz, cdop, frame_id, cluster_ids ? cluster_ids[c] : c, est + c);
+  }
+}
+
 __global__ void __launch_bounds__(kSelectThreads)
 refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
              const double* __restrict__ dop, const int32_t* __restrict__ cluster_ids,
@@ -2254,6 +2420,16 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
 void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                    const Outputs& o, cudaStream_t st) {
   if (f.n_clusters == 0) return;
+  const int64_t avg = f.n_points / f.n_clusters;
+  if (env_int("RVK_SELECT_WARP", avg < 384 ? 1 : 0) != 0) {  // warp per cluster
+    select_warp_kernel<<<(f.n_clusters + kSelectWarps - 1) / kSelectWarps, kSelectWarps * 32, 0,
+                         st>>>(f.n_clusters, f.offsets, f.azimuth, f.doppler, f.keys,
+                               f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
+                               p.threshold_scale, s.upper, p.max_trials, p.rng_seed,
+                               o.inlier_count, o.winning_trial, o.mask, o.est);
+    count_launch();
+    return;
+  }
   const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_SELECT_THREADS", true);
   select_kernel<<<f.n_clusters, sh.threads, 0, st>>>(
       f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
