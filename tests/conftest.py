@@ -130,3 +130,26 @@ def assert_estimates_close(got, want, rel=1e-4, heading_tol=1e-3, label=""):
     h = want["has_heading"] == 1
     dh = np.abs(np.remainder(got["heading"][h] - want["heading"][h] + np.pi, 2 * np.pi) - np.pi)
     assert (dh <= heading_tol).all(), f"{label} heading off by {dh.max()}"
+
+
+def extreme_value_clusters():
+    """Frames that stress the exactness scheme: three-point clusters, signed
+    zeros (Eigen's first-occurrence min/max), magnitudes near the FP64
+    extremes, subnormal spreads, wide dynamic ranges. Shared by the oracle's
+    check against the reference build and the GPU parity test."""
+    rng = np.random.default_rng(23)
+    tiny = np.nextafter(0.0, 1.0)
+    return [
+        [np.array([[0.1, 1.0], [0.2, 2.0], [0.3, 2.5]]),
+         np.array([[0.5, 1.0], [0.5, 3.0], [0.5, 2.0]])],
+        [np.array([[-0.0, 1.0], [0.0, -0.0], [0.0, 0.0], [-0.0, 2.0], [1.0, -0.0]])],
+        [np.stack([rng.uniform(-1, 1, 64) * 1e150, rng.uniform(-1, 1, 64) * 1e-150], 1)],
+        [np.stack([rng.uniform(0, 1, 64) * 1e-300, rng.uniform(-1, 1, 64)], 1)],
+        [np.stack([np.arange(40) * tiny, rng.uniform(-1, 1, 40) * 1e10], 1)],
+        [np.stack([rng.uniform(-np.pi, np.pi, 300),
+                   np.where(rng.uniform(size=300) < 0.5, 1e-9, 1e9) * rng.uniform(-1, 1, 300)],
+                  1)],
+    ]
+
+
+EXTREME_PARAMS = [(1, 1.0), (40, 1.0), (257, 0.5), (64, 1e-6)]

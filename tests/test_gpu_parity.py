@@ -15,7 +15,7 @@ import pytest
 
 import paper_2012_12618_b200 as rvk
 from paper_2012_12618_b200 import workloads as W
-from conftest import ROOT, assert_estimates_close
+from conftest import EXTREME_PARAMS, ROOT, assert_estimates_close, extreme_value_clusters
 from oracle.binding import make_params
 
 pytestmark = pytest.mark.gpu
@@ -215,6 +215,22 @@ def test_edge_cases(gpu_lib, oracle):
             np.testing.assert_array_equal(r.mask, o.mask)
             np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
             np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
+
+
+def test_edge_cases_extreme_values(gpu_lib, oracle):
+    """conftest.extreme_value_clusters (three-point clusters, signed zeros,
+    FP64-extreme magnitudes, subnormal spreads): every decision bit-exact."""
+    for cl in extreme_value_clusters():
+        off, az, dop = rvk.clusters_to_csr(cl)
+        for T, scale in EXTREME_PARAMS:
+            p = rvk.RansacParams(T, scale, 5)
+            r, est = rvk.ransac_estimate_csr(off, az, dop, p)
+            o = oracle.sequential_ransac(off, az, dop, _oracle_params(p))
+            np.testing.assert_array_equal(r.mask, o.mask)
+            np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
+            np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
+            oe = oracle.estimate_all(off, az, dop, o.mask)
+            assert_estimates_close(est, oe, label=f"T={T} scale={scale}")
 
 
 def test_errors_and_reference_shaped_api(gpu_lib, oracle):

@@ -81,6 +81,20 @@ def test_live_against_reference_random(oracle, reference):
         np.testing.assert_array_equal(a.inlier_count, b.inlier_count)
 
 
+def test_live_against_reference_extreme_values(oracle, reference):
+    import paper_2012_12618_b200 as rvk
+    from conftest import EXTREME_PARAMS, extreme_value_clusters
+    for cl in extreme_value_clusters():
+        off, az, dop = rvk.clusters_to_csr(cl)
+        for T, scale in EXTREME_PARAMS:
+            p = make_params(T, scale, 5)
+            a = oracle.sequential_ransac(off, az, dop, p)
+            b = reference.run_ransac(off, az, dop, p, workers=2)
+            np.testing.assert_array_equal(a.mask, b.mask)
+            np.testing.assert_array_equal(a.winning_trial, b.winning_trial)
+            np.testing.assert_array_equal(a.inlier_count, b.inlier_count)
+
+
 # ---- the reference's own known-answer tests, restated ----
 
 def test_kat_mad_one_third(oracle):
