@@ -238,7 +238,7 @@ FrameDev stage_frame(Context& ctx, int64_t frame_id, int32_t n_clusters, const i
 
 Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   Scratch s;
-  const ScoreGeom g = score_geom(std::max(T, 1));
+  ScoreGeom g = score_geom(std::max(T, 1));
   const size_t C = static_cast<size_t>(n_clusters);
   s.xy64 = w.xy64.get<double2>(P);
   s.xy32 = w.xy32.get<float2>(P + 2 * C + 10);
@@ -254,6 +254,8 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
     s.tc_count = w.tc_count.get<int32_t>(kTcBuckets + 1);
   } else {
     s.hyp = w.hyp.get<float>(C * g.Tg * 32);
+    s.ppt = score_ppt(g, P, n_clusters);
+    set_ppt(g, s.ppt);
     s.tile_cap = tile_capacity(g, P, n_clusters);
     s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
     s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);

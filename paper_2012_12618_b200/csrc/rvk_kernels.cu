@@ -390,9 +390,15 @@ __device__ double first_zero(double v, const double* __restrict__ a, int n, doub
   return a[first];
 }
 
-// Size bucket of a partial tile of `rem` points (1 <= rem < kScorePPT):
-// larger tiles get lower buckets, bucket 0 holds the full tiles.
-__device__ __forceinline__ int tile_bucket(int rem) {
+// Size bucket of a partial tile of `rem` points (1 <= rem < ppt): larger
+// tiles get lower buckets, bucket 0 holds the full tiles.
+__device__ __forceinline__ int tile_bucket(int rem, const ScoreGeom& g) {
+  return 1 + (((g.ppt - 1 - rem) * (kTileBuckets - 1)) >> g.ppt_shift);
+}
+// The same for full-size (kScorePPT) units, as the warp-per-cluster prep
+// registers them whatever the call's ppt (its clusters are small and many;
+// tile_capacity() at any ppt <= kScorePPT bounds that count).
+__device__ __forceinline__ int tile_bucket_full(int rem) {
   return 1 + (kScorePPT - 1 - rem) / (kScorePPT / (kTileBuckets - 1));
 }
 
@@ -644,7 +650,7 @@ __device__ __forceinline__ float tc_store_hyp(float* tile, int row, double x1, d
 // coefficients and corridor bound, stored per group of 8 trials as
 // A[8] B[8] C[8] K[8] (K = -t2hi for the squared compare). Trials beyond T
 // in the last group are inert. The cluster's upper-bound counters are zeroed
-// and its scoring tiles (kScorePPT points x TS groups each) are appended to
+// and its scoring tiles (g.ppt <= kScorePPT points x TS groups each) are appended to
 // the size bucket they belong to, so the scoring kernel takes them
 // largest-first.
 __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
@@ -719,23 +725,23 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
     uc[t] = 0;
   }
   // scoring tiles of this cluster
-  const int full = n / kScorePPT, rem = n % kScorePPT;
+  const int full = n >> g.ppt_shift, rem = n & (g.ppt - 1);
   if (threadIdx.x == 0) {
     tile_pos[0] = full ? atomicAdd(&tile_count[0], full * g.nhb) : 0;
-    tile_pos[1] = rem ? atomicAdd(&tile_count[tile_bucket(rem)], g.nhb) : 0;
+    tile_pos[1] = rem ? atomicAdd(&tile_count[tile_bucket(rem, g)], g.nhb) : 0;
   }
   __syncthreads();
   const int64_t base32 = xy32_base(offsets, c);
   for (int i = threadIdx.x; i < full * g.nhb; i += blockDim.x) {
     const int pb = i / g.nhb, hb = i - pb * g.nhb;
     tiles[tile_pos[0] + i] =
-        make_int4(c, static_cast<int>(base32 + pb * kScorePPT), kScorePPT, hb * g.TS);
+        make_int4(c, static_cast<int>(base32 + pb * g.ppt), g.ppt, hb * g.TS);
   }
   if (rem) {
-    const int bk = tile_bucket(rem);
+    const int bk = tile_bucket(rem, g);
     for (int hb = threadIdx.x; hb < g.nhb; hb += blockDim.x)
       tiles[bk * tile_cap + tile_pos[1] + hb] =
-          make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
+          make_int4(c, static_cast<int>(base32 + full * g.ppt), rem, hb * g.TS);
   }
 }
 
@@ -1064,7 +1070,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   int pos0 = 0, pos1 = 0;
   if (lane == 0) {
     pos0 = full ? atomicAdd(&tile_count[0], full * g.nhb) : 0;
-    pos1 = rem ? atomicAdd(&tile_count[tile_bucket(rem)], g.nhb) : 0;
+    pos1 = rem ? atomicAdd(&tile_count[tile_bucket_full(rem)], g.nhb) : 0;
   }
   pos0 = __shfl_sync(0xffffffffu, pos0, 0);
   pos1 = __shfl_sync(0xffffffffu, pos1, 0);
@@ -1074,7 +1080,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     tiles[pos0 + i] = make_int4(c, static_cast<int>(base32 + pb * kScorePPT), kScorePPT, hb * g.TS);
   }
   if (rem) {
-    const int bk = tile_bucket(rem);
+    const int bk = tile_bucket_full(rem);
     for (int hb = lane; hb < g.nhb; hb += 32)
       tiles[bk * tile_cap + pos1 + hb] =
           make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
@@ -2305,7 +2311,8 @@ bool score_uses_tc() {
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  const ScoreGeom g = score_geom(p.max_trials);
+  ScoreGeom g = score_geom(p.max_trials);
+  set_ppt(g, s.ppt);
   TcOut tc;
   if (s.tc) {
     tc.hyp = s.tc_hyp;
@@ -2363,7 +2370,7 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
 
 namespace {
 // Persistent grid: every SM filled to the scoring kernel's occupancy.
-int score_grid(int64_t max_units) {
+int score_resident_ctas() {
   static int grid = 0;
   if (grid == 0) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -2377,11 +2384,29 @@ int score_grid(int64_t max_units) {
     per_sm = std::max(1, std::min(per_sm, env_int("RVK_SCORE_CTAS", per_sm)));
     grid = sms * per_sm;
   }
+  return grid;
+}
+int score_grid(int64_t max_units) {
+  const int grid = score_resident_ctas();
   const int64_t warps_per_cta = kScoreThreads / 32;
   return static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + warps_per_cta - 1) / warps_per_cta)));
 }
 }  // namespace
+
+int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
+  static const int forced = env_int("RVK_SCORE_PPT", 0);
+  if (forced > 0) {  // a power of two in [16, kScorePPT]
+    int ppt = 16;
+    while (ppt < forced && ppt < kScorePPT) ppt <<= 1;
+    return ppt;
+  }
+  const int64_t warps = static_cast<int64_t>(score_resident_ctas()) * (kScoreThreads / 32);
+  int ppt = kScorePPT;
+  while (ppt > 64 && static_cast<int64_t>(g.nhb) * (n_points / ppt + n_clusters) < warps)
+    ppt >>= 1;
+  return ppt;
+}
 
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
@@ -2406,8 +2431,9 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
     count_launch();
     return;
   }
-  const ScoreGeom g = score_geom(p.max_trials);
-  const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / kScorePPT + f.n_clusters);
+  ScoreGeom g = score_geom(p.max_trials);
+  set_ppt(g, s.ppt);
+  const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / g.ppt + f.n_clusters);
   if (score_uses_bulk())
     score_kernel<true><<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
         s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);

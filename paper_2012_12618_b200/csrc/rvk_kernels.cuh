@@ -31,13 +31,22 @@ constexpr int kScoreThreads = 256;
 constexpr int kUnitGroups = 32;                   // groups of 8 hypotheses per unit (one per lane)
 constexpr int kScorePPT = 512;                    // points per scoring unit (max)
 constexpr int kTileBuckets = kScorePPT / 4 + 1;   // 0: full units; 1..128: by size, descending
+static_assert(kScorePPT == 512, "ScoreGeom::ppt_shift default");
 
 struct ScoreGeom {
   int T = 0;    // max_trials
   int Tg = 0;   // hypothesis groups of 8 per cluster
   int TS = 0;   // groups per unit (kUnitGroups)
   int nhb = 0;  // hypothesis blocks per cluster = ceil(Tg / TS)
+  int ppt = kScorePPT;  // points per unit of this call: a power of two <= kScorePPT (score_ppt())
+  int ppt_shift = 9;    // log2(ppt)
 };
+
+inline void set_ppt(ScoreGeom& g, int ppt) {
+  g.ppt = ppt;
+  g.ppt_shift = 0;
+  while ((1 << g.ppt_shift) < ppt) ++g.ppt_shift;
+}
 
 inline __host__ __device__ ScoreGeom score_geom(int T) {
   ScoreGeom g;
@@ -50,8 +59,14 @@ inline __host__ __device__ ScoreGeom score_geom(int T) {
 
 // Capacity of one tile bucket: bounds the total tile count of a frame.
 inline int64_t tile_capacity(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
-  return static_cast<int64_t>(g.nhb) * (n_points / kScorePPT + n_clusters) + 1;
+  return static_cast<int64_t>(g.nhb) * (n_points / g.ppt + n_clusters) + 1;
 }
+
+// Points per scoring unit for a call: kScorePPT when the call has enough
+// units to give every resident scoring warp one, else the largest of 256 /
+// 128 / 64 that does (a single small frame: more, shorter units -> lower
+// latency). RVK_SCORE_PPT overrides (tests).
+int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters);
 
 // Tensor-core scoring (score_tc_kernel): D[h][p] = A_h x_p + B_h y_p + C_h
 // for a block of kTcM hypotheses x up to kTcN points is ONE tcgen05.mma
@@ -84,6 +99,7 @@ struct Scratch {
   int32_t* big_list = nullptr;    // [C] clusters too large for the warp-per-cluster prep
   int32_t* big_ctl = nullptr;     // [2] big_list count + claim counter (zeroed per call)
   int64_t tile_cap = 0;
+  int ppt = kScorePPT;            // points per scoring unit of this call (score_ppt)
   // tensor-core scoring
   float* tc_hyp = nullptr;     // [C][tc_blocks(T)][kTcHypFloats]: K-major operand tile
                                // (4 KB) + squared corridor bound per hypothesis
