@@ -227,7 +227,8 @@ __device__ __forceinline__ int med_bin(unsigned long long key, int nb) {
 }
 
 // Dynamic shared memory of the prep kernels, sized per launch from the
-// sort capacity (prep_dyn_bytes): [keys: cap][cand: candcap][hist: histcap].
+// sort capacity (prep_dyn_bytes): [keys: cap][cand: candcap][hist: histcap]
+// [xs: cap].
 // Addressed from the extern symbol (not through stored pointers) so every
 // access compiles to LDS/STS rather than generic loads.
 extern __shared__ __align__(16) unsigned char prep_dyn[];
@@ -243,6 +244,9 @@ struct PrepShared {
   __device__ unsigned int* hist() const {
     return reinterpret_cast<unsigned int*>(keys() + cap + candcap);
   }
+  // [cap] normalized azimuths (the hypotheses' seed points come from here and
+  // from keys(), not from global memory)
+  __device__ double* xs() const { return reinterpret_cast<double*>(hist() + histcap); }
   int cap;                   // clusters up to this size are kept in shared memory
   int candcap;
   int histcap;               // 2048: 11-bit radix digits, else 8-bit
@@ -263,7 +267,7 @@ __host__ __device__ inline int prep_histcap(int cap) {
 __host__ __device__ inline int prep_candcap(int cap) { return cap < kCandCap ? cap : kCandCap; }
 __host__ __device__ inline size_t prep_dyn_bytes(int cap) {
   return static_cast<size_t>(cap) * 8 + static_cast<size_t>(prep_candcap(cap)) * 8 +
-         static_cast<size_t>(prep_histcap(cap)) * 4;
+         static_cast<size_t>(prep_histcap(cap)) * 4 + static_cast<size_t>(cap) * 8;
 }
 __device__ void prep_smem_setup(PrepShared& sm, int cap) {
   if (threadIdx.x == 0) {
@@ -514,6 +518,7 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
       const unsigned long long key =
           static_cast<unsigned long long>(__double_as_longlong(y)) & ~(1ull << 63);
       sm.keys()[k] = key;
+      sm.xs()[k] = x;
       atomicAdd(&sm.hist()[med_bin(key, nb)], 1u);
     }
   }
@@ -708,14 +713,23 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
     return;
   }
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
+  const bool seeds_in_smem = n <= sm.cap;
   // hyp == nullptr: hyp_kernel builds the hypotheses and zeroes the counters
   for (int t = threadIdx.x; hyp != nullptr && t < g.Tg * 8; t += blockDim.x) {
     FastHyp f = inert_fast();
     if (t < g.T) {
       int i, j;
       seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-      const double2 p = p64[i], q = p64[j];  // written by this CTA before the barrier
-      f = make_fast_from_seeds(p.x, p.y, q.x, q.y, thr_lo, thr_hi);
+      if (seeds_in_smem) {  // |y| (keys): a -0.0 seed is +0.0 here, same FP32 line
+        const double* xs = sm.xs();
+        const unsigned long long* ks = sm.keys();
+        f = make_fast_from_seeds(xs[i], __longlong_as_double(static_cast<long long>(ks[i])),
+                                 xs[j], __longlong_as_double(static_cast<long long>(ks[j])),
+                                 thr_lo, thr_hi);
+      } else {
+        const double2 p = p64[i], q = p64[j];  // written by this CTA before the barrier
+        f = make_fast_from_seeds(p.x, p.y, q.x, q.y, thr_lo, thr_hi);
+      }
     }
     float* h = hc + (t >> 3) * 32 + (t & 7);
     h[0] = f.A;
