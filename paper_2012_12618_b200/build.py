@@ -49,8 +49,10 @@ def build_gpu(force=False):
         [os.path.join(INCLUDE, "rvk_gpu.h")]
     out = os.path.join(LIB, "librvk_gpu.so")
     if force or _stale(out, deps):
+        # RVK_NVCC_FLAGS: extra -D switches for A/B builds of kernel variants
+        extra = os.environ.get("RVK_NVCC_FLAGS", "").split()
         _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-              "-I", INCLUDE, "-o", out, *srcs])
+              *extra, "-I", INCLUDE, "-o", out, *srcs])
     return out
 
 
