@@ -19,7 +19,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --cs
     --streams 1 --e2e-steps 2 > $O/ncu_launch_bench.log 2>&1
 for c in 2 3 4; do
   timeout 900 ncu --set full --clock-control none --import-source on \
-      -k regex:"score_kernel|prep_hyp|prep_warp|select_kernel" -s 6 -c 4 \
+      -k regex:"score_kernel|prep_hyp|prep_warp|select_kernel|select_warp" -s 6 -c 4 \
       -o $O/prof_c$c python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline \
       --streams 1 --e2e-steps 1 --resident-frames 16 > $O/ncu_c$c.log 2>&1
 done
