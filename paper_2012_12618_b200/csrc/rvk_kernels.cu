@@ -2416,8 +2416,8 @@ int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
     return ppt;
   }
   const int64_t warps = static_cast<int64_t>(score_resident_ctas()) * (kScoreThreads / 32);
-  int ppt = kScorePPT;
-  while (ppt > 64 && static_cast<int64_t>(g.nhb) * (n_points / ppt + n_clusters) < warps)
+  int ppt = kScorePPT;  // at least two units per resident warp (measured, one frame of config 2)
+  while (ppt > 32 && static_cast<int64_t>(g.nhb) * (n_points / ppt + n_clusters) < 2 * warps)
     ppt >>= 1;
   return ppt;
 }

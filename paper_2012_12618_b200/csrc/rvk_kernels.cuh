@@ -63,9 +63,9 @@ inline int64_t tile_capacity(const ScoreGeom& g, int64_t n_points, int32_t n_clu
 }
 
 // Points per scoring unit for a call: kScorePPT when the call has enough
-// units to give every resident scoring warp one, else the largest of 256 /
-// 128 / 64 that does (a single small frame: more, shorter units -> lower
-// latency). RVK_SCORE_PPT overrides (tests).
+// units to give every resident scoring warp two, else the largest of 256 /
+// 128 / 64 / 32 that does (a single small frame: more, shorter units ->
+// better balance, lower latency). RVK_SCORE_PPT overrides (tests).
 int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters);
 
 // Tensor-core scoring (score_tc_kernel): D[h][p] = A_h x_p + B_h y_p + C_h
