@@ -27,6 +27,15 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
+// High 64 bits of z * n for a 32-bit n (== __umul64hi(z, n)) in two
+// IMAD.WIDE.U32: floor(z n / 2^64) = floor((zh n + floor(zl n / 2^32)) / 2^32),
+// and zh n + (zl n >> 32) < 2^64.
+__device__ __forceinline__ uint32_t mulhi_64x32(uint64_t z, uint32_t n) {
+  const uint64_t lo = static_cast<uint64_t>(static_cast<uint32_t>(z)) * n;
+  const uint64_t t = (z >> 32) * static_cast<uint64_t>(n) + (lo >> 32);
+  return static_cast<uint32_t>(t >> 32);
+}
+
 // draw_seed_pair (src/ransac.cpp:111-123): KeyedRng(seed, (u32)cluster,
 // (u32)trial); i = next_below(n); j = next_below(n-1), ++j if j >= i.
 // next_below is the high word of the 64x32 product (rng.hpp:34-38).
@@ -39,8 +48,8 @@ __device__ __forceinline__ void seed_pair(uint64_t seed, uint32_t cluster, uint3
   const uint64_t z1 = mix64(state);
   state += kGamma;
   const uint64_t z2 = mix64(state);
-  i = static_cast<int>(__umul64hi(z1, static_cast<uint64_t>(n)));
-  j = static_cast<int>(__umul64hi(z2, static_cast<uint64_t>(n - 1)));
+  i = static_cast<int>(mulhi_64x32(z1, n));
+  j = static_cast<int>(mulhi_64x32(z2, n - 1));
   if (j >= i) ++j;
 }
 
@@ -131,14 +140,25 @@ __device__ __forceinline__ FastHyp make_fast(const Line& L, double thr_lo, doubl
   return fast_coeffs(L.m, L.c, __ddiv_rn(1.0, L.den), thr_lo, thr_hi);
 }
 
-// Fast-pass hypothesis straight from the seeds: the exact FP64 slope and
-// intercept (same operations as make_line) but 1/den by rsqrt instead of a
-// correctly rounded sqrt + divide; used where only the FP32 filter is needed.
+// 1/d to ~1 FP64 ulp: the MUFU seed and two Newton steps (no IEEE divide).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+
+// Fast-pass hypothesis straight from the seeds: the same line as make_line
+// (degeneracy decided on the exact dx), but the slope by a refined
+// reciprocal and 1/den by rsqrt instead of correctly rounded divides and sqrt
+// -- a few FP64 ulps, far inside the guard band (see fast_coeffs); used where
+// only the FP32 filter is needed. |dx| >= kSeedEpsilon keeps the
+// reciprocal clear of the flush-to-zero range.
 __device__ __forceinline__ FastHyp make_fast_from_seeds(double x1, double y1, double x2,
                                                         double y2, double thr_lo, double thr_hi) {
   const double dx = __dsub_rn(x2, x1);
   if (fabs(dx) < kSeedEpsilon) return inert_fast();
-  const double m = __ddiv_rn(__dsub_rn(y2, y1), dx);
+  const double m = __dsub_rn(y2, y1) * fast_rcp(dx);
   const double c = __dsub_rn(y1, __dmul_rn(m, x1));
   return fast_coeffs(m, c, rsqrt(__dadd_rn(__dmul_rn(m, m), 1.0)), thr_lo, thr_hi);
 }
