@@ -193,6 +193,40 @@ def test_batch_composition_invariance(gpu_lib):
             np.testing.assert_array_equal(e[f], est[f][lo:hi])
 
 
+def test_concurrent_host_threads(gpu_lib):
+    """The reference's run_ransac may be called from several host threads;
+    the C-ABI keeps one context (stream, workspace) per thread: concurrent
+    calls on different frames give the sequential results byte for byte."""
+    import threading
+    frames = [W.automotive(seed=500 + i, n_clusters=60) for i in range(8)]
+    p = rvk.RansacParams(512, 1.0, 99)
+    want = [rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p) for w in frames]
+    got = [None] * len(frames)
+    errors = []
+
+    def work(k):
+        try:
+            for i in range(k, len(frames), 4):
+                w = frames[i]
+                for _ in range(3):
+                    got[i] = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for (r0, e0), (r1, e1) in zip(want, got):
+        np.testing.assert_array_equal(r0.mask, r1.mask)
+        np.testing.assert_array_equal(r0.winning_trial, r1.winning_trial)
+        np.testing.assert_array_equal(r0.inlier_count, r1.inlier_count)
+        for f in ("v_x", "v_y", "heading"):
+            np.testing.assert_array_equal(e0[f], e1[f])
+
+
 def test_edge_cases(gpu_lib, oracle):
     rng = np.random.default_rng(11)
     cases = []
