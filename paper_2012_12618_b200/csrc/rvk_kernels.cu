@@ -761,8 +761,11 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
 
 // One CTA per cluster (big_list == nullptr), or persistent CTAs working
 // through the list of clusters the warp kernel left for them
-// (big_ctl[0] = count, big_ctl[1] = claim counter).
-__global__ void __launch_bounds__(kPrepThreads, 4)
+// (big_ctl[0] = count, big_ctl[1] = claim counter). 256-thread CTAs for
+// throughput, 512 for calls with few clusters (latency: the largest
+// cluster's chain is the call's critical path).
+template <int kMaxThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kMaxThreads, kMinBlocks)
 prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 const double* __restrict__ az, const double* __restrict__ dop, double scale,
                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
@@ -2265,8 +2268,18 @@ int env_int(const char* name, int dflt) {
 CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env, bool select) {
   const int64_t avg = n_clusters ? n_points / n_clusters : 0;
   int t = select ? (avg < 384 ? 64 : (avg < 1024 ? 128 : 256)) : (avg < 384 ? 128 : 256);
+  // a call with few clusters (one frame): twice the threads per cluster,
+  // the largest cluster's chain is the latency (measured, tools/frame_latency.py)
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  if (avg >= 384 && n_clusters <= 2 * sms) t = select ? 256 : 512;
   t = env_int(env, t);
-  t = t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : 256));
+  const int tmax = select ? 256 : 512;
+  t = t <= 32 ? 32 : (t <= 64 ? 64 : (t <= 128 ? 128 : (t <= 256 ? 256 : tmax)));
   int cap = std::max(512, t * 8);
   if (!select) cap = env_int("RVK_PREP_CAP", cap);
   // >= 512: prep_cluster's reduction scratch; multiple of 32: 16-byte
@@ -2278,7 +2291,7 @@ CtaShape cluster_cta_shape(int64_t n_points, int32_t n_clusters, const char* env
 void launch_prep(const FrameDev& f, double scale, const Scratch& s, cudaStream_t st) {
   if (f.n_clusters == 0) return;
   const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
-  prep_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
+  prep_kernel<<<f.n_clusters, std::min(sh.threads, kPrepThreads), prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, scale, s.xy64, s.xy32, s.stat, s.norm,
       sh.cap);
   count_launch();
@@ -2368,7 +2381,8 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       big_grid = 2 * sms;
     }
-    prep_hyp_kernel<<<std::min<int64_t>(big_grid, f.n_clusters), 256, prep_dyn_bytes(2048), st>>>(
+    prep_hyp_kernel<256, 4><<<std::min<int64_t>(big_grid, f.n_clusters), 256,
+                              prep_dyn_bytes(2048), st>>>(
         f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
         s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
         2048, s.big_list, s.big_ctl);
@@ -2376,7 +2390,8 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
     launch_hyps();
     return;
   }
-  prep_hyp_kernel<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
+  auto k = sh.threads > 256 ? prep_hyp_kernel<512, 2> : prep_hyp_kernel<256, 4>;
+  k<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
       s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
       sh.cap, nullptr, nullptr);

@@ -385,10 +385,11 @@ def est_dtype():
                                  {"RVK_HYP_KERNEL": "1", "RVK_PREP_WARP": "1"},
                                  {"RVK_SCORE_STAGE": "lanes"},
                                  {"RVK_SELECT_WARP": "1"}, {"RVK_SELECT_WARP": "0"},
-                                 {"RVK_SCORE_PPT": "64"}, {"RVK_SCORE_PPT": "512"}],
+                                 {"RVK_SCORE_PPT": "64"}, {"RVK_SCORE_PPT": "512"},
+                                 {"RVK_PREP_THREADS": "512", "RVK_PREP_WARP": "0"}],
                          ids=["tensor_core_scoring", "cta256", "cta64", "warp_prep", "cta_prep",
                               "hyp_kernel", "hyp_kernel_warp_prep", "cp_async_staging",
-                              "warp_select", "cta_select", "units_64", "units_512"])
+                              "warp_select", "cta_select", "units_64", "units_512", "cta512_prep"])
 def test_alternative_kernel_shapes_parity(gpu_lib, env):
     """Every kernel variant must give the same bytes: the tcgen05 scoring
     kernel (RVK_SCORE=tc), the per-cluster CTA shapes of prep/select, the
