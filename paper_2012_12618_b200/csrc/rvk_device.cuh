@@ -148,6 +148,28 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, fma(-d, r, 1.0), r);
 }
 
+// a / s rounded to nearest, bit-identical to __ddiv_rn(a, s), for a divisor
+// s shared by many dividends (normalize_cluster's spans) with r ~= 1/s
+// precomputed once: Markstein's correction step q1 = q0 + (a - s q0) r, then
+// a verification -- q1 is the correctly rounded quotient iff
+// |a - s q1| < ulp(q1)/2 * s (the residual is exact when q1 is within one ulp;
+// a quotient can never lie exactly on a midpoint) -- and __ddiv_rn for the
+// rare rest (zero or tiny quotients, failed checks). Requires
+// s in [2^-60, 2^60] (div_span_ok) so that the scaled half-ulp is normal.
+__device__ __forceinline__ bool div_span_ok(double s) {
+  return s >= 0x1p-60 && s <= 0x1p60;
+}
+__device__ __forceinline__ double div_rn_shared(double a, double s, double r) {
+  const double q0 = a * r;
+  const double q1 = fma(fma(-q0, s, a), r, q0);
+  const long long e = __double_as_longlong(q1) & 0x7ff0000000000000LL;  // biased exponent
+  if (e >= (0x3ffLL - 900) << 52) {                                     // |q1| >= 2^-900
+    const double half_ulp = __longlong_as_double(e - (53LL << 52));
+    if (fabs(fma(-q1, s, a)) < half_ulp * s) return q1;
+  }
+  return __ddiv_rn(a, s);
+}
+
 // Fast-pass hypothesis straight from the seeds: the same line as make_line
 // (degeneracy decided on the exact dx), but the slope by a refined
 // reciprocal and 1/den by rsqrt instead of correctly rounded divides and sqrt

@@ -506,6 +506,7 @@ __device__ void prep_cluster(PrepShared& sm, int c, const int64_t* __restrict__ 
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   float2* p32 = xy32 + xy32_base(offsets, c);
+  // (div_rn_shared, as in prep_warp_kernel, measured slower here: spills)
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
     const double x = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(az[b + k], lo0), s0);
     const double y = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(dop[b + k], lo1), s1);
@@ -1010,14 +1011,21 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   float2* p32 = xy32 + xy32_base(offsets, c);
+  // the spans are shared by the cluster: one reciprocal each, verified
+  // correctly rounded quotients (div_rn_shared == __ddiv_rn, bit for bit)
+  const bool f0 = div_span_ok(s0), f1 = div_span_ok(s1);
+  const double r0 = f0 ? fast_rcp(s0) : 0.0, r1 = f1 ? fast_rcp(s1) : 0.0;
+  auto norm_div = [](double a, double s, bool fast, double r) {
+    return fast ? div_rn_shared(a, s, r) : __ddiv_rn(a, s);
+  };
   for (int k0 = lane; k0 < n; k0 += 64) {  // two points per lane and step
     const int k1 = k0 + 32;
     const double a0 = az[b + k0], d0 = dop[b + k0];
     const double a1 = k1 < n ? az[b + k1] : 0.0, d1 = k1 < n ? dop[b + k1] : 0.0;
-    const double x0 = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(a0, lo0), s0);
-    const double y0 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d0, lo1), s1);
-    const double x1 = s0 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(a1, lo0), s0);
-    const double y1 = s1 == 0.0 ? 0.5 : __ddiv_rn(__dsub_rn(d1, lo1), s1);
+    const double x0 = s0 == 0.0 ? 0.5 : norm_div(__dsub_rn(a0, lo0), s0, f0, r0);
+    const double y0 = s1 == 0.0 ? 0.5 : norm_div(__dsub_rn(d0, lo1), s1, f1, r1);
+    const double x1 = s0 == 0.0 ? 0.5 : norm_div(__dsub_rn(a1, lo0), s0, f0, r0);
+    const double y1 = s1 == 0.0 ? 0.5 : norm_div(__dsub_rn(d1, lo1), s1, f1, r1);
     xy64[b + k0] = make_double2(x0, y0);
     xy32_put(p32, k0, __double2float_rn(x0), __double2float_rn(y0));
     const unsigned long long key0 =
