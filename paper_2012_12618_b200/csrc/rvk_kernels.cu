@@ -1716,77 +1716,52 @@ __device__ int warp_exact_count(const ExactHyp& H, int n, const float2* __restri
 // (RefitAcc::add); one fused block reduction with a fixed tree follows, so
 // results are deterministic; they differ from Eigen's reduction order only
 // in the last bits (tolerance-checked).
+// Canonical order (every kernel, every launch shape): lane l of ONE warp
+// sums the inliers k == l (mod 32) in increasing k with the explicit FMAs of
+// add_cs, then warp_reduce_refit's butterfly combines the 32 lanes -- so the
+// velocities are bit-identical whatever CTA shape or batch a cluster is in.
 struct RefitAcc {
   double g00 = 0, g01 = 0, g11 = 0, b0 = 0, b1 = 0, ds = 0;
   int nin = 0, first = INT_MAX;
-  __device__ __forceinline__ void add(int k, double a, double d) {
-    double s, c;
-    sincos(a, &s, &c);
-    g00 += c * c;
-    g01 += c * s;
-    g11 += s * s;
-    b0 += c * d;
-    b1 += s * d;
-    ds += d;
+  __device__ __forceinline__ void add_cs(int k, double c, double s, double d) {
+    g00 = fma(c, c, g00);
+    g01 = fma(c, s, g01);
+    g11 = fma(s, s, g11);
+    b0 = fma(c, d, b0);
+    b1 = fma(s, d, b1);
+    ds = __dadd_rn(ds, d);
     ++nin;
     first = k < first ? k : first;
   }
+  __device__ __forceinline__ void add(int k, double a, double d) {
+    double s, c;
+    sincos(a, &s, &c);
+    add_cs(k, c, s, d);
+  }
 };
 
-struct RefitShared {
-  double v[kSelectThreads / 32][6];
-  int i[kSelectThreads / 32][2];
-};
-
-// Block-wide sum of the accumulators; the total is valid in thread 0.
-__device__ RefitAcc block_reduce_refit(RefitAcc a, RefitShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ RefitAcc warp_reduce_refit(RefitAcc a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    a.g00 += __shfl_xor_sync(0xffffffffu, a.g00, o);
-    a.g01 += __shfl_xor_sync(0xffffffffu, a.g01, o);
-    a.g11 += __shfl_xor_sync(0xffffffffu, a.g11, o);
-    a.b0 += __shfl_xor_sync(0xffffffffu, a.b0, o);
-    a.b1 += __shfl_xor_sync(0xffffffffu, a.b1, o);
-    a.ds += __shfl_xor_sync(0xffffffffu, a.ds, o);
+    a.g00 = __dadd_rn(a.g00, __shfl_xor_sync(0xffffffffu, a.g00, o));
+    a.g01 = __dadd_rn(a.g01, __shfl_xor_sync(0xffffffffu, a.g01, o));
+    a.g11 = __dadd_rn(a.g11, __shfl_xor_sync(0xffffffffu, a.g11, o));
+    a.b0 = __dadd_rn(a.b0, __shfl_xor_sync(0xffffffffu, a.b0, o));
+    a.b1 = __dadd_rn(a.b1, __shfl_xor_sync(0xffffffffu, a.b1, o));
+    a.ds = __dadd_rn(a.ds, __shfl_xor_sync(0xffffffffu, a.ds, o));
     a.nin += __shfl_xor_sync(0xffffffffu, a.nin, o);
     a.first = min(a.first, __shfl_xor_sync(0xffffffffu, a.first, o));
   }
-  __syncthreads();  // sh may still be read by a previous reduction
-  if (lane == 0) {
-    sh.v[warp][0] = a.g00;
-    sh.v[warp][1] = a.g01;
-    sh.v[warp][2] = a.g11;
-    sh.v[warp][3] = a.b0;
-    sh.v[warp][4] = a.b1;
-    sh.v[warp][5] = a.ds;
-    sh.i[warp][0] = a.nin;
-    sh.i[warp][1] = a.first;
-  }
-  __syncthreads();
-  RefitAcc t;
-  if (threadIdx.x == 0) {
-    t.g00 = sh.v[0][0];
-    t.g01 = sh.v[0][1];
-    t.g11 = sh.v[0][2];
-    t.b0 = sh.v[0][3];
-    t.b1 = sh.v[0][4];
-    t.ds = sh.v[0][5];
-    t.nin = sh.i[0][0];
-    t.first = sh.i[0][1];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      t.g00 += sh.v[w][0];
-      t.g01 += sh.v[w][1];
-      t.g11 += sh.v[w][2];
-      t.b0 += sh.v[w][3];
-      t.b1 += sh.v[w][4];
-      t.ds += sh.v[w][5];
-      t.nin += sh.i[w][0];
-      t.first = min(t.first, sh.i[w][1]);
-    }
-  }
-  return t;
+  return a;
 }
+
+// Staging for the canonical order in CTA kernels: all threads compute the
+// (cos, sin, doppler) of the inliers of a chunk, warp 0 accumulates it.
+constexpr int kRefitChunk = 1024;
+struct RefitStage {
+  double c[kRefitChunk], s[kRefitChunk], d[kRefitChunk];
+  uint8_t in[kRefitChunk];
+};
 
 // Thread 0: the 2x2 solve, fallback and heading from the reduced sums.
 __device__ void finish_refit(const RefitAcc& a, const double* __restrict__ az,
@@ -1860,15 +1835,38 @@ __device__ void finish_refit(const RefitAcc& a, const double* __restrict__ az,
   *out = e;
 }
 
-// estimate_cluster_velocity on a mask in memory.
+// estimate_cluster_velocity on a mask in memory, in the canonical order
+// (RefitAcc): all threads stage the inliers' (cos, sin, doppler) chunk by
+// chunk, warp 0 accumulates, lane 0 solves.
 __device__ void block_refit(int n, const double* __restrict__ az, const double* __restrict__ dop,
                             const uint8_t* mask, int64_t frame_id, int cluster_id,
-                            rvk_estimate* __restrict__ out, RefitShared& sh) {
+                            rvk_estimate* __restrict__ out, RefitStage& st) {
   RefitAcc acc;
-  for (int k = threadIdx.x; k < n; k += blockDim.x)
-    if (mask[k]) acc.add(k, az[k], dop[k]);
-  const RefitAcc t = block_reduce_refit(acc, sh);
-  if (threadIdx.x == 0) finish_refit(t, az, dop, frame_id, cluster_id, out);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int kb = 0; kb < n; kb += kRefitChunk) {
+    const int kn = min(kRefitChunk, n - kb);
+    for (int i = threadIdx.x; i < kn; i += blockDim.x) {
+      const int k = kb + i;
+      const bool in = mask[k] != 0;
+      st.in[i] = in;
+      if (in) {
+        double sn, cs;
+        sincos(az[k], &sn, &cs);
+        st.c[i] = cs;
+        st.s[i] = sn;
+        st.d[i] = dop[k];
+      }
+    }
+    __syncthreads();
+    if (warp == 0)
+      for (int i = lane; i < kn; i += 32)
+        if (st.in[i]) acc.add_cs(kb + i, st.c[i], st.s[i], st.d[i]);
+    __syncthreads();
+  }
+  if (warp == 0) {
+    const RefitAcc t = warp_reduce_refit(acc);
+    if (lane == 0) finish_refit(t, az, dop, frame_id, cluster_id, out);
+  }
 }
 
 // Exact winner per cluster (one CTA). With U = the fast pass's upper bounds
@@ -1890,7 +1888,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
               int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
               rvk_estimate* __restrict__ est) {
   __shared__ unsigned long long redu[32];
-  __shared__ RefitShared rsh;
+  __shared__ RefitStage rst;
   __shared__ unsigned long long best;
   __shared__ double sh_thr;
   __shared__ int sh_need_exact;
@@ -1920,45 +1918,61 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   // switches to the exact threshold).
   auto pass = [&](int t, int& count, RefitAcc& total) -> bool {
     const ExactHyp H = make_exact(p64, seed, key, static_cast<uint32_t>(t), n, thr_lo, thr_hi);
-    RefitAcc acc;
+    RefitAcc acc;  // warp 0 (canonical order, see RefitAcc)
     bool und = false;
+    int cnt = 0;
     const int nt = blockDim.x;
-    // two points per thread and step, every load issued before the first
-    // use (the loop is latency-bound: few points per thread, one CTA per
-    // cluster; four deep costs more in spills than it hides, measured)
-    for (int k0 = threadIdx.x; k0 < n; k0 += 2 * nt) {
-      float2 pp[2];
-      double pa[2], pd[2];
+    for (int kb = 0; kb < n; kb += kRefitChunk) {
+      const int ke = min(n, kb + kRefitChunk);
+      // two points per thread and step, every load issued before the first
+      // use (the loop is latency-bound: few points per thread, one CTA per
+      // cluster; four deep costs more in spills than it hides, measured)
+      for (int k0 = kb + threadIdx.x; k0 < ke; k0 += 2 * nt) {
+        float2 pp[2];
+        double pa[2], pd[2];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = k0 + u * nt;
-        if (k < n) {
-          pp[u] = xy32_get(p32, k);
+        for (int u = 0; u < 2; ++u) {
+          const int k = k0 + u * nt;
+          if (k < ke) {
+            pp[u] = xy32_get(p32, k);
+            if (refit) {
+              pa[u] = caz[k];
+              pd[u] = cdop[k];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = k0 + u * nt;
+          if (k >= ke) break;
+          const int d = H.L.degenerate ? kOut : classify(H, k, pp[u], p64, thr_lo, thr_hi);
+          und |= d == kUndecided;
+          const bool in = d == kIn;
+          cmask[k] = in ? 1 : 0;
+          cnt += in;
           if (refit) {
-            pa[u] = caz[k];
-            pd[u] = cdop[k];
+            rst.in[k - kb] = in;
+            if (in) {
+              double sn, cs;
+              sincos(pa[u], &sn, &cs);
+              rst.c[k - kb] = cs;
+              rst.s[k - kb] = sn;
+              rst.d[k - kb] = pd[u];
+            }
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = k0 + u * nt;
-        if (k >= n) break;
-        const int d = H.L.degenerate ? kOut : classify(H, k, pp[u], p64, thr_lo, thr_hi);
-        und |= d == kUndecided;
-        cmask[k] = d == kIn ? 1 : 0;
-        if (d == kIn) {
-          if (refit) acc.add(k, pa[u], pd[u]);
-          else ++acc.nin;
-        }
+      if (refit) {
+        __syncthreads();
+        if (warp == 0)
+          for (int i = lane; i < ke - kb; i += 32)
+            if (rst.in[i]) acc.add_cs(kb + i, rst.c[i], rst.s[i], rst.d[i]);
+        __syncthreads();
       }
     }
     if (__syncthreads_or(und)) return false;
-    total = block_reduce_refit(acc, rsh);
-    if (threadIdx.x == 0) redu[0] = static_cast<unsigned long long>(total.nin);
-    __syncthreads();
-    count = static_cast<int>(redu[0]);
-    __syncthreads();
+    count = block_reduce(cnt, SumI(), reinterpret_cast<int*>(redu));
+    if (refit && warp == 0) total = warp_reduce_refit(acc);  // thread 0 solves
     return true;
   };
 
@@ -2049,20 +2063,7 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
 // with a ballot over the upper bounds.
 constexpr int kSelectWarps = 4;
 
-__device__ __forceinline__ RefitAcc warp_reduce_refit(RefitAcc a) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a.g00 += __shfl_xor_sync(0xffffffffu, a.g00, o);
-    a.g01 += __shfl_xor_sync(0xffffffffu, a.g01, o);
-    a.g11 += __shfl_xor_sync(0xffffffffu, a.g11, o);
-    a.b0 += __shfl_xor_sync(0xffffffffu, a.b0, o);
-    a.b1 += __shfl_xor_sync(0xffffffffu, a.b1, o);
-    a.ds += __shfl_xor_sync(0xffffffffu, a.ds, o);
-    a.nin += __shfl_xor_sync(0xffffffffu, a.nin, o);
-    a.first = min(a.first, __shfl_xor_sync(0xffffffffu, a.first, o));
-  }
-  return a;
-}
+
 
 // 5 CTAs per SM (<= 96 registers, a few spills): config 4 select 0.305 ->
 // 0.260 ms against the unbounded 123-register build (4 CTAs); 6 (80
@@ -2213,12 +2214,12 @@ __global__ void __launch_bounds__(kSelectThreads)
 refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
              const double* __restrict__ dop, const int32_t* __restrict__ cluster_ids,
              int64_t frame_id, const uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
-  __shared__ RefitShared rsh;
+  __shared__ RefitStage rst;
   const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   block_refit(n, az + b, dop + b, mask + b, frame_id, cluster_ids ? cluster_ids[c] : c, est + c,
-              rsh);
+              rst);
 }
 
 // Exact count of every (cluster, trial) (warp per trial). Requires the exact
