@@ -1738,6 +1738,19 @@ struct RefitAcc {
     sincos(a, &s, &c);
     add_cs(k, c, s, d);
   }
+  // add_cs for a staged point whose (c, s, d) are zeros unless it is an
+  // inlier: the sums never hold -0.0, so x + 0 == x and the result equals
+  // add_cs on the inliers alone -- branch-free, so the loop can pipeline
+  __device__ __forceinline__ void add_staged(int k, double c, double s, double d, bool in) {
+    g00 = fma(c, c, g00);
+    g01 = fma(c, s, g01);
+    g11 = fma(s, s, g11);
+    b0 = fma(c, d, b0);
+    b1 = fma(s, d, b1);
+    ds = __dadd_rn(ds, d);
+    nin += in;
+    first = in && k < first ? k : first;
+  }
 };
 
 __device__ __forceinline__ RefitAcc warp_reduce_refit(RefitAcc a) {
@@ -1849,18 +1862,21 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
       const int k = kb + i;
       const bool in = mask[k] != 0;
       st.in[i] = in;
+      double sn = 0.0, cs = 0.0, dd = 0.0;
       if (in) {
-        double sn, cs;
         sincos(az[k], &sn, &cs);
-        st.c[i] = cs;
-        st.s[i] = sn;
-        st.d[i] = dop[k];
+        dd = dop[k];
       }
+      st.c[i] = cs;
+      st.s[i] = sn;
+      st.d[i] = dd;
     }
     __syncthreads();
-    if (warp == 0)
+    if (warp == 0) {
+#pragma unroll 4
       for (int i = lane; i < kn; i += 32)
-        if (st.in[i]) acc.add_cs(kb + i, st.c[i], st.s[i], st.d[i]);
+        acc.add_staged(kb + i, st.c[i], st.s[i], st.d[i], st.in[i] != 0);
+    }
     __syncthreads();
   }
   if (warp == 0) {
@@ -1952,21 +1968,21 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
           cnt += in;
           if (refit) {
             rst.in[k - kb] = in;
-            if (in) {
-              double sn, cs;
-              sincos(pa[u], &sn, &cs);
-              rst.c[k - kb] = cs;
-              rst.s[k - kb] = sn;
-              rst.d[k - kb] = pd[u];
-            }
+            double sn = 0.0, cs = 0.0;
+            if (in) sincos(pa[u], &sn, &cs);
+            rst.c[k - kb] = cs;
+            rst.s[k - kb] = sn;
+            rst.d[k - kb] = in ? pd[u] : 0.0;
           }
         }
       }
       if (refit) {
         __syncthreads();
-        if (warp == 0)
+        if (warp == 0) {
+#pragma unroll 4
           for (int i = lane; i < ke - kb; i += 32)
-            if (rst.in[i]) acc.add_cs(kb + i, rst.c[i], rst.s[i], rst.d[i]);
+            acc.add_staged(kb + i, rst.c[i], rst.s[i], rst.d[i], rst.in[i] != 0);
+        }
         __syncthreads();
       }
     }
