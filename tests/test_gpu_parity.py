@@ -294,6 +294,17 @@ def test_launch_shapes_bit_identical(gpu_lib):
     assert len(set(digests.values())) == 1, digests
 
 
+def test_randomised_sweep(gpu_lib):
+    """A short run of tools/fuzz_parity.py (random clustered / uniform /
+    quantised / tiny-spread / near-degenerate frames, random T, scale and
+    seed): masks, trials, counts bit-exact, estimates within tolerance."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_parity.py"),
+                        "--frames", "400", "--seed", "21"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert '"mismatches": 0' in r.stdout
+
+
 def test_edge_cases(gpu_lib, oracle):
     rng = np.random.default_rng(11)
     cases = []
