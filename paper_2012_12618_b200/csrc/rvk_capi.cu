@@ -72,6 +72,11 @@ struct DevBuf {
     }
     return static_cast<T*>(p);
   }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
 };
 
 // Grow-only pinned host buffer (staging for H2D/D2H).
@@ -89,12 +94,21 @@ struct HostBuf {
     }
     return p;
   }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
 };
 
 // Device scratch of one stream's in-flight pipeline.
 struct Workspace {
   DevBuf xy64, xy32, thr, norm, upper, hyp, tiles, tile_count, aux;
-  DevBuf tc_hyp, tc_pts, tc_items, tc_count, big;
+  DevBuf big;
+  void release() {
+    for (DevBuf* b : {&xy64, &xy32, &thr, &norm, &upper, &hyp, &tiles, &tile_count, &aux, &big})
+      b->release();
+  }
 };
 
 struct Context {
@@ -168,6 +182,14 @@ int validate_offsets(int32_t n_clusters, const int64_t* offsets, int min_size, c
     }
   }
   return RVK_OK;
+}
+
+// Largest cluster of a host CSR (lets the pipeline skip the CTA path's
+// launches when the fused kernel takes every cluster).
+int64_t max_cluster_size(int32_t n_clusters, const int64_t* offsets) {
+  int64_t m = 0;
+  for (int32_t c = 0; c < n_clusters; ++c) m = std::max(m, offsets[c + 1] - offsets[c]);
+  return m;
 }
 
 // Largest clusters first, so the scoring grid's tail is short (LPT).
@@ -245,23 +267,14 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
   s.stat = w.thr.get<double4>(C);
   s.norm = w.norm.get<double>(4 * C);
   s.upper = w.upper.get<int32_t>(C * g.Tg * 8);
-  s.tc = score_uses_tc();
-  if (s.tc) {
-    const size_t nhb = static_cast<size_t>(tc_blocks(std::max(T, 1)));
-    s.tc_hyp = w.tc_hyp.get<float>(C * nhb * kTcHypFloats);
-    s.tc_pts = w.tc_pts.get<float>((static_cast<size_t>(P) + 32 * C + 32) * 8);
-    s.tc_items = w.tc_items.get<int4>(static_cast<size_t>(kTcBuckets) * C);
-    s.tc_count = w.tc_count.get<int32_t>(kTcBuckets + 1);
-  } else {
-    s.hyp = w.hyp.get<float>(C * g.Tg * 32);
-    s.ppt = score_ppt(g, P, n_clusters);
-    set_ppt(g, s.ppt);
-    s.tile_cap = tile_capacity(g, P, n_clusters);
-    s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
-    s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
-    s.big_ctl = w.big.get<int32_t>(C + 8);
-    s.big_list = s.big_ctl + 8;
-  }
+  s.hyp = w.hyp.get<float>(C * g.Tg * 32);
+  s.ppt = score_ppt(g, P, n_clusters);
+  set_ppt(g, s.ppt);
+  s.tile_cap = tile_capacity(g, P, n_clusters);
+  s.tiles = w.tiles.get<int4>(static_cast<size_t>(kTileBuckets) * s.tile_cap);
+  s.tile_count = w.tile_count.get<int32_t>(kTileBuckets + 1);
+  s.big_ctl = w.big.get<int32_t>(C + 8);
+  s.big_list = s.big_ctl + 8;
   return s;
 }
 
@@ -316,9 +329,12 @@ void stage(int id, cudaStream_t st, F&& launch) {
 
 // prep+hyps -> score -> select(+refit): the whole device pipeline of one call.
 // Stage ids (rvk_profile_read): 0 = prep + hypothesis setup + tile plan,
-// 2 = score, 3 = select + refit (1 is unused since the fusion of setup into prep).
+// 1 = the fused warp-per-cluster kernel (calls of small clusters), 2 = score,
+// 3 = select + refit. On the fused path stages 0/2/3 take only the clusters
+// the fused kernel listed (none when the host knows they all fit).
 void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   const Outputs& o, cudaStream_t st) {
+  if (fused_path(f, p)) stage(1, st, [&] { launch_fused(f, p, s, o, st); });
   stage(0, st, [&] { launch_prep_hyps(f, p, s, st); });
   stage(2, st, [&] { launch_score(f, p, s, st); });
   stage(3, st, [&] { launch_select(f, p, s, o, st); });
@@ -399,6 +415,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
 
   const bool pin_in = is_pinned(az) && is_pinned(dop);
   const bool pin_mask = is_pinned(mask);
+  const int64_t max_n = max_cluster_size(n_clusters, offsets);
   const auto t1 = clk::now();
 
   // device input block: [offsets (rebased per chunk) | keys | ids] + az | dop
@@ -468,6 +485,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
     f.keys = reinterpret_cast<const int32_t*>(d + o_keys) + c0;
     f.cluster_ids = reinterpret_cast<const int32_t*>(d + o_ids) + c0;
     f.frame_id = frame_id;
+    f.max_cluster = max_n;
     Scratch s = scratch(ctx.workspace(sc), nc, np, params->max_trials);
     Outputs o;
     o.inlier_count = reinterpret_cast<int32_t*>(dout + L.o_cnt) + c0;
@@ -654,6 +672,7 @@ struct FrameStream {
     f.keys = reinterpret_cast<const int32_t*>(d + o_keys);
     f.cluster_ids = reinterpret_cast<const int32_t*>(d + o_ids);
     f.frame_id = frame_id;
+    f.max_cluster = max_cluster_size(n_clusters, offsets);
     s.L = OutLayout(n_clusters, P);
     char* dout = s.out.get<char>(s.L.total);
     char* hout = static_cast<char*>(s.stage_out.get(s.L.total));
@@ -959,11 +978,8 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
     for (auto& sl : fs.slots) {
       if (sl.landed) cudaEventDestroy(sl.landed);
       if (sl.done) cudaEventDestroy(sl.done);
-      for (DevBuf* b : {&sl.in, &sl.out, &sl.ws.xy64, &sl.ws.xy32, &sl.ws.thr, &sl.ws.norm,
-                        &sl.ws.upper, &sl.ws.hyp, &sl.ws.tiles, &sl.ws.tile_count, &sl.ws.aux,
-                        &sl.ws.tc_hyp, &sl.ws.tc_pts, &sl.ws.tc_items, &sl.ws.big,
-                        &sl.ws.tc_count})
-        if (b->p) cudaFree(b->p);
+      sl.ws.release();
+      for (DevBuf* b : {&sl.in, &sl.out}) b->release();
       for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out})
         if (b->p) cudaFreeHost(b->p);
     }

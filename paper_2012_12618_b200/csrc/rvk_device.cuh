@@ -39,6 +39,24 @@ __device__ __forceinline__ uint32_t mulhi_64x32(uint64_t z, uint32_t n) {
 // draw_seed_pair (src/ransac.cpp:111-123): KeyedRng(seed, (u32)cluster,
 // (u32)trial); i = next_below(n); j = next_below(n-1), ++j if j >= i.
 // next_below is the high word of the 64x32 product (rng.hpp:34-38).
+// The trial-independent first step of the key (hoisted by per-cluster loops).
+__device__ __forceinline__ uint64_t seed_key(uint32_t cluster) {
+  return mix64(static_cast<uint64_t>(cluster) + kGamma);
+}
+// seed_pair with k1 = seed_key(cluster) precomputed.
+__device__ __forceinline__ void seed_pair_k(uint64_t seed, uint64_t k1, uint32_t trial, uint32_t n,
+                                            int& i, int& j) {
+  const uint64_t k = mix64(k1 ^ static_cast<uint64_t>(trial));
+  uint64_t state = mix64(k ^ seed);
+  state += kGamma;
+  const uint64_t z1 = mix64(state);
+  state += kGamma;
+  const uint64_t z2 = mix64(state);
+  i = static_cast<int>(mulhi_64x32(z1, n));
+  j = static_cast<int>(mulhi_64x32(z2, n - 1));
+  if (j >= i) ++j;
+}
+
 __device__ __forceinline__ void seed_pair(uint64_t seed, uint32_t cluster, uint32_t trial,
                                           uint32_t n, int& i, int& j) {
   uint64_t k = mix64(static_cast<uint64_t>(cluster) + kGamma);

@@ -579,76 +579,6 @@ prep_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   prep_cluster(sm, blockIdx.x, offsets, az, dop, scale, xy64, xy32, stat, norm);
 }
 
-// ------------------------------------------------ tensor-core operand layout
-//
-// The scoring MMA computes D[h][p] = sum_k Hyp[h][k] * Pt[p][k] over K = 8
-// tf32 values per row, with every FP64 coefficient and coordinate split into
-// two tf32 parts (v = v1 + v2 + O(2^-22 v)):
-//   hypothesis row h: [A1, A1, A2, B1, B1, B2, C1, C2]
-//   point row p:      [x1, x2, x1, y1, y2, y1, 1,  1 ]
-// so D = A x + B y + C with |D - exact| <= ~2^-22 S (measured 2^-22.3 S,
-// tools/tc_probe.cu; S = |A| + |B| + |C|). The corridor band is 2^-18 S.
-// Rows are stored in the K-major, no-swizzle canonical layout of
-// tcgen05.mma: 8-row x 16-byte core matrices, the two 16-byte K halves
-// 128 B apart (LBO), consecutive 8-row groups 256 B apart (SBO).
-constexpr float kTcBig = 0x1p100f;  // inert rows: |D| >= 2^100 is never inside a corridor
-
-struct TcOut {
-  float* hyp = nullptr;
-  float* pts = nullptr;
-  int4* items = nullptr;
-  int32_t* count = nullptr;
-  int64_t cap = 0;  // entries per size class
-};
-
-__host__ __device__ __forceinline__ int tc_kmaj_off(int row, int k) {  // in floats
-  return (row >> 3) * 64 + (k >> 2) * 32 + (row & 7) * 4 + (k & 3);
-}
-__device__ __forceinline__ float tf32_rna(float f) {
-  return __uint_as_float((__float_as_uint(f) + 0x1000u) & 0xFFFFE000u);
-}
-__device__ __forceinline__ void tf32_split(double v, float& hi, float& lo) {
-  hi = tf32_rna(__double2float_rn(v));
-  lo = tf32_rna(__double2float_rn(v - static_cast<double>(hi)));
-}
-// Writes one K = 8 operand row (two 16-byte halves) of a K-major tile.
-__device__ __forceinline__ void tc_store_row(float* tile, int row, float4 lo, float4 hi) {
-  *reinterpret_cast<float4*>(tile + tc_kmaj_off(row, 0)) = lo;
-  *reinterpret_cast<float4*>(tile + tc_kmaj_off(row, 4)) = hi;
-}
-__device__ __forceinline__ void tc_store_point(float* tile, int row, double x, double y) {
-  float x1, x2, y1, y2;
-  tf32_split(x, x1, x2);
-  tf32_split(y, y1, y2);
-  tc_store_row(tile, row, make_float4(x1, x2, x1, y1), make_float4(y2, y1, 1.f, 1.f));
-}
-__device__ __forceinline__ void tc_store_inert_point(float* tile, int row) {
-  tc_store_row(tile, row, make_float4(0.f, 0.f, 0.f, kTcBig), make_float4(0.f, kTcBig, 1.f, 1.f));
-}
-// Hypothesis row + squared corridor bound from the exact seeds (the same
-// FP64 slope/intercept as make_line, 1/den by rsqrt: a few ulps of 1/den
-// move A, B, C by ~1e-16 relative, far inside the band).
-__device__ __forceinline__ float tc_store_hyp(float* tile, int row, double x1, double y1,
-                                              double x2, double y2, double thr_hi) {
-  const double dx = __dsub_rn(x2, x1);
-  if (fabs(dx) < kSeedEpsilon) {  // degenerate seeds score 0 (src/ransac.cpp:40-42)
-    tc_store_row(tile, row, make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, kTcBig, 0.f));
-    return -1.f;
-  }
-  const double m = __ddiv_rn(__dsub_rn(y2, y1), dx);
-  const double c = __dsub_rn(y1, __dmul_rn(m, x1));
-  const double r = rsqrt(__dadd_rn(__dmul_rn(m, m), 1.0));
-  const double A = -m * r, B = r, C = -c * r;
-  float a1, a2, b1, b2, c1, c2;
-  tf32_split(A, a1, a2);
-  tf32_split(B, b1, b2);
-  tf32_split(C, c1, c2);
-  tc_store_row(tile, row, make_float4(a1, a1, a2, b1), make_float4(b1, b2, c1, c2));
-  const double band = (fabs(A) + fabs(B) + fabs(C)) * 0x1p-18;
-  const double hi = (thr_hi + band) * (1.0 + 0x1p-30);
-  return __double2float_ru(hi * hi);
-}
-
 // prep + hypothesis setup + tile registration, one CTA per cluster.
 //
 // Hypotheses (src/ransac.cpp:35-46 for every trial of draw_seed_pair
@@ -666,61 +596,22 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
                               uint64_t seed, double2* xy64, float2* __restrict__ xy32,
                               double4* __restrict__ stat, float* __restrict__ hyp,
                               int32_t* __restrict__ upper, int4* __restrict__ tiles,
-                              int32_t* __restrict__ tile_count, int64_t tile_cap,
-                              const TcOut& tc) {
+                              int32_t* __restrict__ tile_count, int64_t tile_cap) {
   prep_cluster(sm, c, offsets, az, dop, scale, xy64, xy32, stat, nullptr);
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const uint64_t k1 = seed_key(key);
   const double thr_lo = sm.stat.x, thr_hi = sm.stat.y;
   const double2* p64 = xy64 + b;  // written by this CTA before the barrier
   int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
-  if (tc.hyp != nullptr) {
-    // tensor-core operands: point rows, hypothesis tiles, corridor bounds
-    const int nhb = tc_blocks(g.T);
-    float* pts = tc.pts + tc_row_base(b, c) * 8;
-    const int nr = (n + 15) & ~15;
-    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-      float* tile = pts + (k & ~(kTcN - 1)) * 8;
-      if (k >= n) {
-        tc_store_inert_point(tile, k & (kTcN - 1));
-      } else {
-        const double2 q = p64[k];
-        tc_store_point(tile, k & (kTcN - 1), q.x, q.y);
-      }
-    }
-    float* hb0 = tc.hyp + static_cast<int64_t>(c) * nhb * kTcHypFloats;
-    for (int t = threadIdx.x; t < nhb * kTcM; t += blockDim.x) {
-      float* tile = hb0 + (t / kTcM) * kTcHypFloats;
-      float t2 = -1.f;
-      if (t < g.T) {
-        int i, j;
-        seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-        const double2 p = p64[i], q = p64[j];
-        t2 = tc_store_hyp(tile, t % kTcM, p.x, p.y, q.x, q.y, thr_hi);
-      } else {
-        tc_store_row(tile, t % kTcM, make_float4(0.f, 0.f, 0.f, 0.f),
-                     make_float4(0.f, 0.f, kTcBig, 0.f));
-      }
-      tile[kTcM * 8 + t % kTcM] = t2;
-    }
-    for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) uc[t] = 0;
-    if (threadIdx.x == 0) {
-      const int bk = kTcBuckets - 1 - min(kTcBuckets - 1, (n - 1) >> 6);
-      const int64_t r0 = tc_row_base(b, c);
-      tc.items[static_cast<int64_t>(bk) * tc.cap + atomicAdd(&tc.count[bk], 1)] =
-          make_int4(c, n, static_cast<int>(r0 & 0xFFFFFFFF), static_cast<int>(r0 >> 32));
-    }
-    return;
-  }
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   const bool seeds_in_smem = n <= sm.cap;
-  // hyp == nullptr: hyp_kernel builds the hypotheses and zeroes the counters
-  for (int t = threadIdx.x; hyp != nullptr && t < g.Tg * 8; t += blockDim.x) {
+  for (int t = threadIdx.x; t < g.Tg * 8; t += blockDim.x) {
     FastHyp f = inert_fast();
     if (t < g.T) {
       int i, j;
-      seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+      seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
       if (seeds_in_smem) {  // |y| (keys): a -0.0 seed is +0.0 here, same FP32 line
         const double* xs = sm.xs();
         const unsigned long long* ks = sm.keys();
@@ -772,7 +663,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                 const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed, double2* xy64,
                 float2* __restrict__ xy32, double4* __restrict__ stat, float* __restrict__ hyp,
                 int32_t* __restrict__ upper, int4* __restrict__ tiles,
-                int32_t* __restrict__ tile_count, int64_t tile_cap, TcOut tc, int cap,
+                int32_t* __restrict__ tile_count, int64_t tile_cap, int cap,
                 const int32_t* __restrict__ big_list, int32_t* big_ctl) {
   __shared__ PrepShared sm;
   prep_smem_setup(sm, cap);
@@ -780,7 +671,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   __shared__ int s_idx;
   if (big_list == nullptr) {
     prep_hyp_body(sm, tile_pos, blockIdx.x, offsets, az, dop, scale, keys, g, seed, xy64, xy32,
-                  stat, hyp, upper, tiles, tile_count, tile_cap, tc);
+                  stat, hyp, upper, tiles, tile_count, tile_cap);
     return;
   }
   for (;;) {
@@ -789,7 +680,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const int i = s_idx;
     if (i >= *reinterpret_cast<volatile int32_t*>(&big_ctl[0])) break;
     prep_hyp_body(sm, tile_pos, big_list[i], offsets, az, dop, scale, keys, g, seed, xy64, xy32,
-                  stat, hyp, upper, tiles, tile_count, tile_cap, tc);
+                  stat, hyp, upper, tiles, tile_count, tile_cap);
     __syncthreads();
   }
 }
@@ -1061,17 +952,18 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   if (lane == 0) stat[c] = make_double4(thr_lo, thr_hi, med, CUDART_NAN);
   // hypotheses (as prep_hyp_body, FFMA2 layout) and zeroed counters
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const uint64_t k1 = seed_key(key);
   const double2* p64 = xy64 + b;  // written by this warp before __syncwarp
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
   // two trials per lane and step: both seed pairs' loads are in flight
-  // before the first FP64 line is built (hyp == nullptr: hyp_kernel does it)
-  for (int t0 = lane; hyp != nullptr && t0 < g.Tg * 8; t0 += 64) {
+  // before the first FP64 line is built
+  for (int t0 = lane; t0 < g.Tg * 8; t0 += 64) {
     const int t1 = t0 + 32;
     const bool a0 = t0 < g.T, a1 = t1 < g.T;
     int i0 = 0, j0 = 0, i1 = 0, j1 = 0;
-    if (a0) seed_pair(seed, key, static_cast<uint32_t>(t0), static_cast<uint32_t>(n), i0, j0);
-    if (a1) seed_pair(seed, key, static_cast<uint32_t>(t1), static_cast<uint32_t>(n), i1, j1);
+    if (a0) seed_pair_k(seed, k1, static_cast<uint32_t>(t0), static_cast<uint32_t>(n), i0, j0);
+    if (a1) seed_pair_k(seed, k1, static_cast<uint32_t>(t1), static_cast<uint32_t>(n), i1, j1);
     const double2 p0 = p64[i0], q0 = p64[j0], p1 = p64[i1], q1 = p64[j1];
     const FastHyp f0 = a0 ? make_fast_from_seeds(p0.x, p0.y, q0.x, q0.y, thr_lo, thr_hi)
                           : inert_fast();
@@ -1112,39 +1004,6 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       tiles[bk * tile_cap + pos1 + hb] =
           make_int4(c, static_cast<int>(base32 + full * kScorePPT), rem, hb * g.TS);
   }
-}
-
-// Every trial's FP32 fast-pass hypothesis and zeroed counter, one thread per
-// trial over all clusters (after the prep kernels have written xy64 and the
-// threshold interval): the same seed pair, FP64 line and coefficients as
-// prep_hyp_body, without the per-cluster kernel's barriers in its way.
-__global__ void __launch_bounds__(256)
-hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
-           const int32_t* __restrict__ keys, ScoreGeom g, uint64_t seed,
-           const double2* __restrict__ xy64, const double4* __restrict__ stat,
-           float* __restrict__ hyp, int32_t* __restrict__ upper) {
-  const int tg8 = g.Tg * 8;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<int64_t>(n_clusters) * tg8) return;
-  const int c = static_cast<int>(idx / tg8);
-  const int t = static_cast<int>(idx - static_cast<int64_t>(c) * tg8);
-  FastHyp f = inert_fast();
-  if (t < g.T) {
-    const int64_t b = offsets[c];
-    const int n = static_cast<int>(offsets[c + 1] - b);
-    const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-    const double4 st = stat[c];
-    int i, j;
-    seed_pair(seed, key, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-    const double2 p = xy64[b + i], q = xy64[b + j];
-    f = make_fast_from_seeds(p.x, p.y, q.x, q.y, st.x, st.y);
-  }
-  float* h = hyp + static_cast<int64_t>(c) * g.Tg * 32 + (t >> 3) * 32 + (t & 7);
-  h[0] = f.A;
-  h[8] = f.B;
-  h[16] = f.C;
-  h[24] = -f.t2hi;  // K: the squared compare's bound
-  upper[idx] = 0;   // rows of Tg * 8 counters, cluster-major
 }
 
 // The exact reference threshold (left-to-right MAD sum), one warp per
@@ -1237,21 +1096,8 @@ __device__ __forceinline__ int4 unit_desc(const int* bstart, const int4* __restr
 }
 
 // Stages a unit's points (an even-aligned run of float2 = (n + 1) / 2 float4)
-// into a warp's shared-memory slot: cp.async, 16 B per lane and step, one
-// commit group per unit.
-__device__ __forceinline__ void stage_points(float4* slot, const float2* __restrict__ xy32,
-                                             int4 d, int lane) {
-  const float4* src = reinterpret_cast<const float4*>(xy32 + d.y);
-  const int m2 = (d.z + 1) >> 1;
-  for (int i = lane; i < m2; i += 32)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(slot + i)),
-                 "l"(src + i)
-                 : "memory");
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-// The same staging through the TMA engine: one 1-D bulk copy issued by lane 0,
-// completion (bytes) tracked on the slot's mbarrier.
+// into a warp's shared-memory slot through the TMA engine: one 1-D bulk copy
+// issued by lane 0, completion (bytes) tracked on the slot's mbarrier.
 __device__ __forceinline__ void stage_points_bulk(float4* slot, uint64_t* bar,
                                                   const float2* __restrict__ xy32, int4 d,
                                                   int lane) {
@@ -1262,7 +1108,6 @@ __device__ __forceinline__ void stage_points_bulk(float4* slot, uint64_t* bar,
   }
 }
 
-template <bool kBulk>
 __global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
@@ -1272,14 +1117,14 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
   // two point slots per warp: the current unit's and the next unit's (prefetch)
   extern __shared__ __align__(16) float4 pts_dyn[];
   auto pts_s = reinterpret_cast<float4(*)[2][kSlot]>(pts_dyn);
-  __shared__ __align__(8) uint64_t slot_bar[kScoreThreads / 32][2];  // kBulk: per slot
+  __shared__ __align__(8) uint64_t slot_bar[kScoreThreads / 32][2];  // per slot
   const int tid = threadIdx.x, lane = tid & 31;
-  if (kBulk && lane == 0) {
+  if (lane == 0) {
     mbar_init(&slot_bar[tid >> 5][0], 1);
     mbar_init(&slot_bar[tid >> 5][1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  uint32_t phase = 0;  // kBulk: parity bit per slot (bit b = slot b)
+  uint32_t phase = 0;  // parity bit per slot (bit b = slot b)
   if (tid < 32) {  // exclusive prefix of the bucket sizes
     int carry = 0;
     for (int b0 = 0; b0 < kTileBuckets; b0 += 32) {
@@ -1308,8 +1153,7 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
   int buf = 0;
   if (u < total) {
     d = unit_desc(bstart, tiles, tile_cap, u);
-    if (kBulk) stage_points_bulk(pts_s[tid >> 5][0], &slot_bar[tid >> 5][0], xy32, d, lane);
-    else stage_points(pts_s[tid >> 5][0], xy32, d, lane);
+    stage_points_bulk(pts_s[tid >> 5][0], &slot_bar[tid >> 5][0], xy32, d, lane);
   }
 #pragma unroll 1
   while (u < total) {
@@ -1343,21 +1187,13 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     int4 dn = make_int4(0, 0, 0, 0);
     if (u_next < total) {
       dn = unit_desc(bstart, tiles, tile_cap, u_next);
-      if (kBulk)  // the slot was last read one unit ago (the warp is converged)
-        stage_points_bulk(pts_s[tid >> 5][buf ^ 1], &slot_bar[tid >> 5][buf ^ 1], xy32, dn, lane);
-      else
-        stage_points(pts_s[tid >> 5][buf ^ 1], xy32, dn, lane);
-    } else if (!kBulk) {
-      asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count
+      // the slot was last read one unit ago (the warp is converged)
+      stage_points_bulk(pts_s[tid >> 5][buf ^ 1], &slot_bar[tid >> 5][buf ^ 1], xy32, dn, lane);
     }
     if (lane == 0) un = atomicAdd(next, 1);
     // 3. this unit's points have landed
-    if (kBulk) {
-      mbar_wait(&slot_bar[tid >> 5][buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-    } else {
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // all but the newest group
-    }
+    mbar_wait(&slot_bar[tid >> 5][buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
     __syncwarp();
 
     uint32_t cnt[kNH];
@@ -1400,293 +1236,6 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     u = u_next;
     d = dn;
     buf ^= 1;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
-// ---------------------------------------------------- tensor-core scoring
-//
-// score_tc_kernel: persistent, warp-specialized, one CTA per SM, 18 warps:
-//   warp 0      producer: claims work items (batches of 8, largest clusters
-//               first) and streams each item's hypothesis tile (+ corridor
-//               bounds) and its point tiles into shared memory with
-//               cp.async.bulk (TMA engine) on mbarriers;
-//   warp 1      MMA issuer (one lane): per point block ONE tcgen05.mma
-//               kind::tf32 (M = 128 hypotheses, N <= kTcN points, K = 8)
-//               into one of the TMEM accumulator buffers, tcgen05.commit to the
-//               epilogue and to the smem stages it frees;
-//   warps 2-17  epilogue: tcgen05.ld of the accumulator (thread = one
-//               hypothesis row, registers = points; four warps per TMEM lane
-//               quarter, kTcN / 4 columns each), g = D^2 - t2hi (FFMA2 over column
-//               pairs), sign-bit count (LEA.HI); per item one integer atomic
-//               per thread.
-// A work item = (cluster, block of 128 hypotheses) over all of the cluster's
-// points. Counts are upper bounds of the exact FP64 counts (band 2^-18 S,
-// see the operand layout above), as the FFMA2 path's; select_kernel decides
-// exactly.
-constexpr int kTcAStages = 4;
-constexpr int kTcBStages = 8;
-constexpr int kTcDStages = 8;
-constexpr int kTcTBufs = 512 / kTcN;                // TMEM accumulator buffers
-constexpr int kTcW = kTcN / 4;                      // columns per epilogue warp and block
-constexpr int kTcEpiWarps = 16;
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
-constexpr int kTcBatch = 8;                          // items per claim
-constexpr uint32_t kTcTmemCols = kTcTBufs * kTcN;    // 512: the whole TMEM
-constexpr uint32_t kTcATileBytes = kTcHypFloats * 4; // operand tile + bounds
-constexpr uint32_t kTcAStageBytes = 5120;
-constexpr uint32_t kTcBTileBytes = kTcN * kTcRowBytes;
-constexpr size_t kTcSmemUsed = 1024 + kTcAStages * kTcAStageBytes + kTcBStages * kTcBTileBytes;
-// more than half of the SM's shared memory: two scoring CTAs (each owning all
-// 512 TMEM columns) can never be co-resident
-constexpr size_t kTcSmemBytes = 116 * 1024;
-static_assert(kTcSmemUsed <= kTcSmemBytes, "stages exceed the reservation");
-
-struct TcShared {
-  uint64_t a_full[kTcAStages], a_empty[kTcAStages];
-  uint64_t b_full[kTcBStages], b_empty[kTcBStages];
-  uint64_t t_full[kTcTBufs], t_empty[kTcTBufs];
-  uint64_t d_full[kTcDStages], d_empty[kTcDStages];
-  int4 desc[kTcDStages];
-  int bstart[kTcBuckets + 1];
-  uint32_t tmem;
-};
-static_assert(sizeof(TcShared) <= 1024, "TcShared must fit the 1 KB header");
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-// Shared-memory matrix descriptor: K-major, no swizzle, LBO 128 B, SBO 256 B.
-__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
-         (static_cast<uint64_t>(256 >> 4) << 32) | (1ull << 46);
-}
-// D[tmem] = A[smem] * B[smem]^T, kind::tf32, f32 result (no accumulation).
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t rows) {
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((rows >> 3) << 17) |
-                         (static_cast<uint32_t>(kTcM >> 4) << 24);
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(0)
-      : "memory");
-}
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tc_ld_wait() {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-// Sign-bit count of D^2 - t2hi over 16 accumulator columns (FFMA2 pairs).
-__device__ __forceinline__ void tc_count16(const uint32_t (&r)[16], float2 nt2,
-                                           uint32_t (&cnt)[4]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float2 e = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-    const float2 g = __ffma2_rn(e, e, nt2);
-    cnt[(2 * j) & 3] += __float_as_uint(g.x) >> 31;
-    cnt[(2 * j + 1) & 3] += __float_as_uint(g.y) >> 31;
-  }
-}
-
-__global__ void __launch_bounds__(kTcThreads, 1)
-score_tc_kernel(const int4* __restrict__ items, int64_t cap, int32_t* __restrict__ item_count,
-                const float* __restrict__ hyp, const float* __restrict__ pts, int T, int Tg8,
-                int32_t* __restrict__ upper) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  TcShared& sh = *reinterpret_cast<TcShared*>(smem);
-  unsigned char* a_st = smem + 1024;
-  unsigned char* b_st = a_st + kTcAStages * kTcAStageBytes;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nhb = tc_blocks(T);
-  if (warp == 0) {
-    const int v = lane < kTcBuckets ? item_count[lane] : 0;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
-    }
-    if (lane < kTcBuckets) sh.bstart[lane] = incl - v;
-    if (lane == 31) sh.bstart[kTcBuckets] = incl;
-    if (lane == 0) {
-      for (int i = 0; i < kTcAStages; ++i) {
-        mbar_init(&sh.a_full[i], 1);
-        mbar_init(&sh.a_empty[i], 1 + kTcEpiWarps);  // MMA done + bounds read
-      }
-      for (int i = 0; i < kTcBStages; ++i) {
-        mbar_init(&sh.b_full[i], 1);
-        mbar_init(&sh.b_empty[i], 1);
-      }
-      for (int i = 0; i < kTcTBufs; ++i) {
-        mbar_init(&sh.t_full[i], 1);
-        mbar_init(&sh.t_empty[i], kTcEpiWarps);
-      }
-      for (int i = 0; i < kTcDStages; ++i) {
-        mbar_init(&sh.d_full[i], 1);
-        mbar_init(&sh.d_empty[i], kTcEpiWarps + 1);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sh.tmem)),
-                 "n"(kTcTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = sh.tmem;
-  const int total = sh.bstart[kTcBuckets] * nhb;
-
-  if (warp == 0) {  // ---- producer
-    int* next = item_count + kTcBuckets;
-    int k = 0, kb = 0;
-    for (bool done = false; !done;) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(next, kTcBatch);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      // lanes 0..7 resolve one item each: (cluster, n, row base), hyp block
-      int4 e = make_int4(-1, 0, 0, 0);
-      int hb = 0;
-      const int i = base + lane;
-      if (lane < kTcBatch && i < total) {
-        const int li = i / nhb;
-        hb = i - li * nhb;
-        int bk = 0;
-        while (sh.bstart[bk + 1] <= li) ++bk;
-        e = items[bk * cap + (li - sh.bstart[bk])];
-      }
-      for (int j = 0; j <= kTcBatch; ++j) {
-        const int c = j < kTcBatch ? __shfl_sync(0xffffffffu, e.x, j) : -1;
-        if (j == kTcBatch) break;  // batch done, claim the next one
-        const int n = __shfl_sync(0xffffffffu, e.y, j);
-        const int64_t row0 = (static_cast<int64_t>(__shfl_sync(0xffffffffu, e.w, j)) << 32) |
-                             static_cast<uint32_t>(__shfl_sync(0xffffffffu, e.z, j));
-        const int h = __shfl_sync(0xffffffffu, hb, j);
-        const int ds = k % kTcDStages;
-        if (lane == 0) {
-          mbar_wait(&sh.d_empty[ds], ((k / kTcDStages) & 1) ^ 1);
-          sh.desc[ds] = make_int4(c, h, n, 0);
-          mbar_arrive(&sh.d_full[ds]);
-        }
-        if (c < 0) {
-          done = true;
-          break;
-        }
-        if (lane == 0) {
-          const int as = k % kTcAStages;
-          mbar_wait(&sh.a_empty[as], ((k / kTcAStages) & 1) ^ 1);
-          mbar_expect_tx(&sh.a_full[as], kTcATileBytes);
-          bulk_g2s(a_st + as * kTcAStageBytes,
-                   hyp + (static_cast<int64_t>(c) * nhb + h) * kTcHypFloats, kTcATileBytes,
-                   &sh.a_full[as]);
-          for (int p0 = 0; p0 < n; p0 += kTcN, ++kb) {
-            const int bs = kb % kTcBStages;
-            const uint32_t rows = static_cast<uint32_t>(min(kTcN, (n - p0 + 15) & ~15));
-            mbar_wait(&sh.b_empty[bs], ((kb / kTcBStages) & 1) ^ 1);
-            mbar_expect_tx(&sh.b_full[bs], rows * kTcRowBytes);
-            bulk_g2s(b_st + bs * kTcBTileBytes, pts + (row0 + p0) * 8, rows * kTcRowBytes,
-                     &sh.b_full[bs]);
-          }
-        }
-        ++k;
-      }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      int kb = 0, kt = 0;
-      for (int k = 0;; ++k) {
-        const int ds = k % kTcDStages;
-        mbar_wait(&sh.d_full[ds], (k / kTcDStages) & 1);
-        const int4 d = sh.desc[ds];
-        mbar_arrive(&sh.d_empty[ds]);
-        if (d.x < 0) break;
-        const int n = d.z;
-        const int as = k % kTcAStages;
-        mbar_wait(&sh.a_full[as], (k / kTcAStages) & 1);
-        const uint64_t da = tc_desc(smem_u32(a_st + as * kTcAStageBytes));
-        for (int p0 = 0; p0 < n; p0 += kTcN, ++kb, ++kt) {
-          const int bs = kb % kTcBStages, tb = kt % kTcTBufs;
-          const uint32_t rows = static_cast<uint32_t>(min(kTcN, (n - p0 + 15) & ~15));
-          mbar_wait(&sh.b_full[bs], (kb / kTcBStages) & 1);
-          mbar_wait(&sh.t_empty[tb], ((kt / kTcTBufs) & 1) ^ 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          tc_mma(tmem + tb * kTcN, da, tc_desc(smem_u32(b_st + bs * kTcBTileBytes)), rows);
-          tc_commit(&sh.t_full[tb]);
-          tc_commit(&sh.b_empty[bs]);
-        }
-        tc_commit(&sh.a_empty[as]);
-      }
-    }
-    __syncwarp();
-  } else {  // ---- epilogue
-    const int quarter = warp & 3;          // a warp reads TMEM lanes 32 * (warp % 4) ..
-    const int part = (warp - 2) >> 2;      // columns [32 part, 32 part + 32) of each block
-    const int row = quarter * 32 + lane;
-    int kt = 0;
-    for (int k = 0;; ++k) {
-      const int ds = k % kTcDStages;
-      mbar_wait(&sh.d_full[ds], (k / kTcDStages) & 1);
-      const int4 d = sh.desc[ds];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.d_empty[ds]);
-      if (d.x < 0) break;
-      const int c = d.x, hb = d.y, n = d.z;
-      const int t = hb * kTcM + row;
-      const int as = k % kTcAStages;
-      mbar_wait(&sh.a_full[as], (k / kTcAStages) & 1);
-      const float bound =
-          reinterpret_cast<const float*>(a_st + as * kTcAStageBytes)[kTcM * 8 + row];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.a_empty[as]);
-      const float2 nt2 = make_float2(-bound, -bound);
-      uint32_t cnt[4] = {0u, 0u, 0u, 0u};
-      for (int p0 = 0; p0 < n; p0 += kTcN, ++kt) {
-        const int tb = kt % kTcTBufs;
-        const int rows = min(kTcN, (n - p0 + 15) & ~15);
-        const int c0 = part * kTcW;
-        mbar_wait(&sh.t_full[tb], (kt / kTcTBufs) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t base =
-            tmem + (static_cast<uint32_t>(quarter * 32) << 16) + tb * kTcN + c0;
-        uint32_t r[kTcW / 16][16];
-#pragma unroll
-        for (int q = 0; q < kTcW / 16; ++q)
-          if (c0 + 16 * q < rows) tc_ld16(base + 16 * q, r[q]);
-        tc_ld_wait();
-#pragma unroll
-        for (int q = 0; q < kTcW / 16; ++q)
-          if (c0 + 16 * q < rows) tc_count16(r[q], nt2, cnt);
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sh.t_empty[tb]);
-      }
-      const uint32_t tot = cnt[0] + cnt[1] + cnt[2] + cnt[3];
-      if (t < T && tot)
-        atomicAdd(&upper[static_cast<int64_t>(c) * Tg8 + t], static_cast<int32_t>(tot));
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(kTcTmemCols));
   }
 }
 
@@ -1777,7 +1326,7 @@ struct RefitStage {
 };
 
 // Thread 0: the 2x2 solve, fallback and heading from the reduced sums.
-__device__ void finish_refit(const RefitAcc& a, const double* __restrict__ az,
+__device__ __noinline__ void finish_refit(const RefitAcc& a, const double* __restrict__ az,
                              const double* __restrict__ dop, int64_t frame_id, int cluster_id,
                              rvk_estimate* __restrict__ out) {
   const double g00 = a.g00, g01 = a.g01, g11 = a.g11, b0 = a.b0, b1 = a.b1;
@@ -1894,21 +1443,18 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
 // the mask (evaluate_trial, :129-136) and accumulates the LSQ refit sums of
 // its inliers; only if another trial wins (or a distance fell inside the
 // threshold interval) is the pass repeated.
-__global__ void __launch_bounds__(kSelectThreads, 3)
-select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
-              const double* __restrict__ dop, const int32_t* __restrict__ keys,
-              const int32_t* __restrict__ cluster_ids, int64_t frame_id,
-              const double2* __restrict__ xy64, const float2* __restrict__ xy32,
-              const double4* __restrict__ stat, double scale, const int32_t* __restrict__ upper,
-              int T, uint64_t seed, int32_t* __restrict__ out_count,
-              int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
-              rvk_estimate* __restrict__ est) {
+__device__ __forceinline__ void select_cluster(
+    int c, const int64_t* __restrict__ offsets, const double* __restrict__ az,
+    const double* __restrict__ dop, const int32_t* __restrict__ keys,
+    const int32_t* __restrict__ cluster_ids, int64_t frame_id, const double2* __restrict__ xy64,
+    const float2* __restrict__ xy32, const double4* __restrict__ stat, double scale,
+    const int32_t* __restrict__ upper, int T, uint64_t seed, int32_t* __restrict__ out_count,
+    int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask, rvk_estimate* __restrict__ est) {
   __shared__ unsigned long long redu[32];
   __shared__ RefitStage rst;
   __shared__ unsigned long long best;
   __shared__ double sh_thr;
   __shared__ int sh_need_exact;
-  const int c = blockIdx.x;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
@@ -2070,6 +1616,31 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
   }
 }
 
+// One CTA per cluster (list == nullptr), or persistent CTAs over the list of
+// clusters the fused warp kernel left for the CTA path (list_n[0] entries).
+__global__ void __launch_bounds__(kSelectThreads, 3)
+select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
+              const double* __restrict__ dop, const int32_t* __restrict__ keys,
+              const int32_t* __restrict__ cluster_ids, int64_t frame_id,
+              const double2* __restrict__ xy64, const float2* __restrict__ xy32,
+              const double4* __restrict__ stat, double scale, const int32_t* __restrict__ upper,
+              int T, uint64_t seed, int32_t* __restrict__ out_count,
+              int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
+              rvk_estimate* __restrict__ est, const int32_t* __restrict__ list,
+              const int32_t* list_n) {
+  if (list == nullptr) {
+    select_cluster(blockIdx.x, offsets, az, dop, keys, cluster_ids, frame_id, xy64, xy32, stat,
+                   scale, upper, T, seed, out_count, out_trial, mask, est);
+    return;
+  }
+  const int m = *list_n;
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    select_cluster(list[i], offsets, az, dop, keys, cluster_ids, frame_id, xy64, xy32, stat,
+                   scale, upper, T, seed, out_count, out_trial, mask, est);
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------ warp-per-cluster select
 //
 // The same exact winner / mask / refit as select_kernel with ONE warp per
@@ -2226,6 +1797,482 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   }
 }
 
+// --------------------------------------------- fused warp-per-cluster path
+//
+// One warp owns one cluster of up to kFusedCap points from the raw FP64 input
+// to the outputs; every intermediate lives in the warp's shared-memory slot
+// or in registers:
+//   1. load az/dop once (coalesced) into the slot, min/max (first-occurrence
+//      +-0 semantics), exact normalisation in place (normalize_cluster,
+//      src/ransac.cpp:69-87) + FP32 point pairs for the scoring loop;
+//   2. exact median of the normalized dopplers and the MAD interval
+//      (include/rvk/ransac.hpp:53-84, src/ransac.cpp:89-94), as
+//      prep_warp_kernel;
+//   3. per block of 256 trials: lane j builds trials 8j..8j+7 (seed pairs,
+//      src/ransac.cpp:111-123; FP32 coefficients of the line, :35-46) in
+//      registers and scores them against the staged points (the FFMA2 loop
+//      of score_kernel): upper-bound counts, kept as u16 in the slot;
+//   4. the exact argmax / verification / winner mask / LSQ refit of
+//      select_warp_kernel (src/ransac.cpp:158-199, src/velocity.cpp:26-90).
+// HBM sees only the input (16 B/pt), the mask (1 B/pt) and the per-cluster
+// outputs -- no xy64 / xy32 / hypothesis / upper-bound round trips.
+// Persistent: warps claim clusters from a counter, so the latency-bound
+// phases of some warps overlap the FMA-bound scoring of the others.
+// Clusters larger than kFusedCap (or calls with T > kFusedMaxT) go to the
+// list for the CTA path (prep_hyp_kernel -> score_kernel -> select list).
+// 508 points: four 4-warp CTAs per SM fit the 228 KB of shared memory
+constexpr int kFusedCap = 508;
+constexpr int kFusedHist = 512;              // median buckets (power of two >= cap)
+constexpr int kFusedMaxT = 2 * kFusedHist;   // u16 upper bounds in the hist region
+constexpr int kFusedWarps = 4;
+constexpr int kFusedPairs = kFusedCap / 2 + 3;  // float4 (two points) per slot, + read-ahead
+static_assert(8 * kWarpCand <= 16 * kFusedPairs, "median candidates live in the pair region");
+
+// Byte offsets inside one warp's slot. The pair region holds the median's
+// candidates until the pairs are written (after the median).
+constexpr size_t kFsX = 0;                                   // double x[cap]  (normalized)
+constexpr size_t kFsY = kFsX + 8 * kFusedCap;                // double y[cap]  (normalized)
+constexpr size_t kFsP = kFsY + 8 * kFusedCap;                // float4 pairs | u64 cand
+constexpr size_t kFsH = kFsP + 16 * kFusedPairs;             // u32 hist[512] | u16 upper[1024]
+constexpr size_t kFusedSlotBytes = kFsH + 4 * kFusedHist;
+constexpr size_t kFusedSmemBytes = kFusedSlotBytes * kFusedWarps;
+
+extern __shared__ __align__(16) unsigned char fused_dyn[];
+
+// median key of point i: the normalized doppler's bits with the sign cleared
+// (-0.0 sorts with +0.0, as std::sort's operator< treats them)
+__device__ __forceinline__ unsigned long long fused_key(const double* y, int i) {
+  return static_cast<unsigned long long>(__double_as_longlong(y[i])) & ~(1ull << 63);
+}
+
+// k-th smallest key, MSD radix select with 8-bit digits (crowded bucket).
+__device__ __noinline__ unsigned long long fused_radix_select(const double* y, unsigned int* hist,
+                                                              int n, int k, int lane) {
+  unsigned long long prefix = 0, mask = 0;
+#pragma unroll 1
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const unsigned long long key = fused_key(y, i);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncwarp();
+    int digit, below;
+    warp_find_rank(hist, 8, k, lane, digit, below);
+    prefix |= static_cast<unsigned long long>(digit) << shift;
+    mask |= 0xFFull << shift;
+    k -= below;
+    __syncwarp();
+  }
+  return prefix;
+}
+
+// k-th and (k+1)-th smallest keys (warp_select_pair on the slot's arrays).
+// On entry hist[0, nb) holds the bucket histogram of the n keys.
+__device__ __forceinline__ void fused_select_pair(const double* y, unsigned int* hist,
+                                                  unsigned long long* cand, int n, int k,
+                                                  bool pair, int nb, int lane,
+                                                  unsigned long long& v0,
+                                                  unsigned long long& v1) {
+  int bin, below;
+  warp_find_rank(hist, nb >> 5, k, lane, bin, below);
+  const int in_bin = static_cast<int>(hist[bin]);
+  if (in_bin > kWarpCand) {
+    __syncwarp();
+    v0 = fused_radix_select(y, hist, n, k, lane);
+    if (pair) v1 = fused_radix_select(y, hist, n, k + 1, lane);
+    return;
+  }
+  int cnt = 0;  // compact the bucket's keys (order irrelevant)
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned long long key = i < n ? fused_key(y, i) : 0ull;
+    const bool hit = i < n && med_bin(key, nb) == bin;
+    const unsigned int m = __ballot_sync(0xffffffffu, hit);
+    if (hit) cand[cnt + __popc(m & ((1u << lane) - 1u))] = key;
+    cnt += __popc(m);
+  }
+  __syncwarp();
+  const int r0 = k - below;
+  const bool second_in_bin = pair && k + 1 < below + in_bin;
+  unsigned long long s0 = 0, s1 = 0;
+  bool f0 = false, f1 = false;
+  for (int i = lane; i < in_bin; i += 32) {
+    const unsigned long long ci = cand[i];
+    int less = 0, eq = 0;
+    for (int j = 0; j < in_bin; ++j) {
+      const unsigned long long cj = cand[j];
+      less += cj < ci;
+      eq += cj == ci;
+    }
+    if (r0 >= less && r0 < less + eq) {
+      s0 = ci;
+      f0 = true;
+    }
+    if (second_in_bin && r0 + 1 >= less && r0 + 1 < less + eq) {
+      s1 = ci;
+      f1 = true;
+    }
+  }
+  v0 = __shfl_sync(0xffffffffu, s0, __ffs(__ballot_sync(0xffffffffu, f0)) - 1);
+  if (pair) {
+    if (second_in_bin) {
+      v1 = __shfl_sync(0xffffffffu, s1, __ffs(__ballot_sync(0xffffffffu, f1)) - 1);
+    } else {  // the smallest key above the bucket
+      unsigned long long m = ~0ull;
+      for (int i = lane; i < n; i += 32) {
+        const unsigned long long key = fused_key(y, i);
+        if (med_bin(key, nb) > bin && key < m) m = key;
+      }
+      v1 = warp_umin64(m);
+    }
+  }
+  __syncwarp();
+}
+
+// exact_threshold on the slot's normalized dopplers (the reference's
+// left-to-right MAD sum, ransac.hpp:74-84 + ransac.cpp:89-94), one lane.
+__device__ __noinline__ double fused_exact_threshold(const double* y, int n, double med,
+                                                     double scale) {
+  double acc = 0.0;
+  for (int k = 0; k < n; ++k) acc = __dadd_rn(acc, fabs(__dsub_rn(y[k], med)));
+  return __dmul_rn(scale, __ddiv_rn(acc, static_cast<double>(n)));
+}
+
+// One cluster's slot as the select phase sees it.
+struct FusedCluster {
+  const double* xs;
+  const double* ys;
+  const float2* p32;
+  const double* caz;
+  const double* cdop;
+  uint8_t* cmask;
+  int n;
+  uint32_t key;
+  uint64_t seed;
+  bool refit;
+};
+
+__device__ __forceinline__ ExactHyp fused_make_exact(const FusedCluster& fc, int t, double thr_lo,
+                                                     double thr_hi) {
+  ExactHyp H;
+  seed_pair(fc.seed, fc.key, static_cast<uint32_t>(t), static_cast<uint32_t>(fc.n), H.a, H.b);
+  H.L = make_line(fc.xs[H.a], fc.ys[H.a], fc.xs[H.b], fc.ys[H.b]);
+  H.f = make_fast(H.L, thr_lo, thr_hi);
+  return H;
+}
+
+// classify() on the slot: the FP32 test with its certain-in / certain-out
+// bounds, the FP64 reference distance inside the band.
+__device__ __forceinline__ int fused_classify(const FusedCluster& fc, const ExactHyp& H, int k,
+                                              double thr_lo, double thr_hi) {
+  if (k == H.a || k == H.b) return kIn;
+  const float2 p = xy32_get(fc.p32, k);
+  const float e = __fmaf_rn(H.f.A, p.x, __fmaf_rn(H.f.B, p.y, H.f.C));
+  if (__fmaf_rn(e, e, -H.f.t2lo) < 0.f) return kIn;
+  if (!(__fmaf_rn(e, e, -H.f.t2hi) < 0.f)) return kOut;
+  const double r = __dsub_rn(__dadd_rn(__dmul_rn(-H.L.m, fc.xs[k]), fc.ys[k]), H.L.c);
+  const double d = __ddiv_rn(fabs(r), H.L.den);
+  if (d <= thr_lo) return kIn;
+  if (d > thr_hi) return kOut;
+  return kUndecided;
+}
+
+// One pass for trial t: mask + exact count + refit sums in the canonical
+// order (lane l, points k == l mod 32 ascending). false: some distance was
+// undecided (nothing valid; the caller switches to the exact threshold).
+__device__ __noinline__ bool fused_pass(const FusedCluster fc, int t, double thr_lo,
+                                        double thr_hi, int& count, RefitAcc& total) {
+  const ExactHyp H = fused_make_exact(fc, t, thr_lo, thr_hi);
+  RefitAcc acc;
+  bool und = false;
+  for (int k = threadIdx.x & 31; k < fc.n; k += 32) {
+    const int d = H.L.degenerate ? kOut : fused_classify(fc, H, k, thr_lo, thr_hi);
+    und |= d == kUndecided;
+    fc.cmask[k] = d == kIn ? 1 : 0;
+    if (d == kIn) {
+      if (fc.refit) acc.add(k, fc.caz[k], fc.cdop[k]);
+      else ++acc.nin;
+    }
+  }
+  if (__any_sync(0xffffffffu, und)) return false;
+  total = warp_reduce_refit(acc);
+  count = total.nin;
+  return true;
+}
+
+// Exact count of trial t by the warp (und: some distance undecided).
+__device__ __noinline__ int fused_exact_count(const FusedCluster fc, int t, double thr_lo,
+                                              double thr_hi, bool& und_out) {
+  const ExactHyp H = fused_make_exact(fc, t, thr_lo, thr_hi);
+  if (H.L.degenerate) {
+    und_out = false;
+    return 0;
+  }
+  int cnt = 0;
+  bool und = false;
+  for (int k = threadIdx.x & 31; k < fc.n; k += 32) {
+    const int d = fused_classify(fc, H, k, thr_lo, thr_hi);
+    cnt += d == kIn;
+    und |= d == kUndecided;
+  }
+  und_out = __any_sync(0xffffffffu, und);
+  return warp_reduce(cnt, SumI());
+}
+
+__global__ void __launch_bounds__(kFusedWarps * 32, 4)
+fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
+                  const double* __restrict__ az, const double* __restrict__ dop, double scale,
+                  const int32_t* __restrict__ keys, const int32_t* __restrict__ cluster_ids,
+                  int64_t frame_id, int T, uint64_t seed, int32_t* __restrict__ out_count,
+                  int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
+                  rvk_estimate* __restrict__ est, int32_t* __restrict__ big_list,
+                  int32_t* big_ctl) {
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  unsigned char* slot = fused_dyn + kFusedSlotBytes * wib;
+  double* xs = reinterpret_cast<double*>(slot + kFsX);
+  double* ys = reinterpret_cast<double*>(slot + kFsY);
+  float4* pairs = reinterpret_cast<float4*>(slot + kFsP);
+  float2* p32 = reinterpret_cast<float2*>(slot + kFsP);  // xy32_put / xy32_get layout
+  unsigned int* hist = reinterpret_cast<unsigned int*>(slot + kFsH);
+  uint16_t* upper = reinterpret_cast<uint16_t*>(slot + kFsH);
+  unsigned long long* cand = reinterpret_cast<unsigned long long*>(slot + kFsP);
+  const bool refit = est != nullptr;
+  const int fused_T = T <= kFusedMaxT;
+
+#pragma unroll 1
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&big_ctl[2], 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_clusters) break;
+    const int64_t b = offsets[c];
+    const int n = static_cast<int>(offsets[c + 1] - b);
+    if (n > kFusedCap || !fused_T) {  // the CTA path takes it
+      if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
+      continue;
+    }
+    const double* caz = az + b;
+    const double* cdop = dop + b;
+
+    // ---- 1. load, min/max, normalize (src/ransac.cpp:69-87)
+    int nb = 32;  // median buckets: about one per point, a power of two
+    while (nb < n) nb <<= 1;
+    for (int i = lane; i < nb; i += 32) hist[i] = 0;
+    double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
+    for (int k = lane; k < n; k += 32) {
+      const double a = caz[k], d = cdop[k];
+      xs[k] = a;  // raw values, normalized in place below (same lane)
+      ys[k] = d;
+      lo0 = a < lo0 ? a : lo0;
+      hi0 = a > hi0 ? a : hi0;
+      lo1 = d < lo1 ? d : lo1;
+      hi1 = d > hi1 ? d : hi1;
+    }
+    warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
+    if (lo0 == 0.0 || hi0 == 0.0 || lo1 == 0.0 || hi1 == 0.0) {
+      __syncwarp();  // (rare) the first +-0 in index order, from the raw slot
+      lo0 = warp_first_zero(lo0, xs, n, lane);
+      hi0 = warp_first_zero(hi0, xs, n, lane);
+      lo1 = warp_first_zero(lo1, ys, n, lane);
+      hi1 = warp_first_zero(hi1, ys, n, lane);
+    }
+    const double s0 = __dsub_rn(hi0, lo0);
+    const double s1 = __dsub_rn(hi1, lo1);
+    {
+      const bool f0 = div_span_ok(s0), f1 = div_span_ok(s1);
+      const double r0 = f0 ? fast_rcp(s0) : 0.0, r1 = f1 ? fast_rcp(s1) : 0.0;
+      for (int k = lane; k < n; k += 32) {
+        const double x = s0 == 0.0 ? 0.5
+                         : (f0 ? div_rn_shared(__dsub_rn(xs[k], lo0), s0, r0)
+                               : __ddiv_rn(__dsub_rn(xs[k], lo0), s0));
+        const double y = s1 == 0.0 ? 0.5
+                         : (f1 ? div_rn_shared(__dsub_rn(ys[k], lo1), s1, r1)
+                               : __ddiv_rn(__dsub_rn(ys[k], lo1), s1));
+        xs[k] = x;
+        ys[k] = y;
+        atomicAdd(&hist[med_bin(fused_key(ys, k), nb)], 1u);
+      }
+    }
+    __syncwarp();
+
+    // ---- 2. median (ransac.hpp:53-70) and the MAD interval (prep_cluster)
+    double thr_lo, thr_hi, med;
+    {
+      const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
+      unsigned long long v0 = 0, v1 = 0;
+      fused_select_pair(ys, hist, cand, n, k0, (n & 1) == 0, nb, lane, v0, v1);
+      const double d0 = __longlong_as_double(static_cast<long long>(v0));
+      med = (n & 1) ? d0
+                    : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))),
+                                2.0);
+      double part = 0.0;
+      for (int k = lane; k < n; k += 32)
+        part += fabs(__dsub_rn(__longlong_as_double(static_cast<long long>(fused_key(ys, k))), med));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const double mid = scale * (part / n);
+      const double delta = (4.0 * n + 16.0) * 0x1p-53;
+      thr_lo = mid * (1.0 - delta);
+      thr_hi = mid * (1.0 + delta);
+    }
+    __syncwarp();  // cand and hist are free: the pairs and the upper bounds reuse them
+    // FP32 point pairs (x_2q, x_2q+1, y_2q, y_2q+1) for the scoring loop;
+    // odd n padded with an inert point, plus the loop's read-ahead slack
+    {
+      const int m2 = (n + 1) >> 1;
+      for (int q = lane; q < m2 + 3; q += 32) {
+        float4 v = make_float4(0.f, 0.f, kPadY, kPadY);
+        const int k0 = 2 * q, k1 = 2 * q + 1;
+        if (k0 < n) {
+          v.x = __double2float_rn(xs[k0]);
+          v.z = __double2float_rn(ys[k0]);
+        }
+        if (k1 < n) {
+          v.y = __double2float_rn(xs[k1]);
+          v.w = __double2float_rn(ys[k1]);
+        }
+        pairs[q] = v;
+      }
+    }
+    __syncwarp();
+
+    // ---- 3. hypotheses + FP32 upper-bound scoring, 256 trials per block
+    const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+    const uint64_t k1 = seed_key(key);
+    unsigned long long vbest = 0;
+    const int m2 = (n + 1) >> 1;
+#pragma unroll 1
+    for (int tb = 0; tb < T; tb += 8 * 32) {
+      float A[kNH], B[kNH];
+      float2 Cc[kNH], T2[kNH];
+      // one copy of the (long) hypothesis code: trial q enters at slot kNH-1
+      // and the registers rotate down, so slot q holds trial 8 lane + q at
+      // the end (static register indices; the kernel's code size is what
+      // keeps the instruction cache warm across warps in different phases)
+#pragma unroll 1
+      for (int q = 0; q < kNH; ++q) {
+        const int t = tb + 8 * lane + q;
+        FastHyp f = inert_fast();
+        if (t < T) {
+          int i, j;
+          seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+          f = make_fast_from_seeds(xs[i], ys[i], xs[j], ys[j], thr_lo, thr_hi);
+        }
+#pragma unroll
+        for (int r = 0; r + 1 < kNH; ++r) {
+          A[r] = A[r + 1];
+          B[r] = B[r + 1];
+          Cc[r] = Cc[r + 1];
+          T2[r] = T2[r + 1];
+        }
+        A[kNH - 1] = f.A;
+        B[kNH - 1] = f.B;
+        Cc[kNH - 1] = make_float2(f.C, f.C);
+        T2[kNH - 1] = make_float2(-f.t2hi, -f.t2hi);
+      }
+      uint32_t cnt[kNH];
+#pragma unroll
+      for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+      auto score_pair = [&](const float4& v) {
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+        for (int h = 0; h < kNH; ++h) {
+          float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
+                                __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
+          e = __ffma2_rn(e, e, T2[h]);
+          cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
+        }
+      };
+      // four pairs per iteration; the padded slack is inert (e^2 overflows)
+#pragma unroll 1
+      for (int q2 = 0; q2 < m2; q2 += 4) {
+        const float4 v0 = pairs[q2], v1 = pairs[q2 + 1], v2 = pairs[q2 + 2], v3 = pairs[q2 + 3];
+        score_pair(v0);
+        score_pair(v1);
+        score_pair(v2);
+        score_pair(v3);
+      }
+#pragma unroll
+      for (int q = 0; q < kNH; ++q) {
+        const int t = tb + 8 * lane + q;
+        if (t < T) {
+          upper[t] = static_cast<uint16_t>(cnt[q]);
+          vbest = MaxU64()(vbest, pack_best(static_cast<int>(cnt[q]), t));
+        }
+      }
+    }
+    vbest = warp_reduce(vbest, MaxU64());
+    __syncwarp();  // upper[] visible to the whole warp
+    const int t0 = unpack_trial(vbest);
+    const int u0 = unpack_count(vbest);
+
+    // ---- 4. exact winner, mask, refit (select_warp_kernel on the slot)
+    const FusedCluster fc{xs, ys, p32, caz, cdop, mask + b, n, key, seed, refit};
+    auto pass = [&](int t, int& count, RefitAcc& total) -> bool {
+      return fused_pass(fc, t, thr_lo, thr_hi, count, total);
+    };
+    auto exact_count = [&](int t, bool& und) -> int {
+      return fused_exact_count(fc, t, thr_lo, thr_hi, und);
+    };
+    auto go_exact = [&]() {  // the exact sequential threshold (rare)
+      double t = 0.0;
+      if (lane == 0) t = fused_exact_threshold(ys, n, med, scale);
+      thr_lo = thr_hi = __shfl_sync(0xffffffffu, t, 0);
+    };
+    int e0 = 0;
+    RefitAcc tot;
+    if (!pass(t0, e0, tot)) {
+      go_exact();
+      pass(t0, e0, tot);
+    }
+    unsigned long long best = pack_best(e0, t0);
+    if (u0 > e0) {  // verify the trials that could still win
+      for (int round = 0; round < 2; ++round) {
+        bool need_exact = false;
+        for (int tb = 0; tb < T; tb += 32) {
+          const int tl = tb + lane;
+          const int u = tl < T ? static_cast<int>(upper[tl]) : -1;
+          unsigned cand_m = __ballot_sync(
+              0xffffffffu, tl < T && tl != t0 && !(u < e0 || (u == e0 && tl > t0)));
+          while (cand_m) {
+            const int t = tb + __ffs(cand_m) - 1;
+            cand_m &= cand_m - 1;
+            bool und;
+            const int e = exact_count(t, und);
+            if (und) need_exact = true;
+            else best = MaxU64()(best, pack_best(e, t));
+          }
+        }
+        if (need_exact && round == 0) {
+          go_exact();  // redo every candidate (and t0) with the exact threshold
+          pass(t0, e0, tot);
+          best = pack_best(e0, t0);
+          continue;
+        }
+        break;
+      }
+    }
+    const int win = unpack_trial(best);
+    const int win_count = unpack_count(best);
+    if (win != t0) {  // another trial won: its mask and refit sums
+      int cnt;
+      if (!pass(win, cnt, tot)) {
+        go_exact();
+        pass(win, cnt, tot);
+      }
+    }
+    if (lane == 0) {
+      if (out_count) out_count[c] = win_count;
+      if (out_trial) out_trial[c] = win;
+      if (refit) finish_refit(tot, caz, cdop, frame_id, cluster_ids ? cluster_ids[c] : c, est + c);
+    }
+    __syncwarp();  // the slot is rewritten by the next cluster
+  }
+}
+
 __global__ void __launch_bounds__(kSelectThreads)
 refit_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az,
              const double* __restrict__ dop, const int32_t* __restrict__ cluster_ids,
@@ -2332,37 +2379,32 @@ void launch_mad_exact(const FrameDev& f, double scale, const Scratch& s, cudaStr
   count_launch();
 }
 
-// The FFMA2 kernel is the default: measured on B200 (config 2, 8 frames per
-// call) it scores in 0.149 ms vs 0.183 ms for score_tc_kernel -- a kind::tf32
-// MMA of 128 x 256 x 8 keeps the tensor pipe busy ~470 cycles, so the tensor
-// path caps near 70 evals/cycle/SM while its epilogue still needs one ALU
-// instruction per eval (profiles/r1c_summary.md). RVK_SCORE=tc selects it.
-// Hypotheses inside the per-cluster prep kernels (default) or in their own
-// one-thread-per-trial kernel (RVK_HYP_KERNEL=1). Measured on B200
-// (gpurun_out/hk1): the split is slower -- config 2 prep + hypotheses 0.094
-// -> 0.108 ms -- because inside the prep kernels the hypothesis loop fills
-// the issue slots the latency-bound median phases of the other CTAs leave.
-bool hyp_kernel_enabled() {
-  static const bool v = env_int("RVK_HYP_KERNEL", 0) != 0;
-  return v;
-}
-
-// Point staging of score_kernel: TMA bulk copies with an mbarrier per slot
-// (default) or per-lane cp.async (RVK_SCORE_STAGE=lanes).
-bool score_uses_bulk() {
-  static const bool v = [] {
-    const char* e = std::getenv("RVK_SCORE_STAGE");
-    return !(e && std::strcmp(e, "lanes") == 0);
+int sm_count() {
+  static const int v = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
   }();
   return v;
 }
 
-bool score_uses_tc() {
-  static const bool v = [] {
-    const char* e = std::getenv("RVK_SCORE");
-    return e && std::strcmp(e, "tc") == 0;
-  }();
-  return v;
+// The fused warp-per-cluster kernel (RVK_FUSED=1; off by default): it
+// removes every intermediate HBM round trip but measured slower on B200 than
+// the three-kernel pipeline -- config 4, 4 frames: 0.42 vs 0.35 ms -- because
+// warps in different phases of the ~7.5k-instruction kernel thrash the
+// instruction cache (ncu: stall_no_instruction is its top stall reason, 3.0
+// cycles per issue; profiles/r2_fused_summary.md).
+bool fused_path(const FrameDev& f, const rvk_ransac_params& p) {
+  if (f.n_clusters == 0 || p.max_trials > kFusedMaxT) return false;
+  static const int forced = env_int("RVK_FUSED", 0);
+  return forced != 0;
+}
+
+// Whether the CTA path has clusters to take after the fused kernel: unknown
+// (device-side sizes) unless the host passed the largest cluster size.
+bool fused_leaves_big(const FrameDev& f) {
+  return f.max_cluster < 0 || f.max_cluster > kFusedCap;
 }
 
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
@@ -2370,61 +2412,42 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
   if (f.n_clusters == 0) return;
   ScoreGeom g = score_geom(p.max_trials);
   set_ppt(g, s.ppt);
-  TcOut tc;
-  if (s.tc) {
-    tc.hyp = s.tc_hyp;
-    tc.pts = s.tc_pts;
-    tc.items = s.tc_items;
-    tc.count = s.tc_count;
-    tc.cap = f.n_clusters;
-    cudaMemsetAsync(s.tc_count, 0, sizeof(int32_t) * (kTcBuckets + 1), st);
-  } else {
-    cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  if (fused_path(f, p)) {
+    // the clusters the fused kernel listed, by persistent CTAs
+    if (!fused_leaves_big(f)) return;
+    prep_hyp_kernel<256, 4><<<std::min<int64_t>(2 * sm_count(), f.n_clusters), 256,
+                              prep_dyn_bytes(2048), st>>>(
+        f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, 2048,
+        s.big_list, s.big_ctl);
+    count_launch();
+    return;
   }
   const CtaShape sh = cluster_cta_shape(f.n_points, f.n_clusters, "RVK_PREP_THREADS", false);
   const int64_t avg = f.n_points / f.n_clusters;
-  // hypotheses by hyp_kernel (one thread per trial) instead of inside the
-  // per-cluster prep kernels
-  const bool split = !s.tc && hyp_kernel_enabled();
-  float* prep_hyp_out = split ? nullptr : s.hyp;
-  auto launch_hyps = [&]() {
-    if (!split) return;
-    const int64_t total = static_cast<int64_t>(f.n_clusters) * g.Tg * 8;
-    hyp_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-        f.n_clusters, f.offsets, f.keys, g, p.rng_seed, s.xy64, s.stat, s.hyp, s.upper);
-    count_launch();
-  };
-  if (!s.tc && env_int("RVK_PREP_WARP", avg < 384 ? 1 : 0) != 0) {
+  if (env_int("RVK_PREP_WARP", avg < 384 ? 1 : 0) != 0) {
     // warp per cluster up to kWarpCap points; the rest by persistent CTAs
-    cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 2, st);
+    cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 4, st);
     prep_warp_kernel<<<(f.n_clusters + kPrepWarps - 1) / kPrepWarps, kPrepWarps * 32, 0, st>>>(
         f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-        s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap,
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap,
         s.big_list, s.big_ctl);
     count_launch();
-    static int big_grid = 0;
-    if (big_grid == 0) {
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      big_grid = 2 * sms;
-    }
-    prep_hyp_kernel<256, 4><<<std::min<int64_t>(big_grid, f.n_clusters), 256,
+    prep_hyp_kernel<256, 4><<<std::min<int64_t>(2 * sm_count(), f.n_clusters), 256,
                               prep_dyn_bytes(2048), st>>>(
         f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-        s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
-        2048, s.big_list, s.big_ctl);
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, 2048,
+        s.big_list, s.big_ctl);
     count_launch();
-    launch_hyps();
     return;
   }
   auto k = sh.threads > 256 ? prep_hyp_kernel<512, 2> : prep_hyp_kernel<256, 4>;
   k<<<f.n_clusters, sh.threads, prep_dyn_bytes(sh.cap), st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
-      s.xy64, s.xy32, s.stat, prep_hyp_out, s.upper, s.tiles, s.tile_count, s.tile_cap, tc,
-      sh.cap, nullptr, nullptr);
+      s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, sh.cap, nullptr,
+      nullptr);
   count_launch();
-  launch_hyps();
 }
 
 namespace {
@@ -2432,16 +2455,13 @@ namespace {
 int score_resident_ctas() {
   static int grid = 0;
   if (grid == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    for (auto k : {score_kernel<true>, score_kernel<false>})
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kScoreSmemBytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<true>, kScoreThreads,
+    int per_sm = 0;
+    cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kScoreSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kScoreThreads,
                                                   kScoreSmemBytes);
     per_sm = std::max(1, std::min(per_sm, env_int("RVK_SCORE_CTAS", per_sm)));
-    grid = sms * per_sm;
+    grid = sm_count() * per_sm;
   }
   return grid;
 }
@@ -2450,6 +2470,19 @@ int score_grid(int64_t max_units) {
   const int64_t warps_per_cta = kScoreThreads / 32;
   return static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + warps_per_cta - 1) / warps_per_cta)));
+}
+int fused_resident_ctas() {
+  static int grid = 0;
+  if (grid == 0) {
+    int per_sm = 0;
+    cudaFuncSetAttribute(fused_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kFusedSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_warp_kernel, kFusedWarps * 32,
+                                                  kFusedSmemBytes);
+    per_sm = std::max(1, std::min(per_sm, env_int("RVK_FUSED_CTAS", per_sm)));
+    grid = sm_count() * per_sm;
+  }
+  return grid;
 }
 }  // namespace
 
@@ -2467,38 +2500,28 @@ int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
   return ppt;
 }
 
+void launch_fused(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                  const Outputs& o, cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 4, st);
+  const int64_t want = (static_cast<int64_t>(f.n_clusters) + kFusedWarps - 1) / kFusedWarps;
+  const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(), want));
+  fused_warp_kernel<<<grid, kFusedWarps * 32, kFusedSmemBytes, st>>>(
+      f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, f.cluster_ids,
+      f.frame_id, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial, o.mask, o.est,
+      s.big_list, s.big_ctl);
+  count_launch();
+}
+
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
-  if (s.tc) {
-    static int grid = 0;
-    if (grid == 0) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaFuncSetAttribute(score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kTcSmemBytes));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_tc_kernel, kTcThreads,
-                                                    kTcSmemBytes);
-      grid = sms;  // one CTA per SM: it owns all 512 TMEM columns
-    }
-    const int64_t items = static_cast<int64_t>(f.n_clusters) * tc_blocks(p.max_trials);
-    const ScoreGeom g = score_geom(p.max_trials);
-    score_tc_kernel<<<static_cast<int>(std::min<int64_t>(grid, items)), kTcThreads, kTcSmemBytes,
-                      st>>>(s.tc_items, f.n_clusters, s.tc_count, s.tc_hyp, s.tc_pts,
-                            p.max_trials, g.Tg * 8, s.upper);
-    count_launch();
-    return;
-  }
+  if (fused_path(f, p) && !fused_leaves_big(f)) return;
   ScoreGeom g = score_geom(p.max_trials);
   set_ppt(g, s.ppt);
   const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / g.ppt + f.n_clusters);
-  if (score_uses_bulk())
-    score_kernel<true><<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
-        s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
-  else
-    score_kernel<false><<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
-        s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+  score_kernel<<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
+      s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
   count_launch();
 }
 
@@ -2506,6 +2529,15 @@ void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch&
                    const Outputs& o, cudaStream_t st) {
   if (f.n_clusters == 0) return;
   const int64_t avg = f.n_points / f.n_clusters;
+  if (fused_path(f, p)) {  // the CTA path's share: the listed clusters
+    if (!fused_leaves_big(f)) return;
+    select_kernel<<<std::min<int64_t>(2 * sm_count(), f.n_clusters), 256, 0, st>>>(
+        f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32,
+        s.stat, p.threshold_scale, s.upper, p.max_trials, p.rng_seed, o.inlier_count,
+        o.winning_trial, o.mask, o.est, s.big_list, s.big_ctl);
+    count_launch();
+    return;
+  }
   if (env_int("RVK_SELECT_WARP", avg < 384 ? 1 : 0) != 0) {  // warp per cluster
     select_warp_kernel<<<(f.n_clusters + kSelectWarps - 1) / kSelectWarps, kSelectWarps * 32, 0,
                          st>>>(f.n_clusters, f.offsets, f.azimuth, f.doppler, f.keys,
@@ -2519,7 +2551,7 @@ void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch&
   select_kernel<<<f.n_clusters, sh.threads, 0, st>>>(
       f.offsets, f.azimuth, f.doppler, f.keys, f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
       p.threshold_scale, s.upper, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial,
-      o.mask, o.est);
+      o.mask, o.est, nullptr, nullptr);
   count_launch();
 }
 

@@ -21,6 +21,7 @@ struct FrameDev {
   const int32_t* cluster_ids = nullptr;  // [C] or null (positional)
   const int32_t* order = nullptr;     // [C] scoring order (largest first) or null
   int64_t frame_id = 0;
+  int64_t max_cluster = -1;           // largest cluster size if the host knows it, else -1
 };
 
 // Scoring geometry for a given max_trials T (host and device agree on it).
@@ -68,23 +69,6 @@ inline int64_t tile_capacity(const ScoreGeom& g, int64_t n_points, int32_t n_clu
 // better balance, lower latency). RVK_SCORE_PPT overrides (tests).
 int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters);
 
-// Tensor-core scoring (score_tc_kernel): D[h][p] = A_h x_p + B_h y_p + C_h
-// for a block of kTcM hypotheses x up to kTcN points is ONE tcgen05.mma
-// kind::tf32 (K = 8) over split operands; the epilogue squares and counts.
-constexpr int kTcM = 128;         // hypotheses per block (MMA M, TMEM lanes)
-constexpr int kTcN = 256;         // points per block (MMA N, TMEM columns per buffer)
-constexpr int kTcBuckets = 32;    // item size classes (cluster size / 64), largest first
-constexpr int kTcRowBytes = 32;   // one K = 8 row of tf32 operands
-// one hypothesis block in HBM: the 4 KB operand tile + its 128 corridor bounds
-constexpr int kTcHypFloats = kTcM * 8 + kTcM;
-
-inline __host__ __device__ int tc_blocks(int T) { return (T + kTcM - 1) / kTcM; }
-// first operand row of cluster c in the point-tile array (16-row aligned,
-// room for the padding of every cluster before it)
-inline __host__ __device__ int64_t tc_row_base(int64_t offset_c, int c) {
-  return ((offset_c + 15) & ~int64_t{15}) + 32 * static_cast<int64_t>(c);
-}
-
 struct Scratch {
   double2* xy64 = nullptr;   // [P] normalized (x, y), FP64
   float2* xy32 = nullptr;    // [P + 2C + 10] normalized (x, y), FP32, each cluster
@@ -96,17 +80,11 @@ struct Scratch {
   float* hyp = nullptr;      // [C*Tg*32] per group of 8: A[8] B[8] C[8] K[8]
   int4* tiles = nullptr;     // [kTileBuckets * tile_cap] scoring tile descriptors
   int32_t* tile_count = nullptr;  // [kTileBuckets + 1] tiles per bucket + claim counter (zeroed per call)
-  int32_t* big_list = nullptr;    // [C] clusters too large for the warp-per-cluster prep
-  int32_t* big_ctl = nullptr;     // [2] big_list count + claim counter (zeroed per call)
+  int32_t* big_list = nullptr;    // [C] clusters too large for the warp-per-cluster kernels
+  int32_t* big_ctl = nullptr;     // [4] big_list count, CTA-prep claim counter, fused-kernel
+                                  // claim counter (zeroed per call)
   int64_t tile_cap = 0;
   int ppt = kScorePPT;            // points per scoring unit of this call (score_ppt)
-  // tensor-core scoring
-  float* tc_hyp = nullptr;     // [C][tc_blocks(T)][kTcHypFloats]: K-major operand tile
-                               // (4 KB) + squared corridor bound per hypothesis
-  float* tc_pts = nullptr;     // [P + 32C + 32] K-major operand rows (points), tc_row_base
-  int4* tc_items = nullptr;    // [kTcBuckets][C] (cluster, n, row base) by size class
-  int32_t* tc_count = nullptr; // [kTcBuckets + 1] per-class counts + claim counter (zeroed per call)
-  bool tc = false;             // scoring path: tensor cores (default) or FFMA2
 };
 
 struct Outputs {
@@ -127,10 +105,15 @@ void launch_mad_exact(const FrameDev& f, double threshold_scale, const Scratch& 
 // coefficients) + scoring-tile registration, one CTA per cluster.
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                       cudaStream_t st);
-// Scoring path selection (RVK_SCORE=tc selects the tensor-core kernel; default FFMA2).
-bool score_uses_tc();
-// Upper-bound inlier counts for every (cluster, trial): tensor-core (tcgen05)
-// or FFMA2 scoring.
+// Whether a call takes the fused warp-per-cluster kernel (launch_fused) for its
+// clusters of <= 512 points; the CTA path (prep_hyps -> score -> select) then
+// runs on the clusters the fused kernel lists.
+bool fused_path(const FrameDev& f, const rvk_ransac_params& p);
+// The whole path for every cluster of <= 512 points, one warp each: normalize,
+// median/MAD, hypotheses, FP32 upper-bound scoring, exact select, mask, refit.
+void launch_fused(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                  const Outputs& o, cudaStream_t st);
+// Upper-bound inlier counts for every (cluster, trial): FFMA2 scoring.
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);
 // Exact argmax (verifying every candidate that could win), winner mask,

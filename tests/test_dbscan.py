@@ -152,7 +152,7 @@ def test_gpu_estimate_frame_matches_reference_pipeline(gpu_lib, reference):
         np.testing.assert_array_equal(res.mask, r.mask)
         np.testing.assert_array_equal(res.winning_trial, r.winning_trial)
         np.testing.assert_array_equal(res.inlier_count, r.inlier_count)
-        assert_estimates_close(est, e, label=f"frame {s}")
+        assert_estimates_close(est, e, label=f"frame {s}", frame=(roff, az, r.mask))
 
 
 # ------------------------------------------------------------ combine_masks

@@ -34,9 +34,9 @@ def test_native_library_is_the_cuda_one(gpu_lib):
     gpu_lib.rvk_reset_kernel_launches()
     off = np.array([0, 5], np.int64)
     rvk.run_ransac_csr(off, np.linspace(0, 1, 5), np.linspace(1, 2, 5), rvk.RansacParams(8))
-    # prep (one CTA per cluster, or warp-per-cluster + persistent CTAs for
-    # the large clusters), hypotheses (unless RVK_HYP_KERNEL=0), score, select
-    assert gpu_lib.rvk_kernel_launches() in (3, 4, 5)
+    # the fused warp-per-cluster kernel alone (the host knows every cluster
+    # fits), or prep (+ the persistent CTA prep of large clusters), score, select
+    assert gpu_lib.rvk_kernel_launches() in (1, 3, 4)
 
 
 def test_seed_pairs_vs_oracle(gpu_lib, oracle):
@@ -90,12 +90,13 @@ def test_ransac_estimate_golden(gpu_lib, golden_cases):
                                          frame_id=g["frame_id"],
                                          cluster_ids=np.arange(n, dtype=np.int32) + 100)
         np.testing.assert_array_equal(r.mask, g["mask"], err_msg=g["name"])
-        assert_estimates_close(est, g["estimates"], label=g["name"])
+        fr = (g["offsets"], g["az"], g["mask"])
+        assert_estimates_close(est, g["estimates"], label=g["name"], frame=fr)
         # estimate_all on the reference's masks too
         est2 = rvk.estimate_all_csr(g["offsets"], g["az"], g["dop"], g["mask"],
                                     frame_id=g["frame_id"],
                                     cluster_ids=np.arange(n, dtype=np.int32) + 100)
-        assert_estimates_close(est2, g["estimates"], label=g["name"] + "/estimate_all")
+        assert_estimates_close(est2, g["estimates"], label=g["name"] + "/estimate_all", frame=fr)
 
 
 def test_c3_thousand_random_frames(gpu_lib, oracle):
@@ -111,7 +112,7 @@ def test_c3_thousand_random_frames(gpu_lib, oracle):
         np.testing.assert_array_equal(r.winning_trial, o.winning_trial, err_msg=f"frame {f}")
         np.testing.assert_array_equal(r.inlier_count, o.inlier_count, err_msg=f"frame {f}")
         oe = oracle.estimate_all(off, az, dop, o.mask, frame_id=f)
-        assert_estimates_close(est, oe, label=f"frame {f}")
+        assert_estimates_close(est, oe, label=f"frame {f}", frame=(off, az, o.mask))
 
 
 @pytest.mark.parametrize("scale", [1.0, 0.25, 1e-3, 3.0])
@@ -137,7 +138,7 @@ def test_config1_full(gpu_lib, oracle):
     np.testing.assert_array_equal(r.mask, o.mask)
     np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
     np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
-    assert_estimates_close(est, oe)
+    assert_estimates_close(est, oe, frame=(w.offsets, w.azimuth, o.mask))
 
 
 @pytest.mark.parametrize("cfg", [2, 3, 4])
@@ -162,7 +163,8 @@ def test_full_size_configs_sampled(gpu_lib, oracle, cfg):
         np.testing.assert_array_equal(r.mask[sl], o.mask[sl], err_msg=f"cfg {cfg} cluster {c}")
         assert r.winning_trial[c] == o.winning_trial[c]
         assert r.inlier_count[c] == o.inlier_count[c]
-        assert_estimates_close(est[c:c + 1], oe[c:c + 1], label=f"cfg {cfg} cluster {c}")
+        assert_estimates_close(est[c:c + 1], oe[c:c + 1], label=f"cfg {cfg} cluster {c}",
+                               frame=(w.offsets[c:c + 2] - w.offsets[c], w.azimuth[sl], o.mask[sl]))
     # size-independent properties over every cluster
     per = np.add.reduceat(r.mask.astype(np.int64), w.offsets[:-1])
     np.testing.assert_array_equal(per, r.inlier_count)
@@ -286,7 +288,7 @@ def test_launch_shapes_bit_identical(gpu_lib):
                 {"RVK_SELECT_WARP": "0", "RVK_SELECT_THREADS": "64"},
                 {"RVK_SELECT_WARP": "0", "RVK_SELECT_THREADS": "256"},
                 {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0", "RVK_PREP_THREADS": "512"},
-                {"RVK_SCORE_PPT": "64"}):
+                {"RVK_SCORE_PPT": "64"}, {"RVK_FUSED": "1"}, {"RVK_FUSED": "0"}):
         r = subprocess.run([sys.executable, "-c", _SHAPE_SCRIPT, ROOT], capture_output=True,
                            text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -342,7 +344,7 @@ def test_edge_cases_extreme_values(gpu_lib, oracle):
             np.testing.assert_array_equal(r.winning_trial, o.winning_trial)
             np.testing.assert_array_equal(r.inlier_count, o.inlier_count)
             oe = oracle.estimate_all(off, az, dop, o.mask)
-            assert_estimates_close(est, oe, label=f"T={T} scale={scale}")
+            assert_estimates_close(est, oe, label=f"T={T} scale={scale}", frame=(off, az, o.mask))
 
 
 def test_errors_and_reference_shaped_api(gpu_lib, oracle):
@@ -455,30 +457,34 @@ def est_dtype():
     return _native.ESTIMATE_DTYPE
 
 
-@pytest.mark.parametrize("env", [{"RVK_SCORE": "tc"},
-                                 {"RVK_PREP_THREADS": "256", "RVK_SELECT_THREADS": "256"},
-                                 {"RVK_PREP_THREADS": "64", "RVK_SELECT_THREADS": "64"},
-                                 {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0"},
-                                 {"RVK_HYP_KERNEL": "1"},
-                                 {"RVK_HYP_KERNEL": "1", "RVK_PREP_WARP": "1"},
-                                 {"RVK_SCORE_STAGE": "lanes"},
-                                 {"RVK_SELECT_WARP": "1"}, {"RVK_SELECT_WARP": "0"},
+@pytest.mark.parametrize("env", [{"RVK_FUSED": "1"}, {"RVK_FUSED": "0"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "256",
+                                  "RVK_SELECT_THREADS": "256"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "64",
+                                  "RVK_SELECT_THREADS": "64"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_WARP": "1"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_WARP": "0"},
+                                 {"RVK_FUSED": "0", "RVK_SELECT_WARP": "1"},
+                                 {"RVK_FUSED": "0", "RVK_SELECT_WARP": "0"},
                                  {"RVK_SCORE_PPT": "64"}, {"RVK_SCORE_PPT": "512"},
-                                 {"RVK_PREP_THREADS": "512", "RVK_PREP_WARP": "0"}],
-                         ids=["tensor_core_scoring", "cta256", "cta64", "warp_prep", "cta_prep",
-                              "hyp_kernel", "hyp_kernel_warp_prep", "cp_async_staging",
-                              "warp_select", "cta_select", "units_64", "units_512", "cta512_prep"])
+                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "512",
+                                  "RVK_PREP_WARP": "0"}],
+                         ids=["fused", "unfused", "cta256", "cta64", "warp_prep", "cta_prep",
+                              "warp_select", "cta_select", "units_64", "units_512",
+                              "cta512_prep"])
 def test_alternative_kernel_shapes_parity(gpu_lib, env):
-    """Every kernel variant must give the same bytes: the tcgen05 scoring
-    kernel (RVK_SCORE=tc), the per-cluster CTA shapes of prep/select, the
-    warp-per-cluster prep (normally chosen from the mean cluster size) and the
-    separate one-thread-per-trial hypothesis kernel (RVK_HYP_KERNEL=1). The golden, C3 and
-    full-size parity tests re-run in a child process with the variant
-    selected (selections are read once per process)."""
+    """Every kernel variant must give the same bytes: the fused
+    warp-per-cluster kernel forced on/off for every call (normally chosen from
+    the mean cluster size; clusters > 512 points then take the CTA path), the
+    per-cluster CTA shapes of prep/select, the warp-per-cluster prep and
+    select, the scoring unit sizes. The golden, C3 and full-size parity tests
+    re-run in a child process with the variant selected (selections are read
+    once per process)."""
     r = subprocess.run(
         [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
          os.path.join(ROOT, "tests", "test_gpu_parity.py"),
-         "-k", "golden or c3 or config1 or full_size or edge or batch_composition or radar"],
+         "-k", "golden or c3 or config1 or full_size or edge or batch_composition or radar or "
+         "device_api or bench_batches"],
         capture_output=True, text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout

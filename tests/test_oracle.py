@@ -61,7 +61,8 @@ def test_lsq_matches_reference(oracle, golden_cases):
         # Eigen stand-in: bit-identical.
         for f in ("v_x", "v_y", "heading", "has_heading", "condition_ok", "inlier_count"):
             np.testing.assert_array_equal(est[f], g["estimates"][f], err_msg=g["name"] + f)
-        assert_estimates_close(est, g["estimates"], label=g["name"])
+        assert_estimates_close(est, g["estimates"], label=g["name"],
+                               frame=(g["offsets"], g["az"], g["mask"]))
 
 
 def test_live_against_reference_random(oracle, reference):

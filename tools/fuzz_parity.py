@@ -68,7 +68,7 @@ def main():
         np.testing.assert_array_equal(r.winning_trial, ro.winning_trial, err_msg=f"frame {f}")
         np.testing.assert_array_equal(r.inlier_count, ro.inlier_count, err_msg=f"frame {f}")
         oe = o.estimate_all(off, az, dop, ro.mask, frame_id=f)
-        assert_estimates_close(est, oe, label=f"frame {f}")
+        assert_estimates_close(est, oe, label=f"frame {f}", frame=(off, az, ro.mask))
         n_clusters += k
         n_points += int(off[-1])
     print(json.dumps({"frames": args.frames, "clusters": n_clusters, "points": n_points,
