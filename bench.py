@@ -89,7 +89,7 @@ def h2d_link_probe(step_bytes, dev):
 
 
 def make_frames(cfg, indices):
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     out = []
     for i in indices:
         if cfg == 2:

@@ -382,6 +382,14 @@ class Reference(_Lib, _Clustering):
                       0 if mode == "parallel" else 2, eps, min_pts, max_trials, threshold_scale,
                       seed))
 
+    def rng_units(self, seed, hi, lo, out):
+        f = self._fn("rng_units")
+        f.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_double)]
+        f.restype = None
+        f(seed & (2**64 - 1), hi & (2**64 - 1), lo & (2**64 - 1), out.size,
+          _p(out, C.c_double))
+        return out
+
     def generate_frame(self, seed, objects, offset_range=(2.0, 5.0)):
         objects = np.ascontiguousarray(objects, np.float64).reshape(-1, 10)
         p = int(objects[:, 6].sum())

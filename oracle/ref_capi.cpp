@@ -234,6 +234,12 @@ int rvk_ref_seed_pair(uint64_t seed, int32_t cluster, int32_t trial, int32_t n, 
   });
 }
 
+// n draws of KeyedRng(seed, hi, lo).next_unit() (workload layout draws).
+void rvk_ref_rng_units(uint64_t seed, uint64_t hi, uint64_t lo, int64_t n, double* out) {
+  rvk::KeyedRng rng(seed, hi, lo);
+  for (int64_t i = 0; i < n; ++i) out[i] = rng.next_unit();
+}
+
 uint64_t rvk_ref_rng_u64(uint64_t seed, uint64_t hi, uint64_t lo, int32_t k) {
   rvk::KeyedRng rng(seed, hi, lo);
   uint64_t v = 0;

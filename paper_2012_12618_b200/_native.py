@@ -1,7 +1,7 @@
 """ctypes binding of the in-tree native libraries.
 
 * ``lib/librvk_gpu.so``   -- the sm_100a kernels + C-ABI (include/rvk_gpu.h).
-* ``lib/librvk_scene.so`` -- host-side synthetic frame generator (csrc/rvk_scene.c).
+* ``lib/librvk_probe.so`` -- the FP32-pipe peak probe (bench.py's roofline denominator).
 
 There is no fallback: if the CUDA library is missing, ``gpu()`` raises. Build
 with ``python -m paper_2012_12618_b200.build`` (or ``__graft_entry__.build()``).
@@ -17,7 +17,6 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(PKG, "lib")
 GPU_SO = os.path.join(LIB_DIR, "librvk_gpu.so")
-SCENE_SO = os.path.join(LIB_DIR, "librvk_scene.so")
 PROBE_SO = os.path.join(LIB_DIR, "librvk_probe.so")
 
 RVK_OK, RVK_EINVAL, RVK_ECLUSTER_TOO_SMALL, RVK_ECUDA, RVK_ENOMEM = range(5)
@@ -51,7 +50,6 @@ assert ESTIMATE_DTYPE.itemsize == C.sizeof(EstimateC) == 48
 
 _lock = threading.Lock()
 _gpu = None
-_scene = None
 
 _P = C.c_void_p
 _I32, _I64, _U64, _F64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
@@ -84,13 +82,6 @@ GPU_SIGNATURES = {
     "rvk_profile_read": (C.c_int, [_P, _P, _I32]),
 }
 
-SCENE_SIGNATURES = {
-    "rvk_scene_generate": (C.c_int, [_U64, _I32, _P, _F64, _F64, _P, _P, _P, _P, _P]),
-    "rvk_scene_rng_u64": (_U64, [_U64, _U64, _U64, _I32]),
-    "rvk_scene_rng_units": (None, [_U64, _U64, _U64, _I64, _P]),
-}
-
-
 def _bind(lib, sigs):
     for name, (res, args) in sigs.items():
         f = getattr(lib, name)
@@ -112,16 +103,6 @@ def gpu():
             if _gpu.rvk_abi_version() != 1:
                 raise RuntimeError("librvk_gpu.so ABI mismatch")
         return _gpu
-
-
-def scene():
-    global _scene
-    with _lock:
-        if _scene is None:
-            if not os.path.exists(SCENE_SO):
-                raise RuntimeError(f"{SCENE_SO} is missing: run the package build")
-            _scene = _bind(C.CDLL(SCENE_SO), SCENE_SIGNATURES)
-        return _scene
 
 
 def probe():

@@ -4,7 +4,6 @@
 
 * lib/librvk_gpu.so   nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3
                       csrc/rvk_kernels.cu csrc/rvk_capi.cu      (C-ABI, include/rvk_gpu.h)
-* lib/librvk_scene.so gcc csrc/rvk_scene.c                      (host workload generator)
 * lib/rvk_gpu          g++ csrc/rvk_cli.cpp: the reference CLI's `estimate` command
                       (frame CSV in, estimate CSV out) on the device path.
 * lib/librvk_dropin.so g++ csrc/rvk_dropin.cpp against the Eigen stand-in: the
@@ -64,15 +63,6 @@ def build_probe(force=False):
     return out
 
 
-def build_scene(force=False):
-    src = os.path.join(CSRC, "rvk_scene.c")
-    out = os.path.join(LIB, "librvk_scene.so")
-    if force or _stale(out, [src]):
-        _run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", out, src,
-              "-lm"])
-    return out
-
-
 def build_dropin(force=False):
     """The C++ drop-in needs the reference's public headers (include/rvk/*.hpp)
     only at compile time; it is built where they are available."""
@@ -99,7 +89,7 @@ def build_cli(force=False):
 
 def build(force=False):
     os.makedirs(LIB, exist_ok=True)
-    return [build_gpu(force), build_probe(force), build_scene(force), build_dropin(force),
+    return [build_gpu(force), build_probe(force), build_dropin(force),
             build_cli(force)]
 
 

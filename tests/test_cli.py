@@ -67,7 +67,7 @@ def _read_est(path):
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["gpu", "lsq-only"])
 def test_cli_estimate_matches_reference_run_estimate(gpu_lib, reference, mode):
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     frames = []
     for k in range(4):
         w = W.automotive(seed=500 + k, n_clusters=25)

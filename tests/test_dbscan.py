@@ -120,7 +120,7 @@ def test_gpu_dbscan_edge_cases(gpu_lib, oracle):
 def test_gpu_dbscan_large_radar_frame(gpu_lib, reference):
     """A 20k-point radar frame from the reference's generate_frame."""
     import paper_2012_12618_b200 as rvk
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     w = W.imaging(seed=77, n_clusters=100, total=20000)
     x, y = w.x, w.y
     want = reference.dbscan(x, y, None, 2.0, 3, 0)
@@ -134,7 +134,7 @@ def test_gpu_estimate_frame_matches_reference_pipeline(gpu_lib, reference):
     (tools/rvk_main.cpp:128-141) on radar frames."""
     import paper_2012_12618_b200 as rvk
     from oracle.binding import make_params
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     for s in range(3):
         w = W.automotive(seed=300 + s, n_clusters=40)
         fr = rvk.Frame(frame_id=s, x=w.x, y=w.y, z=np.zeros(w.n_points), doppler=w.doppler,
@@ -185,7 +185,7 @@ def test_gpu_combine_masks_vs_oracle(gpu_lib, oracle):
         np.testing.assert_array_equal(rvk.combine_masks_labels(*args), oracle.combine_masks(*args),
                                       err_msg=f"case {k}")
     # frame-level: the masks of the device pipeline on a clustered frame
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     w = W.automotive(seed=5, n_clusters=30)
     fr = rvk.Frame(frame_id=0, x=w.x, y=w.y, doppler=w.doppler, azimuth=w.azimuth)
     labels, off, pi, res, _ = rvk.estimate_frame(fr, rvk.ClusteringParams(2.0, 3),

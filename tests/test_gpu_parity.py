@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2012_12618_b200 as rvk
-from paper_2012_12618_b200 import workloads as W
+from tools import workloads as W
 from conftest import EXTREME_PARAMS, ROOT, assert_estimates_close, extreme_value_clusters
 from oracle.binding import make_params
 
@@ -266,7 +266,7 @@ import hashlib, sys
 import numpy as np
 sys.path.insert(0, sys.argv[1])
 import paper_2012_12618_b200 as rvk
-from paper_2012_12618_b200 import workloads as W
+from tools import workloads as W
 h = hashlib.sha256()
 for w in (W.automotive(seed=77, n_clusters=40), W.imaging(seed=78, n_clusters=300, total=60_000)):
     r, e = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, rvk.RansacParams(512, 1.0, 5))

@@ -18,7 +18,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2012_12618_b200 import stream as S
-from paper_2012_12618_b200 import workloads as W
+from tools import workloads as W
 
 
 def _frames(n):

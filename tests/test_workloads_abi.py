@@ -1,7 +1,8 @@
 """CPU: workload generator pinned to the reference; C-ABI library surface.
 
-* csrc/rvk_scene.c == rvk::generate_frame (src/scene.cpp:105-189), bit-exact,
-  on the golden specs and (live) on the bench shapes.
+* tools/rvk_scene.c == rvk::generate_frame (src/scene.cpp:105-189), bit-exact,
+  on the golden specs and (live) on the bench shapes; the two generator
+  backends of tools/workloads.py give identical frames.
 * librvk_gpu.so loads without a GPU and exports every function declared in
   include/rvk_gpu.h; host-side validation (which runs before any CUDA call)
   returns the reference's status and messages.
@@ -21,7 +22,7 @@ from conftest import ROOT
 def test_scene_generator_matches_reference_golden(golden_scene):
     from conftest import _ensure_built
     _ensure_built()
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     for g in golden_scene:
         x, y, d, a, flag = W.generate(g["seed"], g["objects"])
         np.testing.assert_array_equal(x, g["x"])
@@ -32,7 +33,7 @@ def test_scene_generator_matches_reference_golden(golden_scene):
 
 
 def test_bench_workloads_match_reference_live(reference):
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     for w in (W.single_frame(), W.automotive(n_clusters=40)):
         objs = np.zeros((w.n_clusters, 10))
         # rebuild the spec the workload used and ask the reference for it
@@ -46,8 +47,28 @@ def test_bench_workloads_match_reference_live(reference):
         del objs
 
 
+def test_generator_backends_identical(reference):
+    """bench.py --impl reference draws its frames through oracle/_ref's
+    generate_frame + KeyedRng; our arm through tools/rvk_scene.c: the same
+    arrays for every config the reference can generate (config 3's 50%
+    outliers are beyond generate_frame's check, scene.cpp:39)."""
+    from tools import workloads as W
+    makers = [lambda: W.single_frame(seed=9), lambda: W.automotive(seed=4, n_clusters=30),
+              lambda: W.imaging(seed=4003, n_clusters=300, total=60_000)]
+    try:
+        for mk in makers:
+            W.set_generator("scene")
+            a = mk()
+            W.set_generator("reference")
+            b = mk()
+            for f in ("offsets", "azimuth", "doppler", "outlier", "truth_v"):
+                np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    finally:
+        W.set_generator("scene")
+
+
 def _spec_of(w):
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     if w.name == "single":
         vx, vy = W._velocities(w.meta["scene_seed"], w.n_clusters)
         objs = np.zeros((w.n_clusters, 10))
@@ -69,7 +90,7 @@ def _spec_of(w):
 def test_workload_shapes():
     from conftest import _ensure_built
     _ensure_built()
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     w1 = W.single_frame()
     assert w1.n_clusters == 8 and w1.n_points == 1024 and w1.evals == 262144
     w2 = W.automotive()

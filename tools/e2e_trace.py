@@ -4,7 +4,8 @@ import numpy as np, torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2012_12618_b200 as rvk
-from paper_2012_12618_b200 import _native, workloads as W, stream as S
+from paper_2012_12618_b200 import _native, stream as S
+from tools import workloads as W
 frames = [W.automotive(seed=1000 + i) for i in range(8)]
 off, az, dop, keys, _, _ = S.batch_frames(frames)
 pin = lambda a: torch.from_numpy(a).pin_memory()

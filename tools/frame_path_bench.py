@@ -16,7 +16,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2012_12618_b200 as rvk  # noqa: E402
-from paper_2012_12618_b200 import workloads as W  # noqa: E402
+from tools import workloads as W  # noqa: E402
 
 
 def timeit(f, reps):

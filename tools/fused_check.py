@@ -21,7 +21,7 @@ def child():
     import torch
     import bench
     import paper_2012_12618_b200 as rvk
-    from paper_2012_12618_b200 import workloads as W
+    from tools import workloads as W
     out = {}
     dev = torch.device("cuda", 0)
     cases = [("cfg1", [W.single_frame()], 256),

@@ -1,12 +1,21 @@
-"""Synthetic clustered radar frames of the BASELINE.json shapes.
+"""Synthetic clustered radar frames of the BASELINE.json shapes (bench and test
+infrastructure; not part of the product package).
 
-Points come from the host generator csrc/rvk_scene.c, a restatement of
-rvk::generate_frame (/root/reference/proj/src/scene.cpp:105-189): object
-points uniform in a box, azimuth = atan2(y, x), Doppler = radial projection
-+ sigma * N(0, 1), floor(f * n) outliers offset by +-U[2, 5] m/s. Clusters
-are taken from the truth table (one cluster per object, no DBSCAN), as
-src/bench.cpp:57-63 does. All layout/velocity draws use the reference's
+Points come from rvk::generate_frame (/root/reference/proj/src/scene.cpp:105-189):
+object points uniform in a box, azimuth = atan2(y, x), Doppler = radial
+projection + sigma * N(0, 1), floor(f * n) outliers offset by +-U[2, 5] m/s.
+Clusters are taken from the truth table (one cluster per object, no DBSCAN),
+as src/bench.cpp:57-63 does. All layout/velocity draws use the reference's
 KeyedRng, so a (config, seed) pair names a bit-identical frame everywhere.
+
+Two interchangeable generators (tests/test_workloads_abi.py pins them equal):
+  "scene"     tools/rvk_scene.c, a C restatement of generate_frame, built into
+              tools/_build/librvk_scene.so -- travels with the repo and allows
+              outlier_fraction 0.5 (config 3), which the reference rejects
+              (scene.cpp:39);
+  "reference" oracle/_ref/librvk_ref.so, the unmodified reference build
+              (bench.py --impl reference uses it, so that arm maps no repo
+              library besides the reference itself).
 
 Configs (BASELINE.json "configs"):
   1 single   8 objects x 128 pts, 20% outliers, T=256   (bench.cpp:38-51 lattice)
@@ -17,12 +26,63 @@ Configs (BASELINE.json "configs"):
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
+import os
+import subprocess
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _native as N
+HERE = os.path.dirname(os.path.abspath(__file__))
+SCENE_SRC = os.path.join(HERE, "rvk_scene.c")
+SCENE_SO = os.path.join(HERE, "_build", "librvk_scene.so")
+
+_lock = threading.Lock()
+_scene = None
+_generator = os.environ.get("RVK_WORKLOAD_GENERATOR", "scene")
+
+
+def build_scene(force: bool = False) -> str:
+    """gcc tools/rvk_scene.c -> tools/_build/librvk_scene.so (flags of the
+    reference build: no FMA contraction)."""
+    os.makedirs(os.path.dirname(SCENE_SO), exist_ok=True)
+    if force or not os.path.exists(SCENE_SO) or \
+            os.path.getmtime(SCENE_SO) < os.path.getmtime(SCENE_SRC):
+        r = subprocess.run(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fPIC", "-shared",
+                            "-o", SCENE_SO, SCENE_SRC, "-lm"], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("scene build failed: " + r.stderr[-3000:])
+    return SCENE_SO
+
+
+def _scene_lib():
+    global _scene
+    with _lock:
+        if _scene is None:
+            if not os.path.exists(SCENE_SO):
+                build_scene()
+            lib = C.CDLL(SCENE_SO)
+            lib.rvk_scene_generate.restype = C.c_int
+            lib.rvk_scene_generate.argtypes = [C.c_uint64, C.c_int32] + [C.c_void_p] + \
+                [C.c_double] * 2 + [C.c_void_p] * 5
+            lib.rvk_scene_rng_units.restype = None
+            lib.rvk_scene_rng_units.argtypes = [C.c_uint64] * 3 + [C.c_int64, C.c_void_p]
+            _scene = lib
+        return _scene
+
+
+def set_generator(name: str) -> None:
+    """"scene" (default) or "reference" (oracle/_ref's generate_frame)."""
+    global _generator
+    if name not in ("scene", "reference"):
+        raise ValueError(name)
+    _generator = name
+
+
+def generator() -> str:
+    return _generator
 
 
 @dataclass
@@ -55,21 +115,29 @@ class Workload:
 
 
 def rng_units(seed: int, hi: int, lo: int, n: int) -> np.ndarray:
+    """n draws of KeyedRng(seed, hi, lo).next_unit() (include/rvk/rng.hpp:40-41)."""
     out = np.zeros(n)
-    N.scene().rvk_scene_rng_units(seed & (2**64 - 1), hi, lo, n, out.ctypes.data)
+    if _generator == "reference":
+        from oracle.binding import Reference
+        Reference().rng_units(seed, hi, lo, out)
+    else:
+        _scene_lib().rvk_scene_rng_units(seed & (2**64 - 1), hi, lo, n, out.ctypes.data)
     return out
 
 
 def generate(seed: int, objects: np.ndarray, offset_range=(2.0, 5.0)):
-    """rvk_scene_generate: objects [k, 10] -> (x, y, doppler, azimuth, outlier_flag)."""
+    """generate_frame: objects [k, 10] -> (x, y, doppler, azimuth, outlier_flag)."""
     objects = np.ascontiguousarray(objects, dtype=np.float64).reshape(-1, 10)
+    if _generator == "reference":
+        from oracle.binding import Reference
+        return Reference().generate_frame(seed & (2**64 - 1), objects, offset_range)
     p = int(objects[:, 6].sum())
     x, y, d, a = (np.zeros(p) for _ in range(4))
     flag = np.zeros(p, np.int32)
-    st = N.scene().rvk_scene_generate(seed & (2**64 - 1), objects.shape[0], objects.ctypes.data,
-                                      offset_range[0], offset_range[1], x.ctypes.data,
-                                      y.ctypes.data, d.ctypes.data, a.ctypes.data,
-                                      flag.ctypes.data)
+    st = _scene_lib().rvk_scene_generate(seed & (2**64 - 1), objects.shape[0],
+                                         objects.ctypes.data, offset_range[0], offset_range[1],
+                                         x.ctypes.data, y.ctypes.data, d.ctypes.data,
+                                         a.ctypes.data, flag.ctypes.data)
     if st != 0:
         raise RuntimeError("rvk_scene_generate failed")
     return x, y, d, a, flag
