@@ -307,6 +307,16 @@ def test_randomised_sweep(gpu_lib):
     assert '"mismatches": 0' in r.stdout
 
 
+def test_randomised_sweep_stress(gpu_lib):
+    """The config-3 regime of tools/fuzz_parity.py: T in {2048, 4096},
+    threshold_scale 0.25, exactly 50% outliers, 64-2048-point clusters."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_parity.py"),
+                        "--frames", "60", "--seed", "22", "--stress"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert '"mismatches": 0' in r.stdout
+
+
 def test_edge_cases(gpu_lib, oracle):
     rng = np.random.default_rng(11)
     cases = []
@@ -484,7 +494,7 @@ def test_alternative_kernel_shapes_parity(gpu_lib, env):
         [sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
          os.path.join(ROOT, "tests", "test_gpu_parity.py"),
          "-k", "golden or c3 or config1 or full_size or edge or batch_composition or radar or "
-         "device_api or bench_batches"],
+         "device_api"],
         capture_output=True, text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout

@@ -23,13 +23,14 @@ from conftest import assert_estimates_close  # noqa: E402
 from oracle.binding import Oracle, make_params  # noqa: E402
 
 
-def cluster(rng, n):
-    kind = rng.integers(0, 5)
-    if kind == 0:  # a moving object + outliers
+def cluster(rng, n, stress=False):
+    kind = 0 if stress else rng.integers(0, 5)
+    if kind == 0:  # a moving object + outliers (stress: exactly 50%, micro-Doppler-like)
         th = rng.uniform(-1.2, 1.2) + rng.normal(0, rng.uniform(0.001, 0.3), n)
         v = rng.uniform(-30, 30, 2)
         d = v[0] * np.cos(th) + v[1] * np.sin(th) + rng.normal(0, 0.05, n)
-        out = rng.uniform(size=n) < rng.uniform(0, 0.5)
+        out = (rng.permutation(n) < n // 2) if stress else \
+            rng.uniform(size=n) < rng.uniform(0, 0.5)
         d[out] = rng.uniform(-40, 40, out.sum())
         return np.stack([th, d], 1)
     if kind == 1:  # uniform
@@ -49,18 +50,29 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=3000)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--stress", action="store_true",
+                    help="config-3 regime: T in {2048, 4096}, threshold_scale 0.25, "
+                         "50%% outliers, clusters of 64-2048 points")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     o = Oracle()
     t0 = time.time()
     n_clusters = n_points = 0
     for f in range(args.frames):
-        k = int(rng.integers(1, 13))
-        sizes = np.minimum(3000, np.maximum(3, (10 ** rng.uniform(0.5, 3.5, k)).astype(int)))
-        cl = [cluster(rng, int(s)) for s in sizes]
+        if args.stress:
+            k = int(rng.integers(1, 5))
+            sizes = np.rint(64 * 32 ** rng.uniform(size=k)).astype(int)
+            cl = [cluster(rng, int(s), stress=True) for s in sizes]
+            T = int(rng.choice([2048, 4096]))
+            scale = 0.25
+        else:
+            k = int(rng.integers(1, 13))
+            sizes = np.minimum(3000, np.maximum(3, (10 ** rng.uniform(0.5, 3.5, k)).astype(int)))
+            cl = [cluster(rng, int(s)) for s in sizes]
+            T = int(rng.choice([1, 7, 64, 256, 257, 1024, 1500, 2048, 4096]))
+            scale = float(10 ** rng.uniform(-3, 0.7))
         off, az, dop = rvk.clusters_to_csr(cl)
-        T = int(rng.choice([1, 7, 64, 256, 257, 1024, 1500]))
-        p = rvk.RansacParams(T, float(10 ** rng.uniform(-3, 0.7)), int(rng.integers(0, 2**63)))
+        p = rvk.RansacParams(T, scale, int(rng.integers(0, 2**63)))
         r, est = rvk.ransac_estimate_csr(off, az, dop, p, frame_id=f)
         ro = o.sequential_ransac(off, az, dop, make_params(p.max_trials, p.threshold_scale,
                                                            p.rng_seed))
