@@ -134,9 +134,28 @@ int rvk_ransac_estimate(int64_t frame_id, int32_t n_clusters, const int64_t* off
                         int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
                         rvk_estimate* out);
 
+/* rvk_ransac_estimate with the masks bit-packed (the
+ * InlierMask payload of include/rvk/types.hpp:50-55 at 1 bit per point):
+ * mask_bits[ceil(P/8)], point k of the CSR = bit (k & 7) of byte k >> 3
+ * (numpy.packbits(mask, bitorder="little")). The D2H of the mask is P/8
+ * bytes instead of P. Everything else as rvk_ransac_estimate. */
+int rvk_ransac_estimate_packed(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                               const double* azimuth, const double* doppler,
+                               const int32_t* cluster_ids, const rvk_ransac_params* params,
+                               const int32_t* rng_cluster_index, int32_t* inlier_count,
+                               int32_t* winning_trial, uint8_t* mask_bits, rvk_estimate* out);
+
 /* Device-pointer variant of rvk_ransac_estimate (all arrays in HBM, async on
  * `stream`, a cudaStream_t or NULL for the legacy default stream). The
- * caller must keep the inputs alive until the stream reaches this point. */
+ * caller must keep the inputs alive until the stream reaches this point.
+ * Preconditions (the offsets live in HBM, so they are not checked on the
+ * host): d_offsets[0] == 0, non-decreasing, d_offsets[n_clusters] ==
+ * n_points. A cluster with fewer than 3 points -- which the host API rejects
+ * with RVK_ECLUSTER_TOO_SMALL like the reference (src/ransac.cpp:147-156) --
+ * is never read: its outputs are a sentinel, inlier_count = winning_trial =
+ * -1, an all-zero mask and an estimate with v = 0, inlier_count 0,
+ * condition_ok 0 and no heading; every other cluster's outputs are
+ * unaffected. */
 int rvk_ransac_estimate_device(int64_t frame_id, int32_t n_clusters, int64_t n_points,
                                const int64_t* d_offsets, const double* d_azimuth,
                                const double* d_doppler, const int32_t* d_cluster_ids,
@@ -191,6 +210,14 @@ int rvk_stream_submit(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
                       const int32_t* cluster_ids, const int32_t* rng_cluster_index,
                       int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
                       rvk_estimate* out, int64_t* ticket);
+/* rvk_stream_submit with the mask delivered bit-packed (mask_bits[ceil(P/8)],
+ * layout of rvk_ransac_estimate_packed). */
+int rvk_stream_submit_packed(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
+                             const int64_t* offsets, const double* azimuth,
+                             const double* doppler, const int32_t* cluster_ids,
+                             const int32_t* rng_cluster_index, int32_t* inlier_count,
+                             int32_t* winning_trial, uint8_t* mask_bits, rvk_estimate* out,
+                             int64_t* ticket);
 int rvk_stream_wait(rvk_frame_stream* s, int64_t ticket);
 int rvk_stream_destroy(rvk_frame_stream* s);
 

@@ -64,6 +64,8 @@ GPU_SIGNATURES = {
     "rvk_run_ransac": (C.c_int, [_I32, _P, _P, _P, _P, _P, _I32, _P, _P, _P]),
     "rvk_estimate_all": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _P, _I32, _P]),
     "rvk_ransac_estimate": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "rvk_ransac_estimate_packed": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                             _P]),
     "rvk_ransac_estimate_device": (C.c_int, [_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                              _P, _P, _P]),
     "rvk_trial_counts": (C.c_int, [_I32, _P, _P, _P, _P, _P, _P]),
@@ -71,6 +73,8 @@ GPU_SIGNATURES = {
     "rvk_cluster_thresholds": (C.c_int, [_I32, _P, _P, _P, _F64, _P, _P]),
     "rvk_stream_create": (C.c_int, [_P, _I32, _P]),
     "rvk_stream_submit": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "rvk_stream_submit_packed": (C.c_int, [_P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                           _P]),
     "rvk_stream_wait": (C.c_int, [_P, _I64]),
     "rvk_stream_destroy": (C.c_int, [_P]),
     "rvk_dbscan": (C.c_int, [_I64, _P, _P, _P, _P, _P]),

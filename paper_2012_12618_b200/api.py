@@ -196,20 +196,22 @@ def run_ransac_csr(offsets, azimuth, doppler, params: RansacParams,
 
 
 def ransac_estimate_csr(offsets, azimuth, doppler, params: RansacParams, frame_id: int = 0,
-                        cluster_ids=None, rng_cluster_index=None):
-    """rvk_ransac_estimate: run_ransac + estimate_all in one device pass."""
+                        cluster_ids=None, rng_cluster_index=None, packed_mask: bool = False):
+    """rvk_ransac_estimate: run_ransac + estimate_all in one device pass.
+    packed_mask: the mask comes back as bits (rvk_ransac_estimate_packed,
+    uint8 [ceil(P/8)], numpy.packbits(mask, bitorder="little"))."""
     offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
     n = offsets.size - 1
     cnt = np.zeros(n, np.int32)
     tr = np.zeros(n, np.int32)
-    mask = np.zeros(azimuth.size, np.uint8)
+    mask = np.zeros((azimuth.size + 7) // 8 if packed_mask else azimuth.size, np.uint8)
     est = np.zeros(n, N.ESTIMATE_DTYPE)
     ids = _opt_i32(cluster_ids, n)
     keys = _opt_i32(rng_cluster_index, n)
     p = params.c()
-    _check(N.gpu().rvk_ransac_estimate(frame_id, n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
-                                       N.ptr(ids), C.addressof(p), N.ptr(keys), N.ptr(cnt),
-                                       N.ptr(tr), N.ptr(mask), N.ptr(est)))
+    fn = N.gpu().rvk_ransac_estimate_packed if packed_mask else N.gpu().rvk_ransac_estimate
+    _check(fn(frame_id, n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler), N.ptr(ids),
+              C.addressof(p), N.ptr(keys), N.ptr(cnt), N.ptr(tr), N.ptr(mask), N.ptr(est)))
     return RansacResult(cnt, tr, mask), est
 
 
@@ -298,19 +300,24 @@ class FrameStream:
         self._outs = {}
 
     def submit(self, offsets, azimuth, doppler, frame_id: int = 0, cluster_ids=None,
-               rng_cluster_index=None, out=None) -> int:
+               rng_cluster_index=None, out=None, packed_mask: bool = False) -> int:
+        """packed_mask: the mask is delivered as bits (rvk_stream_submit_packed);
+        `out`'s mask array then holds ceil(P/8) bytes."""
         offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
         n = offsets.size - 1
         if out is None:
+            P = int(offsets[-1])
             out = (np.zeros(n, np.int32), np.zeros(n, np.int32),
-                   np.zeros(int(offsets[-1]), np.uint8), np.zeros(n, N.ESTIMATE_DTYPE))
+                   np.zeros((P + 7) // 8 if packed_mask else P, np.uint8),
+                   np.zeros(n, N.ESTIMATE_DTYPE))
         cnt, tr, mask, est = out
         ids = _opt_i32(cluster_ids, n)
         keys = _opt_i32(rng_cluster_index, n)
         t = C.c_int64(-1)
-        _check(self._lib.rvk_stream_submit(self._h, frame_id, n, N.ptr(offsets), N.ptr(azimuth),
-                                           N.ptr(doppler), N.ptr(ids), N.ptr(keys), N.ptr(cnt),
-                                           N.ptr(tr), N.ptr(mask), N.ptr(est), C.byref(t)))
+        fn = self._lib.rvk_stream_submit_packed if packed_mask else self._lib.rvk_stream_submit
+        _check(fn(self._h, frame_id, n, N.ptr(offsets), N.ptr(azimuth), N.ptr(doppler),
+                  N.ptr(ids), N.ptr(keys), N.ptr(cnt), N.ptr(tr), N.ptr(mask), N.ptr(est),
+                  C.byref(t)))
         self._inputs[t.value] = (offsets, azimuth, doppler, ids, keys)
         self._outs[t.value] = out
         # tickets >= depth (<= 8) behind are complete: their inputs are free

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -128,11 +129,31 @@ struct Context {
   cudaStream_t copy = nullptr;
   cudaStream_t pipe[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> landed;  // per chunk: its H2D is done
+  cudaEvent_t joined = nullptr;     // the second compute stream's work is done
+  Context() = default;
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  // Runs at thread exit; errors are ignored (the runtime may already be
+  // shutting down when the main thread's contexts go).
+  ~Context() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return;
+    if (cur != device) cudaSetDevice(device);
+    for (DevBuf* b : {&db, &frame, &labels, &in, &out}) b->release();
+    for (HostBuf* b : {&stage_frame, &stage_in, &stage_out}) b->release();
+    for (auto& kv : ws) kv.second.release();
+    for (cudaEvent_t e : landed) cudaEventDestroy(e);
+    if (joined) cudaEventDestroy(joined);
+    for (cudaStream_t st : {stream, copy, pipe[0], pipe[1]})
+      if (st) cudaStreamDestroy(st);
+    if (cur != device) cudaSetDevice(cur);
+  }
   void ensure_pipe(int chunks) {
     if (!copy) {
       RVK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
       RVK_CUDA(cudaStreamCreateWithFlags(&pipe[0], cudaStreamNonBlocking));
       RVK_CUDA(cudaStreamCreateWithFlags(&pipe[1], cudaStreamNonBlocking));
+      RVK_CUDA(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming));
     }
     while (static_cast<int>(landed.size()) < chunks + 1) {
       cudaEvent_t e;
@@ -142,21 +163,40 @@ struct Context {
   }
 };
 
+// One context per (thread, device), created on the thread's first call on
+// that device and freed when the thread exits (thread_local map of owning
+// pointers): a thread that alternates devices keeps one context per device
+// instead of leaking a fresh one at every switch.
 Context& context() {
-  static std::mutex mu;
-  thread_local Context* ctx = nullptr;
+  thread_local std::unordered_map<int, std::unique_ptr<Context>> ctxs;
   int dev = 0;
   RVK_CUDA(cudaGetDevice(&dev));
-  if (ctx == nullptr || ctx->device != dev) {
-    std::lock_guard<std::mutex> lock(mu);
-    ctx = new Context();  // one per (thread, device); lives for the thread
-    ctx->device = dev;
-    RVK_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  std::unique_ptr<Context>& slot = ctxs[dev];
+  if (!slot) {
+    auto c = std::make_unique<Context>();
+    c->device = dev;
+    RVK_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    slot = std::move(c);
   }
-  return *ctx;
+  return *slot;
 }
 
+// Restores the calling thread's current device on scope exit (entry points
+// that switch to an object's device must not leave it switched).
+struct DeviceGuard {
+  int saved = -1;
+  explicit DeviceGuard(int dev) {
+    RVK_CUDA(cudaGetDevice(&saved));
+    if (saved != dev) RVK_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != saved) cudaSetDevice(saved);
+  }
+};
+
 size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+size_t packed_bytes(int64_t P) { return static_cast<size_t>((P + 7) / 8); }
 
 // Validation in the reference's order (src/ransac.cpp:140-154).
 int validate_params(const rvk_ransac_params* p, const char* who) {
@@ -280,15 +320,17 @@ Scratch scratch(Workspace& w, int32_t n_clusters, int64_t P, int32_t T) {
 
 void check_launch() { RVK_CUDA(cudaGetLastError()); }
 
-// Output block: count[C] | trial[C] | est[C] | mask[P], one D2H.
+// Output block: count[C] | trial[C] | est[C] | mask[P] | mask bits[ceil(P/8)],
+// one D2H.
 struct OutLayout {
-  size_t o_cnt, o_tr, o_est, o_mask, total;
+  size_t o_cnt, o_tr, o_est, o_mask, o_bits, total;
   OutLayout(int32_t C, int64_t P) {
     o_cnt = 0;
     o_tr = align_up(sizeof(int32_t) * C);
     o_est = align_up(o_tr + sizeof(int32_t) * C);
     o_mask = align_up(o_est + sizeof(rvk_estimate) * C);
-    total = align_up(o_mask + P);
+    o_bits = align_up(o_mask + P);
+    total = align_up(o_bits + packed_bytes(P));
   }
 };
 
@@ -387,7 +429,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
                          const double* az, const double* dop, const int32_t* ids,
                          const rvk_ransac_params* params, const int32_t* keys,
                          int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
-                         rvk_estimate* out, bool refit) {
+                         rvk_estimate* out, bool refit, bool packed = false) {
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   int st = validate_params(params, "run_ransac");
@@ -415,6 +457,7 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
 
   const bool pin_in = is_pinned(az) && is_pinned(dop);
   const bool pin_mask = is_pinned(mask);
+  const size_t mask_bytes = packed ? packed_bytes(P) : static_cast<size_t>(P);
   const int64_t max_n = max_cluster_size(n_clusters, offsets);
   const auto t1 = clk::now();
 
@@ -493,8 +536,9 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
     o.est = refit ? reinterpret_cast<rvk_estimate*>(dout + L.o_est) + c0 : nullptr;
     o.mask = reinterpret_cast<uint8_t*>(dout + L.o_mask) + p0;
     run_pipeline(f, *params, s, o, sc);
-    // per-chunk results back
-    if (mask) {
+    // per-chunk results back (a packed mask once every chunk is done, below:
+    // chunk boundaries are not byte-aligned in the bit array)
+    if (mask && !packed) {
       uint8_t* dst = pin_mask ? mask + p0 : reinterpret_cast<uint8_t*>(hout + L.o_mask) + p0;
       RVK_CUDA(cudaMemcpyAsync(dst, o.mask, np, cudaMemcpyDeviceToHost, sc));
     }
@@ -508,13 +552,23 @@ int ransac_estimate_host(int64_t frame_id, int32_t n_clusters, const int64_t* of
       RVK_CUDA(cudaMemcpyAsync(reinterpret_cast<rvk_estimate*>(hout + L.o_est) + c0, o.est,
                                sizeof(rvk_estimate) * nc, cudaMemcpyDeviceToHost, sc));
   }
+  if (mask && packed) {  // 1 bit per point: join the chunks, pack, one D2H
+    RVK_CUDA(cudaEventRecord(ctx.joined, ctx.pipe[1]));
+    RVK_CUDA(cudaStreamWaitEvent(ctx.pipe[0], ctx.joined, 0));
+    uint8_t* dbits = reinterpret_cast<uint8_t*>(dout + L.o_bits);
+    launch_pack_mask(reinterpret_cast<const uint8_t*>(dout + L.o_mask), P, dbits, ctx.pipe[0]);
+    check_launch();
+    uint8_t* dst = pin_mask ? mask : reinterpret_cast<uint8_t*>(hout + L.o_bits);
+    RVK_CUDA(cudaMemcpyAsync(dst, dbits, mask_bytes, cudaMemcpyDeviceToHost, ctx.pipe[0]));
+  }
   const auto t2 = clk::now();
   RVK_CUDA(cudaStreamSynchronize(ctx.pipe[0]));
   RVK_CUDA(cudaStreamSynchronize(ctx.pipe[1]));
   const auto t3 = clk::now();
   if (inlier_count) std::memcpy(inlier_count, hout + L.o_cnt, sizeof(int32_t) * n_clusters);
   if (winning_trial) std::memcpy(winning_trial, hout + L.o_tr, sizeof(int32_t) * n_clusters);
-  if (mask && !pin_mask) std::memcpy(mask, hout + L.o_mask, P);
+  if (mask && !pin_mask)
+    std::memcpy(mask, hout + (packed ? L.o_bits : L.o_mask), mask_bytes);
   if (out && refit) std::memcpy(out, hout + L.o_est, sizeof(rvk_estimate) * n_clusters);
   if (trace_on()) {
     const auto t4 = clk::now();
@@ -588,6 +642,7 @@ struct StreamSlot {
   uint8_t* mask = nullptr;
   rvk_estimate* est = nullptr;
   bool pin_mask = false;
+  bool packed = false;  // mask delivered as bits (ceil(P/8) bytes)
 };
 
 struct FrameStream {
@@ -607,19 +662,23 @@ struct FrameStream {
     if (s.cnt) std::memcpy(s.cnt, h + s.L.o_cnt, sizeof(int32_t) * s.C);
     if (s.tr) std::memcpy(s.tr, h + s.L.o_tr, sizeof(int32_t) * s.C);
     if (s.est) std::memcpy(s.est, h + s.L.o_est, sizeof(rvk_estimate) * s.C);
-    if (s.mask && !s.pin_mask) std::memcpy(s.mask, h + s.L.o_mask, s.P);
+    if (s.mask && !s.pin_mask) {
+      if (s.packed) std::memcpy(s.mask, h + s.L.o_bits, packed_bytes(s.P));
+      else std::memcpy(s.mask, h + s.L.o_mask, s.P);
+    }
     s.ticket = -1;
   }
 
   int submit(int64_t frame_id, int32_t n_clusters, const int64_t* offsets, const double* az,
              const double* dop, const int32_t* ids, const int32_t* keys, int32_t* cnt,
-             int32_t* tr, uint8_t* mask, rvk_estimate* est, int64_t* ticket) {
+             int32_t* tr, uint8_t* mask, rvk_estimate* est, int64_t* ticket,
+             bool packed = false) {
     int st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
     if (st != RVK_OK) return st;
     const int64_t P = n_clusters ? offsets[n_clusters] : 0;
     if ((az == nullptr || dop == nullptr) && P > 0)
       return fail(RVK_EINVAL, "run_ransac: null point arrays");
-    RVK_CUDA(cudaSetDevice(device));
+    DeviceGuard guard(device);
     const int64_t k = next;
     StreamSlot& s = slots[k % depth];
     const auto tw = std::chrono::steady_clock::now();
@@ -688,9 +747,17 @@ struct FrameStream {
     // when it is pinned
     if (cnt || tr || est)
       RVK_CUDA(cudaMemcpyAsync(hout, dout, s.L.o_mask, cudaMemcpyDeviceToHost, sc));
-    if (mask)
+    s.packed = packed;
+    if (mask && packed) {
+      uint8_t* dbits = reinterpret_cast<uint8_t*>(dout + s.L.o_bits);
+      launch_pack_mask(o.mask, P, dbits, sc);
+      check_launch();
+      RVK_CUDA(cudaMemcpyAsync(s.pin_mask ? static_cast<void*>(mask) : hout + s.L.o_bits,
+                               dbits, packed_bytes(P), cudaMemcpyDeviceToHost, sc));
+    } else if (mask) {
       RVK_CUDA(cudaMemcpyAsync(s.pin_mask ? static_cast<void*>(mask) : hout + s.L.o_mask,
                                o.mask, P, cudaMemcpyDeviceToHost, sc));
+    }
     RVK_CUDA(cudaEventRecord(s.done, sc));
     s.ticket = k;
     s.C = n_clusters;
@@ -704,7 +771,7 @@ struct FrameStream {
 
   int wait(int64_t ticket) {
     if (ticket < 0 || ticket >= next) return fail(RVK_EINVAL, "rvk_stream_wait: unknown ticket");
-    RVK_CUDA(cudaSetDevice(device));
+    DeviceGuard guard(device);
     StreamSlot& s = slots[ticket % depth];
     if (s.ticket == ticket) complete(s);
     return RVK_OK;  // older tickets were completed when their slot was reused
@@ -751,6 +818,18 @@ int rvk_ransac_estimate(int64_t frame_id, int32_t n_clusters, const int64_t* off
     return ransac_estimate_host(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
                                 params, rng_cluster_index, inlier_count, winning_trial, mask, out,
                                 true);
+  });
+}
+
+int rvk_ransac_estimate_packed(int64_t frame_id, int32_t n_clusters, const int64_t* offsets,
+                               const double* azimuth, const double* doppler,
+                               const int32_t* cluster_ids, const rvk_ransac_params* params,
+                               const int32_t* rng_cluster_index, int32_t* inlier_count,
+                               int32_t* winning_trial, uint8_t* mask_bits, rvk_estimate* out) {
+  return guarded([&]() -> int {
+    return ransac_estimate_host(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
+                                params, rng_cluster_index, inlier_count, winning_trial, mask_bits,
+                                out, true, true);
   });
 }
 
@@ -957,6 +1036,20 @@ int rvk_stream_submit(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
   });
 }
 
+int rvk_stream_submit_packed(rvk_frame_stream* s, int64_t frame_id, int32_t n_clusters,
+                             const int64_t* offsets, const double* azimuth,
+                             const double* doppler, const int32_t* cluster_ids,
+                             const int32_t* rng_cluster_index, int32_t* inlier_count,
+                             int32_t* winning_trial, uint8_t* mask_bits, rvk_estimate* out,
+                             int64_t* ticket) {
+  return guarded([&]() -> int {
+    if (s == nullptr) return fail(RVK_EINVAL, "rvk_stream_submit: null stream");
+    return s->impl.submit(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
+                          rng_cluster_index, inlier_count, winning_trial, mask_bits, out, ticket,
+                          true);
+  });
+}
+
 int rvk_stream_wait(rvk_frame_stream* s, int64_t ticket) {
   return guarded([&]() -> int {
     if (s == nullptr) return fail(RVK_EINVAL, "rvk_stream_wait: null stream");
@@ -969,8 +1062,8 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
     if (s == nullptr) return RVK_OK;
     FrameStream& fs = s->impl;
     int rc = RVK_OK;
+    DeviceGuard guard(fs.device);
     try {
-      RVK_CUDA(cudaSetDevice(fs.device));
       for (auto& sl : fs.slots) fs.complete(sl);
     } catch (const CudaError& e) {
       rc = fail(RVK_ECUDA, "CUDA error %s in %s", cudaGetErrorName(e.e), e.what);
@@ -980,8 +1073,7 @@ int rvk_stream_destroy(rvk_frame_stream* s) {
       if (sl.done) cudaEventDestroy(sl.done);
       sl.ws.release();
       for (DevBuf* b : {&sl.in, &sl.out}) b->release();
-      for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out})
-        if (b->p) cudaFreeHost(b->p);
+      for (HostBuf* b : {&sl.small_in, &sl.big_in, &sl.stage_out}) b->release();
     }
     if (fs.copy) cudaStreamDestroy(fs.copy);
     for (auto& c : fs.compute)

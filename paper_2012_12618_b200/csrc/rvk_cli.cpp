@@ -1,7 +1,7 @@
 // rvk_gpu -- the reference CLI's `estimate` command (tools/rvk_main.cpp:104-158)
 // on the B200 path, SURVEY.md 8(f) rows 1 and 4.
 //
-//   rvk_gpu estimate FRAMES.csv -o ESTIMATES.csv [--mode gpu|lsq-only]
+//   rvk_gpu estimate FRAMES.csv -o ESTIMATES.csv [--mode parallel|sequential|gpu|lsq-only]
 //           [--seed S] [--eps E] [--min-pts M] [--max-trials T]
 //           [--threshold-scale K] [--workers W (accepted, ignored)]
 //
@@ -148,7 +148,7 @@ void append_estimate(std::string& out, const rvk_estimate& e) {
 
 int usage(const char* msg) {
   std::cerr << "error: " << msg << "\n"
-            << "usage: rvk_gpu estimate FRAMES.csv -o ESTIMATES.csv [--mode gpu|lsq-only] "
+            << "usage: rvk_gpu estimate FRAMES.csv -o ESTIMATES.csv [--mode parallel|sequential|gpu|lsq-only] "
                "[--seed S] [--eps E] [--min-pts M] [--max-trials T] [--threshold-scale K] "
                "[--workers W]\n";
   return kExitUsage;
@@ -239,8 +239,12 @@ int main(int argc, char** argv) {
   }
   if (frames_path.empty() || out_path.empty()) return usage("frames file and -o are required");
   // tools/rvk_main.cpp:106-114
+  // the reference's modes (tools/rvk_main.cpp: parallel is its default,
+  // sequential its 1-core baseline) are accepted as aliases of the device
+  // path: their results are defined to be identical (ransac.hpp:124-125)
+  if (mode == "parallel" || mode == "sequential") mode = "gpu";
   if (mode != "gpu" && mode != "lsq-only") {
-    std::cerr << "error: mode must be gpu or lsq-only\n";
+    std::cerr << "error: mode must be parallel, sequential, gpu or lsq-only\n";
     return kExitUsage;
   }
   if (!(cp.eps > 0.0) || cp.min_pts < 1 || rp.max_trials < 1 || !(rp.threshold_scale > 0.0) ||

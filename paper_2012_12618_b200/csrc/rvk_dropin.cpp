@@ -21,10 +21,11 @@
 // reference's types and messages (std::invalid_argument,
 // rvk::ClusterTooSmall). `workers` is accepted and ignored.
 //
-// Link-time substitution: weaken those two symbols in the
-// reference's ransac.o / velocity.o (objcopy --weaken-symbol) and link this
-// library; every other reference symbol (primitives, sequential baselines,
-// gather, combine_masks) stays the reference's own.
+// Link-time substitution (oracle/Makefile `dropin`): make
+// the reference's definitions of these symbols file-local in its ransac.o /
+// velocity.o / clustering.o (objcopy --localize-symbol, one object at a time)
+// and link this library; every other reference symbol (primitives,
+// sequential baselines, gather) stays the reference's own.
 #include <rvk/clustering.hpp>
 #include <rvk/ransac.hpp>
 #include <rvk/types.hpp>

@@ -597,6 +597,7 @@ __device__ void prep_hyp_body(PrepShared& sm, int* tile_pos, int c,
                               double4* __restrict__ stat, float* __restrict__ hyp,
                               int32_t* __restrict__ upper, int4* __restrict__ tiles,
                               int32_t* __restrict__ tile_count, int64_t tile_cap) {
+  if (offsets[c + 1] - offsets[c] < 3) return;  // select writes the too-small sentinel
   prep_cluster(sm, c, offsets, az, dop, scale, xy64, xy32, stat, nullptr);
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
@@ -876,6 +877,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   WarpPrep& w = wp[threadIdx.x >> 5];
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
+  if (n < 3) return;  // select writes the too-small sentinel
   if (n > kWarpCap) {
     if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
     return;
@@ -1434,6 +1436,33 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
   }
 }
 
+// The device API does no host-side size check (its offsets live in HBM), so a
+// cluster below the reference's minimum (kMinClusterSize = 3,
+// include/rvk/types.hpp:20; the host API throws ClusterTooSmall first,
+// src/ransac.cpp:147-156) is never read: prep skips it and the select /
+// fused kernels write a sentinel -- inlier_count = winning_trial = -1, an
+// all-zero mask, a zero estimate with condition_ok = 0 and no heading.
+constexpr int kMinClusterPoints = 3;
+__device__ void write_too_small(int c, int n, int64_t frame_id, int cluster_id,
+                                int32_t* out_count, int32_t* out_trial, uint8_t* cmask,
+                                rvk_estimate* est, int tid, int nthreads) {
+  for (int k = tid; k < n; k += nthreads) cmask[k] = 0;
+  if (tid == 0) {
+    if (out_count) out_count[c] = -1;
+    if (out_trial) out_trial[c] = -1;
+    if (est) {
+      rvk_estimate e;
+      e.frame_id = frame_id;
+      e.cluster_id = cluster_id;
+      e.inlier_count = 0;
+      e.v_x = e.v_y = e.heading = 0.0;
+      e.has_heading = 0;
+      e.condition_ok = 0;
+      est[c] = e;
+    }
+  }
+}
+
 // Exact winner per cluster (one CTA). With U = the fast pass's upper bounds
 // (exact[t] <= U[t]), t0 = the lowest trial with the largest U and
 // E0 = exact[t0], a trial t can only beat or tie-win against t0 if
@@ -1457,6 +1486,11 @@ __device__ __forceinline__ void select_cluster(
   __shared__ int sh_need_exact;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
+  if (n < kMinClusterPoints) {
+    write_too_small(c, n, frame_id, cluster_ids ? cluster_ids[c] : c, out_count, out_trial,
+                    mask + b, est, threadIdx.x, blockDim.x);
+    return;
+  }
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double4 st = stat[c];
   double thr_lo = st.x, thr_hi = st.y;
@@ -1669,6 +1703,11 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   if (c >= n_clusters) return;
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
+  if (n < kMinClusterPoints) {
+    write_too_small(c, n, frame_id, cluster_ids ? cluster_ids[c] : c, out_count, out_trial,
+                    mask + b, est, lane, 32);
+    return;
+  }
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const double4 st = stat[c];
   double thr_lo = st.x, thr_hi = st.y;
@@ -2050,6 +2089,11 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     if (c >= n_clusters) break;
     const int64_t b = offsets[c];
     const int n = static_cast<int>(offsets[c + 1] - b);
+    if (n < kMinClusterPoints) {
+      write_too_small(c, n, frame_id, cluster_ids ? cluster_ids[c] : c, out_count, out_trial,
+                      mask + b, est, lane, 32);
+      continue;
+    }
     if (n > kFusedCap || !fused_T) {  // the CTA path takes it
       if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
       continue;
@@ -2304,6 +2348,24 @@ exact_counts_kernel(const int64_t* __restrict__ offsets, const int32_t* __restri
     const int e = warp_exact_count(H, n, xy32 + xy32_base(offsets, c), xy64 + b, th, th, &und);
     if ((threadIdx.x & 31) == 0) counts[static_cast<int64_t>(c) * T + t] = e;
   }
+}
+
+// One output byte per thread: 8 mask bytes (one 8-byte load when the run
+// is complete) -> 8 bits, LSB = the lowest point index.
+__global__ void __launch_bounds__(256)
+pack_mask_kernel(const uint8_t* __restrict__ mask, int64_t n_points, uint8_t* __restrict__ bits) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t k0 = i * 8;
+  if (k0 >= n_points) return;
+  uint32_t b = 0;
+  if (k0 + 8 <= n_points && (reinterpret_cast<uintptr_t>(mask + k0) & 7) == 0) {
+    const uint64_t v = *reinterpret_cast<const uint64_t*>(mask + k0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b |= ((v >> (8 * q)) & 1u) << q;
+  } else {
+    for (int q = 0; q < 8 && k0 + q < n_points; ++q) b |= (mask[k0 + q] & 1u) << q;
+  }
+  bits[i] = static_cast<uint8_t>(b);
 }
 
 __global__ void seed_pairs_kernel(const int64_t* __restrict__ offsets,
@@ -2567,6 +2629,13 @@ void launch_exact_counts(const FrameDev& f, const rvk_ransac_params& p, const Sc
   if (f.n_clusters == 0) return;
   exact_counts_kernel<<<f.n_clusters, kSelectThreads, 0, st>>>(
       f.offsets, f.keys, s.xy64, s.xy32, s.stat, p.max_trials, p.rng_seed, counts);
+  count_launch();
+}
+
+void launch_pack_mask(const uint8_t* mask, int64_t n_points, uint8_t* bits, cudaStream_t st) {
+  const int64_t nb = (n_points + 7) / 8;
+  if (nb == 0) return;
+  pack_mask_kernel<<<static_cast<unsigned>((nb + 255) / 256), 256, 0, st>>>(mask, n_points, bits);
   count_launch();
 }
 

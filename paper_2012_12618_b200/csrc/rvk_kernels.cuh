@@ -120,6 +120,8 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
 // optional LSQ refit + heading.
 void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                    const Outputs& o, cudaStream_t st);
+// mask[P] (0/1 bytes) -> bits[ceil(P/8)], point k = bit (k & 7) of byte k >> 3.
+void launch_pack_mask(const uint8_t* mask, int64_t n_points, uint8_t* bits, cudaStream_t st);
 // estimate_all on caller masks.
 void launch_refit(const FrameDev& f, const uint8_t* mask, rvk_estimate* est, cudaStream_t st);
 // Exact count of every (cluster, trial).

@@ -33,7 +33,7 @@ def test_cli_usage_errors():
         f = os.path.join(d, "f.csv")
         open(f, "w").write("frame_id,x,y,z,doppler,azimuth\n0,1,2,0,1,0.5\n")
         code, out = _run("estimate", f, "-o", os.path.join(d, "o.csv"), "--mode", "fast")
-        assert code == 2 and "mode must be gpu or lsq-only" in out
+        assert code == 2 and "mode must be parallel, sequential, gpu or lsq-only" in out
         code, out = _run("estimate", f, "-o", os.path.join(d, "o.csv"), "--eps", "0")
         assert code == 2 and "invalid estimation parameters" in out
 
@@ -65,7 +65,7 @@ def _read_est(path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["gpu", "lsq-only"])
+@pytest.mark.parametrize("mode", ["gpu", "parallel", "sequential", "lsq-only"])
 def test_cli_estimate_matches_reference_run_estimate(gpu_lib, reference, mode):
     from tools import workloads as W
     frames = []
@@ -79,7 +79,7 @@ def test_cli_estimate_matches_reference_run_estimate(gpu_lib, reference, mode):
         code, log = _run("estimate", fp, "-o", ours, "--mode", mode, "--seed", "7",
                          "--max-trials", "128")
         assert code == 0, log
-        reference.run_estimate_csv(fp, theirs, "parallel" if mode == "gpu" else "lsq-only",
+        reference.run_estimate_csv(fp, theirs, "lsq-only" if mode == "lsq-only" else "parallel",
                                    max_trials=128, seed=7)
         a, b = _read_est(ours), _read_est(theirs)
     assert len(a) == len(b) > 0

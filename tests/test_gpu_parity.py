@@ -498,3 +498,89 @@ def test_alternative_kernel_shapes_parity(gpu_lib, env):
         capture_output=True, text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_packed_masks(gpu_lib):
+    """rvk_ransac_estimate_packed / rvk_stream_submit_packed:
+    the bits are numpy.packbits(mask, bitorder="little") of the byte mask, every
+    other output identical; odd point counts, chunked host calls (> 2^18 points)
+    and single points past a byte boundary included."""
+    cases = [W.single_frame(), W.automotive(seed=3, n_clusters=40),
+             W.imaging(seed=5, n_clusters=1500, total=300_001)]
+    for w in cases:
+        p = rvk.RansacParams(w.max_trials, w.threshold_scale, 3)
+        r, e = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p)
+        rb, eb = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p, packed_mask=True)
+        assert rb.mask.size == (w.n_points + 7) // 8
+        np.testing.assert_array_equal(rb.mask, np.packbits(r.mask, bitorder="little"))
+        np.testing.assert_array_equal(rb.inlier_count, r.inlier_count)
+        np.testing.assert_array_equal(rb.winning_trial, r.winning_trial)
+        assert eb.tobytes() == e.tobytes()
+        with rvk.FrameStream(p, depth=2) as fs:
+            t1 = fs.submit(w.offsets, w.azimuth, w.doppler, packed_mask=True)
+            t2 = fs.submit(w.offsets, w.azimuth, w.doppler)
+            rs, es = fs.result(t1)
+            rs2, _ = fs.result(t2)
+        np.testing.assert_array_equal(rs.mask, rb.mask)
+        np.testing.assert_array_equal(rs2.mask, r.mask)
+        assert es.tobytes() == e.tobytes()
+
+
+@pytest.mark.parametrize("env", [{}, {"RVK_FUSED": "1"}, {"RVK_PREP_WARP": "0",
+                                                         "RVK_SELECT_WARP": "0"}],
+                         ids=["default", "fused", "cta"])
+def test_device_api_too_small_clusters(gpu_lib, env):
+    """rvk_ransac_estimate_device does no host-side size check: clusters of 0,
+    1 and 2 points get the sentinel (count = trial = -1, zero mask, zero
+    estimate) and never disturb their neighbours, whose outputs equal the
+    host API's on the valid clusters alone (same RNG keys)."""
+    r = subprocess.run([sys.executable, "-c", _TOO_SMALL_SCRIPT, ROOT], capture_output=True,
+                       text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "ok" in r.stdout
+
+
+_TOO_SMALL_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2012_12618_b200 as rvk
+from paper_2012_12618_b200 import _native
+rng = np.random.default_rng(5)
+sizes = np.array([40, 1, 0, 300, 2, 7, 600, 2, 3])
+off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+P = int(off[-1])
+az = rng.uniform(-1, 1, P); dop = rng.uniform(-5, 5, P)
+keys = np.arange(sizes.size, dtype=np.int32)
+p = rvk.RansacParams(200, 1.0, 9)
+dev = torch.device("cuda", 0)
+d = {k: torch.from_numpy(v).to(dev) for k, v in (("off", off), ("az", az), ("dop", dop), ("keys", keys))}
+C_ = sizes.size
+o = {"inlier_count": torch.full((C_,), 77, dtype=torch.int32, device=dev),
+     "winning_trial": torch.full((C_,), 77, dtype=torch.int32, device=dev),
+     "mask": torch.full((P,), 9, dtype=torch.uint8, device=dev),
+     "est": torch.full((C_ * 48,), 7, dtype=torch.uint8, device=dev)}
+rvk.ransac_estimate_device(d["off"], d["az"], d["dop"], p, o, rng_cluster_index=d["keys"])
+torch.cuda.synchronize()
+cnt = o["inlier_count"].cpu().numpy(); tr = o["winning_trial"].cpu().numpy()
+mask = o["mask"].cpu().numpy(); est = o["est"].cpu().numpy().view(_native.ESTIMATE_DTYPE)
+ok = sizes >= 3
+for c in np.nonzero(~ok)[0]:
+    assert cnt[c] == -1 and tr[c] == -1, (c, cnt[c], tr[c])
+    assert (mask[off[c]:off[c + 1]] == 0).all()
+    e = est[c]
+    assert e["inlier_count"] == 0 and e["v_x"] == 0 and e["v_y"] == 0
+    assert e["has_heading"] == 0 and e["condition_ok"] == 0 and e["cluster_id"] == c
+vc = np.nonzero(ok)[0]
+voff = np.concatenate([[0], np.cumsum(sizes[vc])]).astype(np.int64)
+vaz = np.concatenate([az[off[c]:off[c + 1]] for c in vc])
+vdop = np.concatenate([dop[off[c]:off[c + 1]] for c in vc])
+r, e = rvk.ransac_estimate_csr(voff, vaz, vdop, p, rng_cluster_index=keys[vc],
+                               cluster_ids=vc.astype(np.int32))
+np.testing.assert_array_equal(cnt[vc], r.inlier_count)
+np.testing.assert_array_equal(tr[vc], r.winning_trial)
+np.testing.assert_array_equal(np.concatenate([mask[off[c]:off[c + 1]] for c in vc]), r.mask)
+assert est[vc].tobytes() == e.tobytes()
+print("ok")
+"""
