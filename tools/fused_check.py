@@ -1,9 +1,9 @@
-"""Development check: the fused warp-per-cluster path against the unfused
-CTA/warp kernels on the same inputs (byte-identical outputs), plus a rough
-per-call timing of each. Runs itself twice in child processes (the path
-selection is read once per process).
+"""Development A/B check of a kernel-path switch: the same inputs through
+two settings of an environment variable (default RVK_FUSED=1 vs 0) must give
+byte-identical outputs; prints a rough per-call timing of each. Runs itself
+in child processes (path selections are read once per process).
 
-    python tools/fused_check.py
+    python tools/fused_check.py [--var RVK_FUSED] [--a 1] [--b 0]
 """
 import hashlib
 import json
@@ -65,21 +65,28 @@ def child():
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--var", default="RVK_FUSED")
+    ap.add_argument("--a", default="1")
+    ap.add_argument("--b", default="0")
+    args = ap.parse_args()
     res = {}
-    for fused in ("1", "0"):
+    for val, key in ((args.a, "1"), (args.b, "0")):
         r = subprocess.run([sys.executable, __file__, "--child"], capture_output=True, text=True,
-                           env=dict(os.environ, RVK_FUSED=fused), cwd=ROOT, timeout=900)
+                           env=dict(os.environ, **{args.var: val}), cwd=ROOT, timeout=900)
         if r.returncode != 0:
             print(r.stdout[-3000:], r.stderr[-3000:])
             sys.exit(1)
-        res[fused] = json.loads(r.stdout.strip().splitlines()[-1])
+        res[key] = json.loads(r.stdout.strip().splitlines()[-1])
     ok = True
     for name in res["1"]:
         a, b = res["1"][name], res["0"][name]
         same = a["dev"] == b["dev"] and a["host"] == b["host"] and a["dev"] == a["host"]
         ok &= same
-        print(f"{name:12s} identical={same} fused {a['ms']:.3f} ms ({a['evals'] / a['ms'] / 1e9:.2f}"
-              f" Tev/s)  unfused {b['ms']:.3f} ms ({b['evals'] / b['ms'] / 1e9:.2f} Tev/s)")
+        print(f"{name:12s} identical={same} {args.var}={args.a} {a['ms']:.3f} ms "
+              f"({a['evals'] / a['ms'] / 1e9:.2f} Tev/s)  {args.var}={args.b} {b['ms']:.3f} ms "
+              f"({b['evals'] / b['ms'] / 1e9:.2f} Tev/s)")
     sys.exit(0 if ok else 1)
 
 
