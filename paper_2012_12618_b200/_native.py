@@ -16,7 +16,8 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(PKG, "lib")
-GPU_SO = os.path.join(LIB_DIR, "librvk_gpu.so")
+# RVK_GPU_SO: an alternative in-tree build of the same library (A/B of kernel variants)
+GPU_SO = os.environ.get("RVK_GPU_SO") or os.path.join(LIB_DIR, "librvk_gpu.so")
 PROBE_SO = os.path.join(LIB_DIR, "librvk_probe.so")
 
 RVK_OK, RVK_EINVAL, RVK_ECLUSTER_TOO_SMALL, RVK_ECUDA, RVK_ENOMEM = range(5)

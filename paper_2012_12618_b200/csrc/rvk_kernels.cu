@@ -696,12 +696,18 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 // to a list for the CTA kernel.
 constexpr int kWarpCap = 512;
 constexpr int kWarpCand = 128;
-constexpr int kPrepWarps = 6;  // 6 x 7 KB of static shared memory per CTA
+constexpr int kPrepWarps = 4;  // 4 x 10 KB of static shared memory per CTA
 
+// One warp's cluster in shared memory: the raw azimuth/doppler are staged
+// here by the min/max pass (one global read per point), normalized in place,
+// and the hypotheses' seed points come from here (no global round trip).
 struct WarpPrep {
-  unsigned long long keys[kWarpCap];
-  unsigned long long cand[kWarpCand];
-  unsigned int hist[kWarpCap];
+  unsigned long long keys[kWarpCap];  // raw doppler bits, then |normalized doppler| bits
+  double xs[kWarpCap];                // raw azimuth, then normalized x
+  union {
+    unsigned int hist[kWarpCap];          // median buckets / radix counters
+    unsigned long long cand[kWarpCand];   // the median bucket's keys (after hist is read)
+  };
 };
 
 // Warp-wide (min, max, min, max) of non-NaN partials: plain compares (no
@@ -891,16 +897,21 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
   for (int k = lane; k < n; k += 32) {
     const double a = az[b + k], d = dop[b + k];
+    w.xs[k] = a;  // staged raw; the same lane normalizes it in place below
+    w.keys[k] = static_cast<unsigned long long>(__double_as_longlong(d));
     lo0 = a < lo0 ? a : lo0;
     hi0 = a > hi0 ? a : hi0;
     lo1 = d < lo1 ? d : lo1;
     hi1 = d > hi1 ? d : hi1;
   }
   warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
-  lo0 = warp_first_zero(lo0, az + b, n, lane);
-  hi0 = warp_first_zero(hi0, az + b, n, lane);
-  lo1 = warp_first_zero(lo1, dop + b, n, lane);
-  hi1 = warp_first_zero(hi1, dop + b, n, lane);
+  __syncwarp();  // the zeroed buckets before any lane's atomics
+  if (lo0 == 0.0 || hi0 == 0.0 || lo1 == 0.0 || hi1 == 0.0) {  // (rare) first +-0
+    lo0 = warp_first_zero(lo0, az + b, n, lane);
+    hi0 = warp_first_zero(hi0, az + b, n, lane);
+    lo1 = warp_first_zero(lo1, dop + b, n, lane);
+    hi1 = warp_first_zero(hi1, dop + b, n, lane);
+  }
   const double s0 = __dsub_rn(hi0, lo0);
   const double s1 = __dsub_rn(hi1, lo1);
   float2* p32 = xy32 + xy32_base(offsets, c);
@@ -913,8 +924,9 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   };
   for (int k0 = lane; k0 < n; k0 += 64) {  // two points per lane and step
     const int k1 = k0 + 32;
-    const double a0 = az[b + k0], d0 = dop[b + k0];
-    const double a1 = k1 < n ? az[b + k1] : 0.0, d1 = k1 < n ? dop[b + k1] : 0.0;
+    const double a0 = w.xs[k0], d0 = __longlong_as_double(static_cast<long long>(w.keys[k0]));
+    const double a1 = k1 < n ? w.xs[k1] : 0.0;
+    const double d1 = k1 < n ? __longlong_as_double(static_cast<long long>(w.keys[k1])) : 0.0;
     const double x0 = s0 == 0.0 ? 0.5 : norm_div(__dsub_rn(a0, lo0), s0, f0, r0);
     const double y0 = s1 == 0.0 ? 0.5 : norm_div(__dsub_rn(d0, lo1), s1, f1, r1);
     const double x1 = s0 == 0.0 ? 0.5 : norm_div(__dsub_rn(a1, lo0), s0, f0, r0);
@@ -924,6 +936,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const unsigned long long key0 =
         static_cast<unsigned long long>(__double_as_longlong(y0)) & ~(1ull << 63);
     w.keys[k0] = key0;
+    w.xs[k0] = x0;
     atomicAdd(&w.hist[med_bin(key0, nb)], 1u);
     if (k1 < n) {
       xy64[b + k1] = make_double2(x1, y1);
@@ -931,6 +944,7 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       const unsigned long long key1 =
           static_cast<unsigned long long>(__double_as_longlong(y1)) & ~(1ull << 63);
       w.keys[k1] = key1;
+      w.xs[k1] = x1;
       atomicAdd(&w.hist[med_bin(key1, nb)], 1u);
     }
   }
@@ -955,7 +969,6 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   // hypotheses (as prep_hyp_body, FFMA2 layout) and zeroed counters
   const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
   const uint64_t k1 = seed_key(key);
-  const double2* p64 = xy64 + b;  // written by this warp before __syncwarp
   float* hc = hyp + static_cast<int64_t>(c) * g.Tg * 32;
   int32_t* uc = upper + static_cast<int64_t>(c) * g.Tg * 8;
   // two trials per lane and step: both seed pairs' loads are in flight
@@ -966,10 +979,13 @@ prep_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     int i0 = 0, j0 = 0, i1 = 0, j1 = 0;
     if (a0) seed_pair_k(seed, k1, static_cast<uint32_t>(t0), static_cast<uint32_t>(n), i0, j0);
     if (a1) seed_pair_k(seed, k1, static_cast<uint32_t>(t1), static_cast<uint32_t>(n), i1, j1);
-    const double2 p0 = p64[i0], q0 = p64[j0], p1 = p64[i1], q1 = p64[j1];
-    const FastHyp f0 = a0 ? make_fast_from_seeds(p0.x, p0.y, q0.x, q0.y, thr_lo, thr_hi)
+    // seeds from the slot: x, and |y| (a -0.0 seed is +0.0 here: the same FP32 line)
+    auto ky = [&](int i) { return __longlong_as_double(static_cast<long long>(w.keys[i])); };
+    const FastHyp f0 = a0 ? make_fast_from_seeds(w.xs[i0], ky(i0), w.xs[j0], ky(j0), thr_lo,
+                                                 thr_hi)
                           : inert_fast();
-    const FastHyp f1 = a1 ? make_fast_from_seeds(p1.x, p1.y, q1.x, q1.y, thr_lo, thr_hi)
+    const FastHyp f1 = a1 ? make_fast_from_seeds(w.xs[i1], ky(i1), w.xs[j1], ky(j1), thr_lo,
+                                                 thr_hi)
                           : inert_fast();
     float* h = hc + (t0 >> 3) * 32 + (t0 & 7);
     h[0] = f0.A;
