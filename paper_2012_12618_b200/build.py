@@ -82,8 +82,8 @@ def build_cli(force=False):
     src = os.path.join(CSRC, "rvk_cli.cpp")
     out = os.path.join(LIB, "rvk_gpu")
     if force or _stale(out, [src, os.path.join(INCLUDE, "rvk_gpu.h")]):
-        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", INCLUDE, "-o", out, src,
-              "-L", LIB, "-lrvk_gpu", "-Wl,-rpath,$ORIGIN"])
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-pthread", "-I", INCLUDE, "-o",
+              out, src, "-L", LIB, "-lrvk_gpu", "-Wl,-rpath,$ORIGIN"])
     return out
 
 

@@ -14,6 +14,14 @@
 // for --mode lsq-only the all-true masks (src/ransac.cpp:244-256) through
 // rvk_estimate_all. A failing frame is reported on stderr and skipped
 // (tools/rvk_main.cpp:146-148). Exit codes: 0 ok, 2 usage / input, 3 runtime.
+//
+// Host side: the frame file is parsed by all hardware threads (the body is
+// split at line boundaries, each thread runs from_chars over its chunk; the
+// first malformed line in file order is reported, exactly as the sequential
+// reader would), then grouped into frames in first-appearance order; while
+// the device estimates frame k, a second host thread formats frame k-1's
+// estimate rows.
+#include <algorithm>
 #include <charconv>
 #include <cmath>
 #include <cstdint>
@@ -26,6 +34,7 @@
 #include <sstream>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -56,34 +65,29 @@ bool parse_int(std::string_view t, int64_t& v) {
   return r.ec == std::errc() && r.ptr == t.data() + t.size();
 }
 
-// read_frames (src/frame_io.cpp:86-139)
-std::vector<FrameSoA> read_frames(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw InputError{"cannot open for reading: " + path};
-  std::stringstream ss;
-  ss << in.rdbuf();
-  const std::string text = ss.str();
-  std::vector<FrameSoA> frames;
-  std::unordered_map<int64_t, std::size_t> slot;
-  std::size_t pos = 0, line_no = 0;
-  auto next_line = [&](std::string_view& line) {
-    if (pos >= text.size()) return false;
-    std::size_t e = text.find('\n', pos);
-    if (e == std::string::npos) e = text.size();
-    line = std::string_view(text).substr(pos, e - pos);
-    pos = e + 1;
-    ++line_no;
-    return true;
-  };
-  std::string_view line;
-  if (!next_line(line)) throw InputError{"empty frame file: " + path};
-  if (line != kFrameHeader)
-    throw InputError{"expected header '" + std::string(kFrameHeader) + "', got '" +
-                     std::string(line) + "'"};
-  auto bad = [&](const std::string& what) {
-    throw InputError{"malformed row at line " + std::to_string(line_no) + ": " + what};
-  };
-  while (next_line(line)) {
+// Rows of one chunk of the body, in file order.
+struct Rows {
+  std::vector<int64_t> fid;
+  std::vector<double> v;        // 5 per row: x, y, z, doppler, azimuth
+  std::size_t lines = 0;        // lines consumed (the chunk's own)
+  std::size_t bad_line = 0;     // 1-based within the chunk, 0 = none
+  std::string bad_what;
+};
+
+// One chunk [b, e) of the body (whole lines): the row checks of read_frames
+// (src/frame_io.cpp:100-132), stopping at the chunk's first malformed row.
+void parse_chunk(std::string_view text, std::size_t b, std::size_t e, Rows& out) {
+  std::size_t pos = b;
+  while (pos < e) {
+    std::size_t nl = text.find('\n', pos);
+    if (nl == std::string_view::npos || nl > e) nl = e;
+    const std::string_view line = text.substr(pos, nl - pos);
+    pos = nl + 1;
+    ++out.lines;
+    auto bad = [&](const std::string& what) {
+      out.bad_line = out.lines;
+      out.bad_what = what;
+    };
     std::string_view f[7];
     int nf = 0;
     std::size_t s = 0;
@@ -94,27 +98,82 @@ std::vector<FrameSoA> read_frames(const std::string& path) {
       if (c == std::string_view::npos) break;
       s = c + 1;
     }
-    if (nf != 6) bad("expected 6 fields");
+    if (nf != 6) return bad("expected 6 fields");
     int64_t fid = 0;
-    if (!parse_int(f[0], fid)) bad("bad frame_id '" + std::string(f[0]) + "'");
+    if (!parse_int(f[0], fid)) return bad("bad frame_id '" + std::string(f[0]) + "'");
     double v[5];
     static const char* names[5] = {"x", "y", "z", "doppler", "azimuth"};
     for (int k = 0; k < 5; ++k)
       if (!parse_double(f[k + 1], v[k]) || !std::isfinite(v[k]))
-        bad(std::string("bad ") + names[k] + " '" + std::string(f[k + 1]) + "'");
-    if (!(v[4] > -std::numbers::pi && v[4] <= std::numbers::pi)) bad("azimuth outside (-pi, pi]");
-    auto [it, inserted] = slot.try_emplace(fid, frames.size());
-    if (inserted) {
-      frames.emplace_back();
-      frames.back().frame_id = fid;
-    }
-    FrameSoA& fr = frames[it->second];
-    fr.x.push_back(v[0]);
-    fr.y.push_back(v[1]);
-    fr.z.push_back(v[2]);
-    fr.doppler.push_back(v[3]);
-    fr.azimuth.push_back(v[4]);
+        return bad(std::string("bad ") + names[k] + " '" + std::string(f[k + 1]) + "'");
+    if (!(v[4] > -std::numbers::pi && v[4] <= std::numbers::pi))
+      return bad("azimuth outside (-pi, pi]");
+    out.fid.push_back(fid);
+    out.v.insert(out.v.end(), v, v + 5);
   }
+}
+
+// read_frames (src/frame_io.cpp:86-139), parsed by `threads` threads.
+std::vector<FrameSoA> read_frames(const std::string& path, unsigned threads) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw InputError{"cannot open for reading: " + path};
+  std::stringstream ss;
+  ss << in.rdbuf();
+  const std::string text_s = ss.str();
+  const std::string_view text(text_s);
+  if (text.empty()) throw InputError{"empty frame file: " + path};
+  std::size_t hdr_end = text.find('\n');
+  if (hdr_end == std::string_view::npos) hdr_end = text.size();
+  const std::string_view header = text.substr(0, hdr_end);
+  if (header != kFrameHeader)
+    throw InputError{"expected header '" + std::string(kFrameHeader) + "', got '" +
+                     std::string(header) + "'"};
+  // body [b0, end): chunks of whole lines (the reader's lines end at '\n'; a
+  // final line without one is a line too)
+  const std::size_t b0 = std::min(hdr_end + 1, text.size());
+  std::size_t end = text.size();
+  const std::size_t body = end - b0;
+  threads = std::max(1u, std::min<unsigned>(threads, static_cast<unsigned>(body / (1 << 16) + 1)));
+  std::vector<std::size_t> cut{b0};
+  for (unsigned t = 1; t < threads; ++t) {
+    std::size_t c = b0 + body * t / threads;
+    c = text.find('\n', std::max(c, cut.back()));
+    c = c == std::string_view::npos ? end : c + 1;
+    cut.push_back(std::max(c, cut.back()));
+  }
+  cut.push_back(end);
+  std::vector<Rows> rows(threads);
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < threads; ++t)
+    pool.emplace_back(parse_chunk, text, cut[t], cut[t + 1], std::ref(rows[t]));
+  parse_chunk(text, cut[0], cut[1], rows[0]);
+  for (auto& th : pool) th.join();
+  // the first malformed row in file order
+  std::size_t line_base = 1;  // the header
+  for (const Rows& r : rows) {
+    if (r.bad_line)
+      throw InputError{"malformed row at line " + std::to_string(line_base + r.bad_line) + ": " +
+                       r.bad_what};
+    line_base += r.lines;
+  }
+  // group by frame_id, frames in first-appearance order, rows in file order
+  std::vector<FrameSoA> frames;
+  std::unordered_map<int64_t, std::size_t> slot;
+  for (const Rows& r : rows)
+    for (std::size_t k = 0; k < r.fid.size(); ++k) {
+      auto [it, inserted] = slot.try_emplace(r.fid[k], frames.size());
+      if (inserted) {
+        frames.emplace_back();
+        frames.back().frame_id = r.fid[k];
+      }
+      FrameSoA& fr = frames[it->second];
+      const double* v = &r.v[5 * k];
+      fr.x.push_back(v[0]);
+      fr.y.push_back(v[1]);
+      fr.z.push_back(v[2]);
+      fr.doppler.push_back(v[3]);
+      fr.azimuth.push_back(v[4]);
+    }
   return frames;
 }
 
@@ -254,20 +313,28 @@ int main(int argc, char** argv) {
   }
   std::vector<FrameSoA> frames;
   try {
-    frames = read_frames(frames_path);
+    frames = read_frames(frames_path, std::max(1u, std::thread::hardware_concurrency()));
   } catch (const InputError& e) {
     std::cerr << "error: " << e.what << '\n';
     return kExitUsage;
   }
-  std::vector<rvk_estimate> all;
-  for (const FrameSoA& f : frames) {
-    std::string err;
-    if (!estimate_one(f, mode, cp, rp, all, err))
-      std::cerr << "frame " << f.frame_id << ": " << err << '\n';
-  }
   std::string text(kEstimateHeader);
   text.push_back('\n');
-  for (const rvk_estimate& e : all) append_estimate(text, e);
+  // device work of frame k on this thread, formatting of frame k-1 on another
+  std::vector<rvk_estimate> cur, prev;
+  std::thread fmt;
+  for (const FrameSoA& f : frames) {
+    std::string err;
+    cur.clear();
+    if (!estimate_one(f, mode, cp, rp, cur, err))
+      std::cerr << "frame " << f.frame_id << ": " << err << '\n';
+    if (fmt.joinable()) fmt.join();
+    std::swap(cur, prev);
+    fmt = std::thread([&text, &prev] {
+      for (const rvk_estimate& e : prev) append_estimate(text, e);
+    });
+  }
+  if (fmt.joinable()) fmt.join();
   std::ofstream out(out_path, std::ios::binary | std::ios::trunc);
   if (!out) {
     std::cerr << "error: cannot open for writing: " << out_path << '\n';

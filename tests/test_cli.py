@@ -91,3 +91,23 @@ def test_cli_estimate_matches_reference_run_estimate(gpu_lib, reference, mode):
         assert math.isnan(ha) == math.isnan(hb)
         if not math.isnan(hb):
             assert abs((ha - hb + 180.0) % 360.0 - 180.0) <= math.degrees(1e-3)
+
+
+def test_cli_parallel_parse_reports_first_bad_line():
+    """The frame file is parsed by all host threads in line-aligned chunks;
+    the reported error must still be the first malformed row in file order
+    (src/frame_io.cpp:100-132), wherever the chunk boundaries fall."""
+    rng = np.random.default_rng(4)
+    n = 60_000
+    rows = [f"{i % 7},{x:.6f},{y:.6f},0,{d:.6f},{a:.6f}" for i, (x, y, d, a) in
+            enumerate(zip(rng.uniform(-50, 50, n), rng.uniform(-50, 50, n),
+                          rng.uniform(-9, 9, n), rng.uniform(-3, 3, n)))]
+    rows[41_234] = "3,1.0,2.0,0,zz,0.5"          # line 41236 (header = line 1)
+    rows[52_000] = "3,1.0,2.0"                   # a later error in another chunk
+    rows[59_000] = "4,1.0,2.0,0,1.0,9.0"
+    with tempfile.TemporaryDirectory() as d:
+        f = os.path.join(d, "f.csv")
+        open(f, "w").write("frame_id,x,y,z,doppler,azimuth\n" + "\n".join(rows) + "\n")
+        code, out = _run("estimate", f, "-o", os.path.join(d, "o.csv"))
+        assert code == 2, out
+        assert "malformed row at line 41236: bad doppler 'zz'" in out, out

@@ -424,6 +424,25 @@ def test_reference_acceptance_against_dropin(gpu_lib):
         assert f"[ACCEPTANCE] {crit}" in log and ": PASS" in log
 
 
+def test_reference_bench_harness_gpu_arm(gpu_lib, tmp_path):
+    """The reference's own bench harness (src/bench.cpp run_bench, compiled
+    unmodified) linked against the drop-in: its parallel_* columns time the
+    sm_100a path, the sequential_* columns the reference's 1-core CPU
+    baselines -- the GPU arm of `rvk bench`."""
+    out = tmp_path / "bench.csv"
+    code, log = _run_binary("rvk_dropin_bench", ["--grid", "default", "--reps", "5",
+                                                 "--warmups", "2", "-o", str(out)])
+    assert code == 0, log[-4000:]
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == ("n_clusters,points_per_cluster,parallel_ransac_ms,sequential_ransac_ms,"
+                        "parallel_lsq_ms,sequential_lsq_ms")
+    rows = [list(map(float, ln.split(","))) for ln in lines[1:]]
+    assert [(int(r[0]), int(r[1])) for r in rows] == [(c, p) for c in (8, 16, 32, 64)
+                                                      for p in (100, 150)]
+    assert all(np.isfinite(r[2:]).all() and min(r[2:]) > 0 for r in rows)
+    print(log)
+
+
 @pytest.mark.parametrize("depth", [1, 2, 3])
 def test_frame_stream_matches_host_api(gpu_lib, depth):
     """rvk_stream_*: pipelined frames give the same bytes as one-shot calls,
