@@ -16,8 +16,11 @@ Frames are independent and the RNG is keyed on the frame-local cluster index
   ``depth`` batches in flight, so the H2D of batch k+1 overlaps the kernels
   of batch k.
 * ``gather_to_root(results)``   -- the only cross-rank step: a host gather of
-  the per-frame results to rank 0, in frame order (torch.distributed
-  ``gather_object``; gloo or NCCL process group).
+  the per-frame results to rank 0, in frame order; each rank sends one flat
+  byte image (fixed-layout arrays, masks bit-packed; no pickling) through
+  ``torch.distributed.gather`` (gloo: host tensors; NCCL: device tensors).
+  Single-process multi-GPU streams gather into one pinned frame-indexed store
+  instead (tools/stream_bench.py).
 """
 from __future__ import annotations
 
@@ -112,17 +115,73 @@ def estimate_stream(frames: Sequence, params, frame_ids: Optional[Sequence[int]]
     return out
 
 
+_HDR = np.dtype([("frame", "<i8"), ("C", "<i4"), ("P", "<i4")])
+
+
+def pack_results(results: List[FrameResult]) -> np.ndarray:
+    """Flat uint8 image of a rank's results (no pickling): [n][headers]
+    [counts][trials][estimates][masks, 1 bit per point]."""
+    from ._native import ESTIMATE_DTYPE
+    hdr = np.zeros(len(results), _HDR)
+    for k, r in enumerate(results):
+        hdr[k] = (r.frame, r.inlier_count.size, r.mask.size)
+    parts = [np.array([len(results)], "<i8").view(np.uint8), hdr.view(np.uint8)]
+    parts += [np.ascontiguousarray(r.inlier_count, "<i4").view(np.uint8) for r in results]
+    parts += [np.ascontiguousarray(r.winning_trial, "<i4").view(np.uint8) for r in results]
+    parts += [np.ascontiguousarray(r.estimates, ESTIMATE_DTYPE).view(np.uint8) for r in results]
+    parts += [np.packbits(np.asarray(r.mask, np.uint8) != 0, bitorder="little") for r in results]
+    return np.concatenate(parts) if parts else np.zeros(0, np.uint8)
+
+
+def unpack_results(buf: np.ndarray) -> List[FrameResult]:
+    from ._native import ESTIMATE_DTYPE
+    n = int(buf[:8].view("<i8")[0])
+    pos = 8
+    hdr = buf[pos:pos + n * _HDR.itemsize].view(_HDR)
+    pos += n * _HDR.itemsize
+
+    def take(nbytes):
+        nonlocal pos
+        a = buf[pos:pos + nbytes]
+        pos += nbytes
+        return a
+    cnt = [take(4 * int(h["C"])).view("<i4").copy() for h in hdr]
+    tr = [take(4 * int(h["C"])).view("<i4").copy() for h in hdr]
+    est = [take(ESTIMATE_DTYPE.itemsize * int(h["C"])).view(ESTIMATE_DTYPE).copy() for h in hdr]
+    masks = [np.unpackbits(take((int(h["P"]) + 7) // 8), count=int(h["P"]),
+                           bitorder="little") for h in hdr]
+    return [FrameResult(int(h["frame"]), cnt[k], tr[k], masks[k], est[k])
+            for k, h in enumerate(hdr)]
+
+
 def gather_to_root(results: List[FrameResult], group=None) -> Optional[List[FrameResult]]:
     """Host gather of every rank's results to rank 0, ordered by frame index
-    (None on the other ranks). Single-process runs return the input sorted."""
+    (None on the other ranks). Each rank's results travel as one flat byte
+    image (pack_results: fixed-layout arrays, masks bit-packed -- no object
+    pickling) through torch.distributed.gather: CPU tensors over gloo, device
+    tensors over NCCL (NVLink/NVSwitch to GPU 0, then one D2H). Single-process
+    runs return the input sorted."""
+    import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return sorted(results, key=lambda r: r.frame)
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    bucket = [None] * world if rank == 0 else None
-    dist.gather_object(results, bucket, dst=0, group=group)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    img = pack_results(results)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([img.size], dtype=torch.int64, device=dev), group=group)
+    sizes = [int(x.item()) for x in sizes]
+    cap = max(sizes)
+    mine = torch.zeros(cap, dtype=torch.uint8, device=dev)
+    mine[:img.size] = torch.from_numpy(img).to(dev)
+    bucket = [torch.empty(cap, dtype=torch.uint8, device=dev) for _ in range(world)] \
+        if rank == 0 else None
+    dist.gather(mine, bucket, dst=0, group=group)
     if rank != 0:
         return None
-    merged = [r for part in bucket for r in part]
+    merged = []
+    for b, n in zip(bucket, sizes):
+        merged += unpack_results(b[:n].cpu().numpy())
     return sorted(merged, key=lambda r: r.frame)

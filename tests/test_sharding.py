@@ -128,3 +128,26 @@ def test_device_stream_matches_per_frame_calls(gpu_lib):
         np.testing.assert_array_equal(r.winning_trial, one.winning_trial)
         for f in ("v_x", "v_y", "heading", "inlier_count", "condition_ok"):
             np.testing.assert_array_equal(r.estimates[f], est[f])
+
+
+def test_result_image_round_trip():
+    """pack_results / unpack_results (the gather's wire format): every field
+    back bit for bit, masks through the 1-bit packing, empty frames too."""
+    from paper_2012_12618_b200 import _native
+    rng = np.random.default_rng(2)
+    res = []
+    for f, (C_, P_) in enumerate([(3, 17), (0, 0), (5, 64), (1, 3)]):
+        est = np.zeros(C_, _native.ESTIMATE_DTYPE)
+        est["v_x"] = rng.normal(size=C_)
+        est["cluster_id"] = np.arange(C_)
+        res.append(S.FrameResult(10 + f, rng.integers(0, 99, C_).astype(np.int32),
+                                 rng.integers(0, 99, C_).astype(np.int32),
+                                 (rng.uniform(size=P_) < 0.5).astype(np.uint8), est))
+    back = S.unpack_results(S.pack_results(res))
+    assert len(back) == len(res)
+    for a, b in zip(res, back):
+        assert a.frame == b.frame
+        np.testing.assert_array_equal(a.inlier_count, b.inlier_count)
+        np.testing.assert_array_equal(a.winning_trial, b.winning_trial)
+        np.testing.assert_array_equal(a.mask, b.mask)
+        assert a.estimates.tobytes() == b.estimates.tobytes()
