@@ -18,9 +18,10 @@
 // Host side: the frame file is parsed by all hardware threads (the body is
 // split at line boundaries, each thread runs from_chars over its chunk; the
 // first malformed line in file order is reported, exactly as the sequential
-// reader would), then grouped into frames in first-appearance order; while
-// the device estimates frame k, a second host thread formats frame k-1's
-// estimate rows.
+// reader would), then grouped into frames in first-appearance order; frames
+// then run on three host threads, each with its own device context and
+// stream, so consecutive frames overlap on the device; rows are written in
+// frame order.
 #include <algorithm>
 #include <charconv>
 #include <cmath>
@@ -318,23 +319,29 @@ int main(int argc, char** argv) {
     std::cerr << "error: " << e.what << '\n';
     return kExitUsage;
   }
+  // Frames are dealt round-robin to kFrameWorkers host threads; each thread
+  // has its own device context and stream (rvk_gpu.h: one per thread and
+  // device), so frame k+1's copies and clustering overlap frame k's RANSAC on
+  // the device. Results, errors and output rows stay in frame order.
+  constexpr std::size_t kFrameWorkers = 3;
+  const std::size_t nf = frames.size();
+  std::vector<std::vector<rvk_estimate>> results(nf);
+  std::vector<std::string> errors(nf);
+  std::vector<char> ok(nf, 0);
+  std::vector<std::thread> workers_t;
+  const std::size_t nw = std::min(kFrameWorkers, std::max<std::size_t>(nf, 1));
+  for (std::size_t w = 0; w < nw; ++w)
+    workers_t.emplace_back([&, w] {
+      for (std::size_t k = w; k < nf; k += nw)
+        ok[k] = estimate_one(frames[k], mode, cp, rp, results[k], errors[k]) ? 1 : 0;
+    });
+  for (auto& t : workers_t) t.join();
   std::string text(kEstimateHeader);
   text.push_back('\n');
-  // device work of frame k on this thread, formatting of frame k-1 on another
-  std::vector<rvk_estimate> cur, prev;
-  std::thread fmt;
-  for (const FrameSoA& f : frames) {
-    std::string err;
-    cur.clear();
-    if (!estimate_one(f, mode, cp, rp, cur, err))
-      std::cerr << "frame " << f.frame_id << ": " << err << '\n';
-    if (fmt.joinable()) fmt.join();
-    std::swap(cur, prev);
-    fmt = std::thread([&text, &prev] {
-      for (const rvk_estimate& e : prev) append_estimate(text, e);
-    });
+  for (std::size_t k = 0; k < nf; ++k) {
+    if (!ok[k]) std::cerr << "frame " << frames[k].frame_id << ": " << errors[k] << '\n';
+    for (const rvk_estimate& e : results[k]) append_estimate(text, e);
   }
-  if (fmt.joinable()) fmt.join();
   std::ofstream out(out_path, std::ios::binary | std::ios::trunc);
   if (!out) {
     std::cerr << "error: cannot open for writing: " << out_path << '\n';
