@@ -607,16 +607,21 @@ def main():
         evals_all, clusters_all = float(evals), float(clusters)
 
     # ---- rooflines. Stage ids (rvk_profile_read): 0 = prep (normalize,
-    # median, MAD, hypotheses: the ingest), 2 = score, 3 = select + refit.
-    score_ms = stage_ms[2] / max(1, stage_n[2])
-    evals_per_launch = iso_evals / max(1, stage_n[2])
+    # median, MAD, hypotheses: the ingest), 1 = the fused warp-per-cluster
+    # kernel (calls of at most one imaging frame, e.g. config 1), 2 = score,
+    # 3 = select + refit.
+    fused = stage_n[1] > 0 and stage_ms[1] > stage_ms[2]
+    sc = 1 if fused else 2
+    score_ms = stage_ms[sc] / max(1, stage_n[sc])
+    evals_per_launch = iso_evals / max(1, stage_n[sc])
     achieved = evals_per_launch * FLOP_PER_EVAL / (score_ms / 1e3) / 1e12
     clk = clk.summary()
     sm_max = clk.get("sm_max_mhz") or 1965
     nominal = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
     cap = load_capture(args.config, w0.max_trials) or {}
     total_ms = sum(stage_ms)
-    roofline = {"bound": "fp32", "kernel": "score_kernel", "achieved": achieved, "peak": peak,
+    roofline = {"bound": "fp32", "kernel": "fused_warp_kernel (whole path, scoring inside)"
+                if fused else "score_kernel", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "in-run FP32 FMA-pipe probe (max of FFMA2 %.1f / FFMA %.1f "
                                "TFLOP/s); MEASURED_PEAKS.json has no FP32 entry"
@@ -626,8 +631,9 @@ def main():
                 "avg_launch_ms": score_ms,
                 "traffic": cap.get("score", {}).get("dram_bytes"),
                 "traffic_source": cap.get("source"),
-                "share_of_step": stage_ms[2] / total_ms if total_ms else None,
+                "share_of_step": stage_ms[sc] / total_ms if total_ms else None,
                 "stage_ms_per_step": {"prep_ingest": stage_ms[0] / n_iso,
+                                      "fused": stage_ms[1] / n_iso,
                                       "score": stage_ms[2] / n_iso,
                                       "select_refit": stage_ms[3] / n_iso},
                 "measured": "isolated single-stream pass (%d steps) right after the timed "
@@ -644,7 +650,7 @@ def main():
                 "bytes_model": f"{b_pt:g} B/point + {b_cl} B/cluster (SURVEY.md 8(d))",
                 "avg_ms_per_step": ms,
                 "traffic": cap.get(ncu_key, {}).get("dram_bytes")}
-    roofline["hbm"] = {
+    roofline["hbm"] = None if fused else {
         "ingest": hbm_line("prep kernels (normalize, median, MAD, hypotheses)", 0,
                            INGEST_B_PT, INGEST_B_CL, "prep"),
         "refit": hbm_line("select kernel (exact winner, mask, LSQ refit + heading)", 3,

@@ -2467,16 +2467,22 @@ int sm_count() {
   return v;
 }
 
-// The fused warp-per-cluster kernel (RVK_FUSED=1; off by default): it
-// removes every intermediate HBM round trip but measured slower on B200 than
-// the three-kernel pipeline -- config 4, 4 frames: 0.42 vs 0.35 ms -- because
+// The fused warp-per-cluster kernel removes every intermediate HBM round
+// trip and two launches, but on full batches it is slower on B200 than the
+// three-kernel pipeline -- config 4, 4 frames: 0.42 vs 0.35 ms -- because
 // warps in different phases of the ~7.5k-instruction kernel thrash the
 // instruction cache (ncu: stall_no_instruction is its top stall reason, 3.0
-// cycles per issue; profiles/r2_fused_summary.md).
+// cycles per issue; profiles/r2_fused_summary.md). For a call of at most one
+// imaging frame of small clusters the single launch wins (config 4, one
+// frame: 0.135 vs 0.147 ms; config 1: 0.034 vs 0.037 ms), so it is chosen
+// for those; RVK_FUSED=1/0 forces it on/off.
+constexpr int kFusedAutoMaxClusters = 6144;
 bool fused_path(const FrameDev& f, const rvk_ransac_params& p) {
   if (f.n_clusters == 0 || p.max_trials > kFusedMaxT) return false;
-  static const int forced = env_int("RVK_FUSED", 0);
-  return forced != 0;
+  static const int forced = env_int("RVK_FUSED", -1);
+  if (forced >= 0) return forced != 0;
+  const int64_t avg = f.n_points / f.n_clusters;
+  return avg < 384 && f.n_clusters <= kFusedAutoMaxClusters;
 }
 
 // Whether the CTA path has clusters to take after the fused kernel: unknown

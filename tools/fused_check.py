@@ -25,6 +25,8 @@ def child():
     out = {}
     dev = torch.device("cuda", 0)
     cases = [("cfg1", [W.single_frame()], 256),
+             ("cfg4_1frame", bench.make_frames(4, range(1)), 256),
+             ("cfg2_1frame", bench.make_frames(2, range(1)), 1024),
              ("cfg4_T256", bench.make_frames(4, range(4)), 256),
              ("cfg4_T1024", bench.make_frames(4, range(2)), 1024),
              ("mixed", [W.automotive(seed=5, n_clusters=60, lo_pts=3, hi_pts=1500)], 300),

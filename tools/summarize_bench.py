@@ -26,6 +26,8 @@ def main():
             st = r.get("stage_ms_per_step", {})
             line += " stages " + " ".join(f"{k}={v:.3f}" for k, v in st.items())
             for k, v in (r.get("hbm") or {}).items():
+                if not v:
+                    continue
                 line += f" {k} {v['achieved']:.0f} GB/s ({v['frac']:.3f})"
         for k in ("p50_frame_latency_ms", "p50_frame_latency_e2e_ms", "frames_per_sec"):
             if k in d:
