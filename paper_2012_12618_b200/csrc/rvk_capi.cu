@@ -69,6 +69,9 @@ struct DevBuf {
       p = nullptr;
       cap = 0;
       RVK_CUDA(cudaMalloc(&p, want));
+      // zeroed once per (re)allocation: the alignment padding between the
+      // arrays of a block is then defined when the block is copied whole
+      RVK_CUDA(cudaMemset(p, 0, want));
       cap = want;
     }
     return static_cast<T*>(p);
@@ -91,6 +94,7 @@ struct HostBuf {
       cap = 0;
       const size_t want = std::max<size_t>(bytes + bytes / 4, 1 << 20);
       RVK_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+      std::memset(p, 0, want);  // padding between staged arrays is copied too
       cap = want;
     }
     return p;

@@ -813,8 +813,8 @@ __device__ void warp_select_pair(WarpPrep& w, int n, int k, bool pair, int nb, i
   int bin, below;
   warp_find_rank(w.hist, nb >> 5, k, lane, bin, below);
   const int in_bin = static_cast<int>(w.hist[bin]);
+  __syncwarp();  // every lane's hist reads before cand (aliasing hist) is written
   if (in_bin > kWarpCand) {
-    __syncwarp();
     v0 = warp_radix_select(w, n, k, lane);
     if (pair) v1 = warp_radix_select(w, n, k + 1, lane);
     return;
