@@ -1,18 +1,28 @@
 // sm_100a kernels of the per-cluster velocity-profile estimator.
 //
-//   prep_kernel    normalize_cluster + median + mad_threshold
-//                  (src/ransac.cpp:69-94, include/rvk/ransac.hpp:53-84)
+//   prep_warp_kernel / prep_hyp_kernel
+//                  normalize_cluster + median + mad_threshold
+//                  (src/ransac.cpp:69-94, include/rvk/ransac.hpp:53-84), every
+//                  trial's seed pair (src/ransac.cpp:111-123) and the FP32
+//                  coefficients of its line, scoring-unit registration; one
+//                  warp per small cluster or one CTA per cluster
 //   score_kernel   the hot loop: every (cluster, trial) line hypothesis
 //                  against every point of its cluster (run_trial,
-//                  src/ransac.cpp:32-65, scheduled as in :303-319), FP32
-//                  packed FFMA2 with a guard band -> UPPER-BOUND counts
-//   select_kernel  exact argmax (max count, lowest trial; :321-334): the
-//                  best upper bound is verified exactly, then every trial
-//                  whose upper bound reaches that exact count is verified
-//                  too; winner mask rebuilt exactly (:335-341); then the
-//                  least-squares refit + heading of estimate_cluster_velocity
-//                  (src/velocity.cpp:26-90) on the winning inliers.
+//                  src/ransac.cpp:32-65), FP32 packed FFMA2 with a guard band
+//                  -> UPPER-BOUND counts; persistent, TMA-staged units
+//   select_kernel / select_warp_kernel
+//                  exact argmax (max count, lowest trial; :181-189): the best
+//                  upper bound is verified exactly, then every trial whose
+//                  upper bound reaches that exact count; winner mask rebuilt
+//                  exactly; then the least-squares refit + heading of
+//                  estimate_cluster_velocity (src/velocity.cpp:26-90)
+//   fused_warp_kernel
+//                  all of the above for one small cluster per warp with the
+//                  intermediates in shared memory (single-frame calls)
 //   refit_kernel   estimate_all on caller-provided masks (velocity.cpp:92-121)
+//   pack_mask_kernel, mad_exact_kernel, exact_counts_kernel, seed_pairs_kernel
+//                  packed mask output and the exact-threshold / per-trial-count
+//                  / seed-pair entry points
 //
 // Why the argmax stays exact: upper[t] >= exact[t] for every trial (the FP32
 // band only ever admits extra points). If E0 is the exact count of the
