@@ -1,11 +1,12 @@
 """GPU parity on the exact calls bench.py times, every cluster.
 
-For BASELINE configs 2, 3 and 4 (T=256 and T=1024) the first step of the
+For BASELINE configs 1-4 (config 4 at T=256 and T=1024) the first step of the
 bench -- 16 frames batched into ONE rvk_ransac_estimate_device call with
 frame-local RNG keys (bench.batch, bench.py step()) -- is compared with the
 unmodified reference (oracle/_ref: rvk::run_ransac + estimate_all with all
 host threads, src/ransac.cpp:138-199, src/velocity.cpp:92-121) run frame by
-frame, the C3 pattern of tests/acceptance_test.cpp:257-330: for EVERY cluster
+frame, the C3 pattern of tests/acceptance_test.cpp:257-330 (and the first 16
+frames of the config-5 stream batched the same way): for EVERY cluster
 the inlier count, winning trial and mask bit-exact, the estimates within the
 north_star tolerance (assert_estimates_close). No sampling budget.
 """
@@ -19,8 +20,9 @@ from conftest import assert_estimates_close
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg,T", [(2, 0), (3, 0), (4, 256), (4, 1024)],
-                         ids=["config2", "config3", "config4_T256", "config4_T1024"])
+@pytest.mark.parametrize("cfg,T", [(1, 0), (2, 0), (3, 0), (4, 256), (4, 1024), (5, 0)],
+                         ids=["config1", "config2", "config3", "config4_T256", "config4_T1024",
+                              "config5_stream_frames"])
 def test_bench_batches_every_cluster_vs_reference(gpu_lib, reference, cfg, T):
     import torch
 
@@ -29,7 +31,11 @@ def test_bench_batches_every_cluster_vs_reference(gpu_lib, reference, cfg, T):
     from oracle.binding import make_params
     from paper_2012_12618_b200 import _native
 
-    frames = bench.make_frames(cfg, range(16), T)  # rank 0's first step
+    if cfg == 5:  # the stream's frames (tools/stream_bench.make_pool: seed = index)
+        from tools import workloads as W
+        frames = [W.stream_frame(i) for i in range(16)]
+    else:
+        frames = bench.make_frames(cfg, range(16), T)  # rank 0's first step
     off, az, dop, keys = bench.batch(frames)
     w0 = frames[0]
     p = rvk.RansacParams(w0.max_trials, w0.threshold_scale, w0.rng_seed)
