@@ -607,11 +607,13 @@ def main():
         evals_all, clusters_all = float(evals), float(clusters)
 
     # ---- rooflines. Stage ids (rvk_profile_read): 0 = prep (normalize,
-    # median, MAD, hypotheses: the ingest), 1 = the fused warp-per-cluster
-    # kernel (calls of at most one imaging frame, e.g. config 1), 2 = score,
-    # 3 = select + refit.
+    # median, MAD, hypotheses: the ingest), 1 = a fused warp-per-cluster
+    # kernel (the whole path for calls of at most one small-cluster frame,
+    # e.g. config 1; prep + score for batches of small clusters at T <= 512,
+    # e.g. config 4), 2 = score, 3 = select + refit.
     fused = stage_n[1] > 0 and stage_ms[1] > stage_ms[2]
     sc = 1 if fused else 2
+    whole_path = fused and stage_ms[3] < 0.05 * stage_ms[1]
     score_ms = stage_ms[sc] / max(1, stage_n[sc])
     evals_per_launch = iso_evals / max(1, stage_n[sc])
     achieved = evals_per_launch * FLOP_PER_EVAL / (score_ms / 1e3) / 1e12
@@ -620,8 +622,10 @@ def main():
     nominal = n_sm * 128 * 2 * sm_max * 1e6 / 1e12
     cap = load_capture(args.config, w0.max_trials) or {}
     total_ms = sum(stage_ms)
-    roofline = {"bound": "fp32", "kernel": "fused_warp_kernel (whole path, scoring inside)"
-                if fused else "score_kernel", "achieved": achieved, "peak": peak,
+    kname = ("fused_warp_kernel (whole path, scoring inside)" if whole_path else
+             "fused_warp_kernel<prep + score> (normalize, median, MAD, hypotheses and the "
+             "FFMA2 scoring loop in one warp per cluster)" if fused else "score_kernel")
+    roofline = {"bound": "fp32", "kernel": kname, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
                 "peak_source": "in-run FP32 FMA-pipe probe (max of FFMA2 %.1f / FFMA %.1f "
                                "TFLOP/s); MEASURED_PEAKS.json has no FP32 entry"
@@ -629,11 +633,11 @@ def main():
                 "frac_of_nominal": achieved / nominal, "nominal_peak": nominal,
                 "flop_per_eval": FLOP_PER_EVAL, "evals_per_launch": evals_per_launch,
                 "avg_launch_ms": score_ms,
-                "traffic": cap.get("score", {}).get("dram_bytes"),
+                "traffic": cap.get("fused" if fused else "score", {}).get("dram_bytes"),
                 "traffic_source": cap.get("source"),
                 "share_of_step": stage_ms[sc] / total_ms if total_ms else None,
                 "stage_ms_per_step": {"prep_ingest": stage_ms[0] / n_iso,
-                                      "fused": stage_ms[1] / n_iso,
+                                      "fused_prep_score_or_whole": stage_ms[1] / n_iso,
                                       "score": stage_ms[2] / n_iso,
                                       "select_refit": stage_ms[3] / n_iso},
                 "measured": "isolated single-stream pass (%d steps) right after the timed "
@@ -650,9 +654,9 @@ def main():
                 "bytes_model": f"{b_pt:g} B/point + {b_cl} B/cluster (SURVEY.md 8(d))",
                 "avg_ms_per_step": ms,
                 "traffic": cap.get(ncu_key, {}).get("dram_bytes")}
-    roofline["hbm"] = None if fused else {
-        "ingest": hbm_line("prep kernels (normalize, median, MAD, hypotheses)", 0,
-                           INGEST_B_PT, INGEST_B_CL, "prep"),
+    roofline["hbm"] = None if whole_path else {
+        "ingest": None if fused else hbm_line("prep kernels (normalize, median, MAD, "
+                                              "hypotheses)", 0, INGEST_B_PT, INGEST_B_CL, "prep"),
         "refit": hbm_line("select kernel (exact winner, mask, LSQ refit + heading)", 3,
                           REFIT_B_PT, REFIT_B_CL, "select")}
 

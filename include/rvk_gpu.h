@@ -271,9 +271,12 @@ int rvk_combine_masks(int64_t n, const int32_t* labels, int32_t n_masks, const i
                       const int64_t* mask_offsets, const uint8_t* masks, uint8_t* result);
 
 /* Stage timing for benchmarking/profiling. When enabled, CUDA events bracket
- * every pipeline stage launch on its stream (0 = prep, 1 = hypothesis
- * setup + tile plan, 2 = score, 3 = select+refit); rvk_profile_read waits for them, returns the accumulated
- * device milliseconds and launch counts per stage, and clears the record. */
+ * every pipeline stage launch on its stream (0 = prep + hypothesis setup +
+ * tile plan, 1 = a fused warp-per-cluster kernel -- the whole path for a
+ * single frame of small clusters, or prep + score for batches of them --,
+ * 2 = score, 3 = select + refit); rvk_profile_read waits for them, returns the
+ * accumulated device milliseconds and launch counts per stage, and clears the
+ * record. */
 void rvk_profile_enable(int32_t on);
 int rvk_profile_read(double* ms, int64_t* launches, int32_t n_stages);
 

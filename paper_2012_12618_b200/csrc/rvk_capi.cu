@@ -375,12 +375,14 @@ void stage(int id, cudaStream_t st, F&& launch) {
 
 // prep+hyps -> score -> select(+refit): the whole device pipeline of one call.
 // Stage ids (rvk_profile_read): 0 = prep + hypothesis setup + tile plan,
-// 1 = the fused warp-per-cluster kernel (calls of small clusters), 2 = score,
-// 3 = select + refit. On the fused path stages 0/2/3 take only the clusters
+// 1 = a fused warp-per-cluster kernel (the whole path for single small
+// frames, or prep + score for batches of small clusters), 2 = score,
+// 3 = select + refit. On the fused paths stages 0/2 take only the clusters
 // the fused kernel listed (none when the host knows they all fit).
 void run_pipeline(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   const Outputs& o, cudaStream_t st) {
   if (fused_path(f, p)) stage(1, st, [&] { launch_fused(f, p, s, o, st); });
+  if (prep_score_path(f, p)) stage(1, st, [&] { launch_prep_score(f, p, s, st); });
   stage(0, st, [&] { launch_prep_hyps(f, p, s, st); });
   stage(2, st, [&] { launch_score(f, p, s, st); });
   stage(3, st, [&] { launch_select(f, p, s, o, st); });

@@ -1886,21 +1886,33 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 // Clusters larger than kFusedCap (or calls with T > kFusedMaxT) go to the
 // list for the CTA path (prep_hyp_kernel -> score_kernel -> select list).
 // 508 points: four 4-warp CTAs per SM fit the 228 KB of shared memory
-constexpr int kFusedCap = 508;
-constexpr int kFusedHist = 512;              // median buckets (power of two >= cap)
-constexpr int kFusedMaxT = 2 * kFusedHist;   // u16 upper bounds in the hist region
 constexpr int kFusedWarps = 4;
-constexpr int kFusedPairs = kFusedCap / 2 + 3;  // float4 (two points) per slot, + read-ahead
-static_assert(8 * kWarpCand <= 16 * kFusedPairs, "median candidates live in the pair region");
 
-// Byte offsets inside one warp's slot. The pair region holds the median's
-// candidates until the pairs are written (after the median).
-constexpr size_t kFsX = 0;                                   // double x[cap]  (normalized)
-constexpr size_t kFsY = kFsX + 8 * kFusedCap;                // double y[cap]  (normalized)
-constexpr size_t kFsP = kFsY + 8 * kFusedCap;                // float4 pairs | u64 cand
-constexpr size_t kFsH = kFsP + 16 * kFusedPairs;             // u32 hist[512] | u16 upper[1024]
-constexpr size_t kFusedSlotBytes = kFsH + 4 * kFusedHist;
-constexpr size_t kFusedSmemBytes = kFusedSlotBytes * kFusedWarps;
+// One warp's shared-memory slot for clusters of up to kCap points. The pair
+// region holds the median's candidates until the pairs are written (after
+// the median); the bucket region holds the u16 upper bounds after it.
+template <int kCap>
+struct FusedGeom {
+  static constexpr int cap = kCap;
+  static constexpr int hist = kCap <= 256 ? 256 : 512;  // median buckets (power of two >= cap)
+  static constexpr int max_t = 2 * hist;                // u16 upper bounds in the bucket region
+  static constexpr int pairs = kCap / 2 + 3;            // float4 (two points), + read-ahead
+  static constexpr size_t x = 0;                        // double x[cap]  (normalized)
+  static constexpr size_t y = x + 8 * kCap;             // double y[cap]  (normalized)
+  static constexpr size_t p = y + 8 * kCap;             // float4 pairs | u64 cand
+  static constexpr size_t h = p + 16 * pairs;           // u32 hist | u16 upper
+  static constexpr size_t slot = h + 4 * hist;
+  static constexpr size_t smem = slot * kFusedWarps;
+  static_assert(8 * kWarpCand <= 16 * pairs, "median candidates live in the pair region");
+  static_assert(kCap <= 512, "bucket region");
+};
+// the whole path, one warp per cluster: 508 points, four 4-warp CTAs per SM
+using FusedFull = FusedGeom<508>;
+// prep + score only (select_warp_kernel follows): 384 points (every config-4
+// cluster), five 4-warp CTAs per SM at <= 102 registers
+using FusedPrepScore = FusedGeom<384>;
+constexpr int kFusedCap = FusedFull::cap;
+constexpr int kFusedMaxT = FusedFull::max_t;
 
 extern __shared__ __align__(16) unsigned char fused_dyn[];
 
@@ -2086,26 +2098,38 @@ __device__ __noinline__ int fused_exact_count(const FusedCluster fc, int t, doub
   return warp_reduce(cnt, SumI());
 }
 
-__global__ void __launch_bounds__(kFusedWarps * 32, 4)
+// kSelect == false: the prep + score half only (prep_score mode): the warp
+// writes what select_warp_kernel reads -- xy64, the xy32 pairs, stat and the
+// upper-bound counts -- and moves on; the hypotheses never leave registers.
+struct PrepScoreOut {
+  double2* xy64;
+  float2* xy32;
+  double4* stat;
+  int32_t* upper;  // [C][Tg * 8]
+  int Tg;
+};
+
+template <bool kSelect, class G, int kMinBlocks>
+__global__ void __launch_bounds__(kFusedWarps * 32, kMinBlocks)
 fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                   const double* __restrict__ az, const double* __restrict__ dop, double scale,
                   const int32_t* __restrict__ keys, const int32_t* __restrict__ cluster_ids,
                   int64_t frame_id, int T, uint64_t seed, int32_t* __restrict__ out_count,
                   int32_t* __restrict__ out_trial, uint8_t* __restrict__ mask,
                   rvk_estimate* __restrict__ est, int32_t* __restrict__ big_list,
-                  int32_t* big_ctl) {
+                  int32_t* big_ctl, PrepScoreOut ps) {
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  unsigned char* slot = fused_dyn + kFusedSlotBytes * wib;
-  double* xs = reinterpret_cast<double*>(slot + kFsX);
-  double* ys = reinterpret_cast<double*>(slot + kFsY);
-  float4* pairs = reinterpret_cast<float4*>(slot + kFsP);
-  float2* p32 = reinterpret_cast<float2*>(slot + kFsP);  // xy32_put / xy32_get layout
-  unsigned int* hist = reinterpret_cast<unsigned int*>(slot + kFsH);
-  uint16_t* upper = reinterpret_cast<uint16_t*>(slot + kFsH);
-  unsigned long long* cand = reinterpret_cast<unsigned long long*>(slot + kFsP);
+  unsigned char* slot = fused_dyn + G::slot * wib;
+  double* xs = reinterpret_cast<double*>(slot + G::x);
+  double* ys = reinterpret_cast<double*>(slot + G::y);
+  float4* pairs = reinterpret_cast<float4*>(slot + G::p);
+  float2* p32 = reinterpret_cast<float2*>(slot + G::p);  // xy32_put / xy32_get layout
+  unsigned int* hist = reinterpret_cast<unsigned int*>(slot + G::h);
+  uint16_t* upper = reinterpret_cast<uint16_t*>(slot + G::h);
+  unsigned long long* cand = reinterpret_cast<unsigned long long*>(slot + G::p);
   const bool refit = est != nullptr;
-  const int fused_T = T <= kFusedMaxT;
+  const int fused_T = !kSelect || T <= G::max_t;
 
 #pragma unroll 1
   for (;;) {
@@ -2116,11 +2140,12 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const int64_t b = offsets[c];
     const int n = static_cast<int>(offsets[c + 1] - b);
     if (n < kMinClusterPoints) {
-      write_too_small(c, n, frame_id, cluster_ids ? cluster_ids[c] : c, out_count, out_trial,
-                      mask + b, est, lane, 32);
+      if (kSelect)  // (prep_score mode: select_warp_kernel writes the sentinel)
+        write_too_small(c, n, frame_id, cluster_ids ? cluster_ids[c] : c, out_count, out_trial,
+                        mask + b, est, lane, 32);
       continue;
     }
-    if (n > kFusedCap || !fused_T) {  // the CTA path takes it
+    if (n > G::cap || !fused_T) {  // the CTA path takes it
       if (lane == 0) big_list[atomicAdd(&big_ctl[0], 1)] = c;
       continue;
     }
@@ -2163,6 +2188,7 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                                : __ddiv_rn(__dsub_rn(ys[k], lo1), s1));
         xs[k] = x;
         ys[k] = y;
+        if (!kSelect) ps.xy64[b + k] = make_double2(x, y);
         atomicAdd(&hist[med_bin(fused_key(ys, k), nb)], 1u);
       }
     }
@@ -2187,6 +2213,7 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       const double delta = (4.0 * n + 16.0) * 0x1p-53;
       thr_lo = mid * (1.0 - delta);
       thr_hi = mid * (1.0 + delta);
+      if (!kSelect && lane == 0) ps.stat[c] = make_double4(thr_lo, thr_hi, med, CUDART_NAN);
     }
     __syncwarp();  // cand and hist are free: the pairs and the upper bounds reuse them
     // FP32 point pairs (x_2q, x_2q+1, y_2q, y_2q+1) for the scoring loop;
@@ -2205,6 +2232,8 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
           v.w = __double2float_rn(ys[k1]);
         }
         pairs[q] = v;
+        if (!kSelect && q < m2)  // the same pair layout as xy32_put's
+          reinterpret_cast<float4*>(ps.xy32 + xy32_base(offsets, c))[q] = v;
       }
     }
     __syncwarp();
@@ -2265,6 +2294,15 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
         score_pair(v2);
         score_pair(v3);
       }
+      if (!kSelect) {  // this warp saw every point: plain stores, trials padded to 8
+        int32_t* gu = ps.upper + static_cast<int64_t>(c) * ps.Tg * 8;
+        if (8 * (tb / 8 + lane) < ps.Tg * 8) {
+          int4* g4 = reinterpret_cast<int4*>(gu + tb + 8 * lane);
+          g4[0] = make_int4(cnt[0], cnt[1], cnt[2], cnt[3]);
+          g4[1] = make_int4(cnt[4], cnt[5], cnt[6], cnt[7]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < kNH; ++q) {
         const int t = tb + 8 * lane + q;
@@ -2273,6 +2311,10 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
           vbest = MaxU64()(vbest, pack_best(static_cast<int>(cnt[q]), t));
         }
       }
+    }
+    if (!kSelect) {  // select_warp_kernel takes it from here
+      __syncwarp();
+      continue;
     }
     vbest = warp_reduce(vbest, MaxU64());
     __syncwarp();  // upper[] visible to the whole warp
@@ -2497,8 +2539,42 @@ bool fused_path(const FrameDev& f, const rvk_ransac_params& p) {
 
 // Whether the CTA path has clusters to take after the fused kernel: unknown
 // (device-side sizes) unless the host passed the largest cluster size.
-bool fused_leaves_big(const FrameDev& f) {
-  return f.max_cluster < 0 || f.max_cluster > kFusedCap;
+bool fused_leaves_big(const FrameDev& f, int cap = kFusedCap) {
+  return f.max_cluster < 0 || f.max_cluster > cap;
+}
+
+// Prep + score fused per warp for the clusters of <= 384 points (the
+// hypotheses go from registers straight into the scoring loop; the
+// latency-bound prep of some warps overlaps the FMA-bound scoring of the
+// others), select by select_warp_kernel, larger clusters by the CTA path.
+// Measured on B200 (bench.py, 16 frames): config 4 T = 256 step 1.263 ->
+// 1.171 ms; at T = 1024 the dedicated scoring kernel's 24 warps/SM win
+// (3.190 vs 3.255 ms), so the default takes it for small clusters and
+// T <= 512. RVK_PREP_SCORE=1/0 forces it on/off.
+bool prep_score_path(const FrameDev& f, const rvk_ransac_params& p) {
+  if (f.n_clusters == 0 || fused_path(f, p)) return false;
+  static const int forced = env_int("RVK_PREP_SCORE", -1);
+  if (forced >= 0) return forced != 0;
+  const int64_t avg = f.n_points / f.n_clusters;
+  return avg < 384 && p.max_trials <= 512;
+}
+
+int fused_resident_ctas(bool select);
+
+void launch_prep_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                       cudaStream_t st) {
+  if (f.n_clusters == 0) return;
+  ScoreGeom g = score_geom(p.max_trials);
+  cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 4, st);
+  const int64_t want = (static_cast<int64_t>(f.n_clusters) + kFusedWarps - 1) / kFusedWarps;
+  const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(false), want));
+  const PrepScoreOut ps{s.xy64, s.xy32, s.stat, s.upper, g.Tg};
+  fused_warp_kernel<false, FusedPrepScore, 5><<<grid, kFusedWarps * 32, FusedPrepScore::smem,
+                                                 st>>>(
+      f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, f.cluster_ids,
+      f.frame_id, p.max_trials, p.rng_seed, nullptr, nullptr, nullptr, nullptr, s.big_list,
+      s.big_ctl, ps);
+  count_launch();
 }
 
 void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
@@ -2507,6 +2583,16 @@ void launch_prep_hyps(const FrameDev& f, const rvk_ransac_params& p, const Scrat
   ScoreGeom g = score_geom(p.max_trials);
   set_ppt(g, s.ppt);
   cudaMemsetAsync(s.tile_count, 0, sizeof(int32_t) * (kTileBuckets + 1), st);
+  if (prep_score_path(f, p)) {  // the clusters launch_prep_score listed, by persistent CTAs
+    if (!fused_leaves_big(f, FusedPrepScore::cap)) return;
+    prep_hyp_kernel<256, 4><<<std::min<int64_t>(2 * sm_count(), f.n_clusters), 256,
+                              prep_dyn_bytes(2048), st>>>(
+        f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, g, p.rng_seed,
+        s.xy64, s.xy32, s.stat, s.hyp, s.upper, s.tiles, s.tile_count, s.tile_cap, 2048,
+        s.big_list, s.big_ctl);
+    count_launch();
+    return;
+  }
   if (fused_path(f, p)) {
     // the clusters the fused kernel listed, by persistent CTAs
     if (!fused_leaves_big(f)) return;
@@ -2565,20 +2651,23 @@ int score_grid(int64_t max_units) {
   return static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(grid, (max_units + warps_per_cta - 1) / warps_per_cta)));
 }
-int fused_resident_ctas() {
-  static int grid = 0;
-  if (grid == 0) {
-    int per_sm = 0;
-    cudaFuncSetAttribute(fused_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kFusedSmemBytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_warp_kernel, kFusedWarps * 32,
-                                                  kFusedSmemBytes);
-    per_sm = std::max(1, std::min(per_sm, env_int("RVK_FUSED_CTAS", per_sm)));
-    grid = sm_count() * per_sm;
-  }
-  return grid;
-}
 }  // namespace
+
+int fused_resident_ctas(bool select) {
+  static int grid[2] = {0, 0};
+  int& g = grid[select ? 1 : 0];
+  if (g == 0) {
+    int per_sm = 0;
+    auto k = select ? fused_warp_kernel<true, FusedFull, 4>
+                    : fused_warp_kernel<false, FusedPrepScore, 5>;
+    const size_t smem = select ? FusedFull::smem : FusedPrepScore::smem;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFusedWarps * 32, smem);
+    per_sm = std::max(1, std::min(per_sm, env_int("RVK_FUSED_CTAS", per_sm)));
+    g = sm_count() * per_sm;
+  }
+  return g;
+}
 
 int score_ppt(const ScoreGeom& g, int64_t n_points, int32_t n_clusters) {
   static const int forced = env_int("RVK_SCORE_PPT", 0);
@@ -2599,11 +2688,11 @@ void launch_fused(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   if (f.n_clusters == 0) return;
   cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 4, st);
   const int64_t want = (static_cast<int64_t>(f.n_clusters) + kFusedWarps - 1) / kFusedWarps;
-  const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(), want));
-  fused_warp_kernel<<<grid, kFusedWarps * 32, kFusedSmemBytes, st>>>(
+  const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(true), want));
+  fused_warp_kernel<true, FusedFull, 4><<<grid, kFusedWarps * 32, FusedFull::smem, st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, f.cluster_ids,
       f.frame_id, p.max_trials, p.rng_seed, o.inlier_count, o.winning_trial, o.mask, o.est,
-      s.big_list, s.big_ctl);
+      s.big_list, s.big_ctl, PrepScoreOut{});
   count_launch();
 }
 
@@ -2611,6 +2700,7 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
                   cudaStream_t st) {
   if (f.n_clusters == 0) return;
   if (fused_path(f, p) && !fused_leaves_big(f)) return;
+  if (prep_score_path(f, p) && !fused_leaves_big(f, FusedPrepScore::cap)) return;
   ScoreGeom g = score_geom(p.max_trials);
   set_ppt(g, s.ppt);
   const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / g.ppt + f.n_clusters);
@@ -2632,7 +2722,7 @@ void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch&
     count_launch();
     return;
   }
-  if (env_int("RVK_SELECT_WARP", avg < 384 ? 1 : 0) != 0) {  // warp per cluster
+  if (prep_score_path(f, p) || env_int("RVK_SELECT_WARP", avg < 384 ? 1 : 0) != 0) {
     select_warp_kernel<<<(f.n_clusters + kSelectWarps - 1) / kSelectWarps, kSelectWarps * 32, 0,
                          st>>>(f.n_clusters, f.offsets, f.azimuth, f.doppler, f.keys,
                                f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,

@@ -113,6 +113,11 @@ bool fused_path(const FrameDev& f, const rvk_ransac_params& p);
 // median/MAD, hypotheses, FP32 upper-bound scoring, exact select, mask, refit.
 void launch_fused(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   const Outputs& o, cudaStream_t st);
+// Whether a call takes the fused prep + score warp kernel (launch_prep_score)
+// for its clusters of <= 384 points; select_warp_kernel then selects.
+bool prep_score_path(const FrameDev& f, const rvk_ransac_params& p);
+void launch_prep_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
+                       cudaStream_t st);
 // Upper-bound inlier counts for every (cluster, trial): FFMA2 scoring.
 void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& s,
                   cudaStream_t st);

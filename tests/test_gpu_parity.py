@@ -284,11 +284,13 @@ def test_launch_shapes_bit_identical(gpu_lib):
     included (counts/masks by the exact scheme, velocities by the canonical
     refit order), as the reference's worker-count invariance demands."""
     digests = {}
-    for env in ({}, {"RVK_SELECT_WARP": "1"}, {"RVK_SELECT_WARP": "0"},
-                {"RVK_SELECT_WARP": "0", "RVK_SELECT_THREADS": "64"},
-                {"RVK_SELECT_WARP": "0", "RVK_SELECT_THREADS": "256"},
-                {"RVK_PREP_WARP": "1"}, {"RVK_PREP_WARP": "0", "RVK_PREP_THREADS": "512"},
-                {"RVK_SCORE_PPT": "64"}, {"RVK_FUSED": "1"}, {"RVK_FUSED": "0"}):
+    ps0 = {"RVK_PREP_SCORE": "0"}
+    for env in ({}, dict(ps0, RVK_SELECT_WARP="1"), dict(ps0, RVK_SELECT_WARP="0"),
+                dict(ps0, RVK_SELECT_WARP="0", RVK_SELECT_THREADS="64"),
+                dict(ps0, RVK_SELECT_WARP="0", RVK_SELECT_THREADS="256"),
+                dict(ps0, RVK_PREP_WARP="1"), dict(ps0, RVK_PREP_WARP="0", RVK_PREP_THREADS="512"),
+                {"RVK_SCORE_PPT": "64"}, {"RVK_FUSED": "1"}, {"RVK_FUSED": "0"},
+                {"RVK_FUSED": "0", "RVK_PREP_SCORE": "1"}, {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0"}):
         r = subprocess.run([sys.executable, "-c", _SHAPE_SCRIPT, ROOT], capture_output=True,
                            text=True, env=dict(os.environ, **env), cwd=ROOT, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -487,18 +489,21 @@ def est_dtype():
 
 
 @pytest.mark.parametrize("env", [{"RVK_FUSED": "1"}, {"RVK_FUSED": "0"},
-                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "256",
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "1"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_PREP_THREADS": "256",
                                   "RVK_SELECT_THREADS": "256"},
-                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "64",
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_PREP_THREADS": "64",
                                   "RVK_SELECT_THREADS": "64"},
-                                 {"RVK_FUSED": "0", "RVK_PREP_WARP": "1"},
-                                 {"RVK_FUSED": "0", "RVK_PREP_WARP": "0"},
-                                 {"RVK_FUSED": "0", "RVK_SELECT_WARP": "1"},
-                                 {"RVK_FUSED": "0", "RVK_SELECT_WARP": "0"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_PREP_WARP": "1"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_PREP_WARP": "0"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_SELECT_WARP": "1"},
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_SELECT_WARP": "0"},
                                  {"RVK_SCORE_PPT": "64"}, {"RVK_SCORE_PPT": "512"},
-                                 {"RVK_FUSED": "0", "RVK_PREP_THREADS": "512",
+                                 {"RVK_FUSED": "0", "RVK_PREP_SCORE": "0", "RVK_PREP_THREADS": "512",
                                   "RVK_PREP_WARP": "0"}],
-                         ids=["fused", "unfused", "cta256", "cta64", "warp_prep", "cta_prep",
+                         ids=["fused", "unfused", "prep_score", "no_prep_score", "cta256",
+                              "cta64", "warp_prep", "cta_prep",
                               "warp_select", "cta_select", "units_64", "units_512",
                               "cta512_prep"])
 def test_alternative_kernel_shapes_parity(gpu_lib, env):

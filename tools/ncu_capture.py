@@ -23,6 +23,8 @@ KEYS = {"dram__bytes_read.sum": "dram_read", "dram__bytes_write.sum": "dram_writ
 
 
 def role(name):
+    if "fused_warp" in name:
+        return "fused"
     if "score_kernel" in name:
         return "score"
     if "prep" in name:
