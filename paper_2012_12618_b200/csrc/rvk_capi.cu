@@ -70,8 +70,11 @@ struct DevBuf {
       cap = 0;
       RVK_CUDA(cudaMalloc(&p, want));
       // zeroed once per (re)allocation: the alignment padding between the
-      // arrays of a block is then defined when the block is copied whole
+      // arrays of a block is then defined when the block is copied whole.
+      // The memset runs on the legacy stream, which does not order against
+      // our non-blocking streams: wait for it before any kernel can write.
       RVK_CUDA(cudaMemset(p, 0, want));
+      RVK_CUDA(cudaStreamSynchronize(nullptr));
       cap = want;
     }
     return static_cast<T*>(p);
