@@ -2247,30 +2247,39 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     for (int tb = 0; tb < T; tb += 8 * 32) {
       float A[kNH], B[kNH];
       float2 Cc[kNH], T2[kNH];
-      // one copy of the (long) hypothesis code: trial q enters at slot kNH-1
-      // and the registers rotate down, so slot q holds trial 8 lane + q at
-      // the end (static register indices; the kernel's code size is what
-      // keeps the instruction cache warm across warps in different phases)
+      // kHU trials per step (independent chains), the code of one step once:
+      // the step's trials enter at slots kNH-kHU.. and the registers rotate
+      // down by kHU, so slot q holds trial 8 lane + q at the end (static
+      // register indices; rotating one trial at a time cost 336 moves per
+      // lane and block, measured)
+      constexpr int kHU = 4;
 #pragma unroll 1
-      for (int q = 0; q < kNH; ++q) {
-        const int t = tb + 8 * lane + q;
-        FastHyp f = inert_fast();
-        if (t < T) {
-          int i, j;
-          seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-          f = make_fast_from_seeds(xs[i], ys[i], xs[j], ys[j], thr_lo, thr_hi);
+      for (int q0 = 0; q0 < kNH; q0 += kHU) {
+        FastHyp f[kHU];
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int t = tb + 8 * lane + q0 + u;
+          f[u] = inert_fast();
+          if (t < T) {
+            int i, j;
+            seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+            f[u] = make_fast_from_seeds(xs[i], ys[i], xs[j], ys[j], thr_lo, thr_hi);
+          }
         }
 #pragma unroll
-        for (int r = 0; r + 1 < kNH; ++r) {
-          A[r] = A[r + 1];
-          B[r] = B[r + 1];
-          Cc[r] = Cc[r + 1];
-          T2[r] = T2[r + 1];
+        for (int r = 0; r + kHU < kNH; ++r) {
+          A[r] = A[r + kHU];
+          B[r] = B[r + kHU];
+          Cc[r] = Cc[r + kHU];
+          T2[r] = T2[r + kHU];
         }
-        A[kNH - 1] = f.A;
-        B[kNH - 1] = f.B;
-        Cc[kNH - 1] = make_float2(f.C, f.C);
-        T2[kNH - 1] = make_float2(-f.t2hi, -f.t2hi);
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          A[kNH - kHU + u] = f[u].A;
+          B[kNH - kHU + u] = f[u].B;
+          Cc[kNH - kHU + u] = make_float2(f[u].C, f[u].C);
+          T2[kNH - kHU + u] = make_float2(-f[u].t2hi, -f[u].t2hi);
+        }
       }
       uint32_t cnt[kNH];
 #pragma unroll
@@ -2547,16 +2556,16 @@ bool fused_leaves_big(const FrameDev& f, int cap = kFusedCap) {
 // hypotheses go from registers straight into the scoring loop; the
 // latency-bound prep of some warps overlaps the FMA-bound scoring of the
 // others), select by select_warp_kernel, larger clusters by the CTA path.
-// Measured on B200 (bench.py, 16 frames): config 4 T = 256 step 1.263 ->
-// 1.171 ms; at T = 1024 the dedicated scoring kernel's 24 warps/SM win
-// (3.190 vs 3.255 ms), so the default takes it for small clusters and
-// T <= 512. RVK_PREP_SCORE=1/0 forces it on/off.
+// Measured on B200 (bench.py, 16 frames per step): config 4 step 1.263 ->
+// 1.169 ms at T = 256, 3.190 -> 2.979 ms at T = 1024. The default takes it
+// for calls whose mean cluster is small (as the warp prep it replaces);
+// RVK_PREP_SCORE=1/0 forces it on/off.
 bool prep_score_path(const FrameDev& f, const rvk_ransac_params& p) {
   if (f.n_clusters == 0 || fused_path(f, p)) return false;
   static const int forced = env_int("RVK_PREP_SCORE", -1);
   if (forced >= 0) return forced != 0;
   const int64_t avg = f.n_points / f.n_clusters;
-  return avg < 384 && p.max_trials <= 512;
+  return avg < 384;
 }
 
 int fused_resident_ctas(bool select);
