@@ -9,7 +9,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 for spec in "4 256" "4 1024" "2 0" "3 0"; do
   set -- $spec
   timeout 900 ncu --set full --import-source on --clock-control none \
-    -k regex:"prep_warp|prep_hyp|score_kernel|select_warp|select_kernel" -c 4 \
+    -k regex:"prep_warp|prep_hyp|score_kernel|select_warp|select_kernel|fused_warp" -c 5 \
     -o gpurun_out/r2_c$1_t$2 python tools/one_call.py --config $1 --frames 16 --max-trials $2 --reps 1 \
     > gpurun_out/r2_c$1_t$2.log 2>&1
 done
