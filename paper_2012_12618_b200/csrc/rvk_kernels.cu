@@ -2167,8 +2167,8 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       hi1 = d > hi1 ? d : hi1;
     }
     warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
+    __syncwarp();  // the zeroed buckets and the raw slot before any other lane uses them
     if (lo0 == 0.0 || hi0 == 0.0 || lo1 == 0.0 || hi1 == 0.0) {
-      __syncwarp();  // (rare) the first +-0 in index order, from the raw slot
       lo0 = warp_first_zero(lo0, xs, n, lane);
       hi0 = warp_first_zero(hi0, xs, n, lane);
       lo1 = warp_first_zero(lo1, ys, n, lane);
