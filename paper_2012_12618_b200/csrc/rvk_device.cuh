@@ -262,6 +262,46 @@ __device__ __forceinline__ double exact_threshold(const double2* xy64, int n, do
   return __dmul_rn(scale, __ddiv_rn(acc, static_cast<double>(n)));
 }
 
+// sin and cos of an azimuth for the LSQ design matrix (build_design_matrix,
+// src/velocity.cpp:9-17, which takes Eigen's cos()/sin()). Azimuths are
+// atan2 outputs in (-pi, pi] (src/scene.cpp, the frame reader's check), so
+// the general range reduction of libdevice's sincos is not needed: one
+// Cody-Waite step with the fdlibm split of pi/2 (|q| <= 2, FMA products
+// exact) and the fdlibm kernel polynomials on [-pi/4, pi/4]: within
+// 1.1e-16 absolute of libdevice's sincos over 4e8 points of [-4, 4]
+// (tools/sincos_check.cu; the reference's own libm differs from any other by
+// an ulp too, and the refit is tolerance-checked), in ~25 FP64
+// instructions instead of ~60 plus table loads. Outside [-4, 4]: libdevice.
+__device__ __forceinline__ void sincos_az(double x, double* s, double* c) {
+  if (!(fabs(x) <= 4.0)) {
+    sincos(x, s, c);
+    return;
+  }
+  const double q = rint(x * 0.63661977236758134308);  // 2/pi
+  double r = fma(-q, 1.57079632673412561417e+00, x);  // pi/2, first 33 bits
+  r = fma(-q, 6.07710050650619224932e-11, r);          // next 33 bits
+  r = fma(-q, 2.02226624879595063154e-21, r);          // tail
+  const double z = r * r;
+  const double ps = fma(z, fma(z, fma(z, fma(z, fma(z, 1.58969099521155010221e-10,
+                                                      -2.50507602534068634195e-08),
+                                               2.75573137070700676789e-06),
+                                        -1.98412698298579493134e-04),
+                                 8.33333333332248946124e-03),
+                          -1.66666666666666324348e-01);
+  const double sr = fma(r * z, ps, r);
+  const double pc = fma(z, fma(z, fma(z, fma(z, fma(z, -1.13596475577881948265e-11,
+                                                      2.08757232129817482790e-09),
+                                               -2.75573143513906633035e-07),
+                                        2.48015872894767294178e-05),
+                                 -1.38888888888741095749e-03),
+                          4.16666666666666019037e-02);
+  const double cr = fma(z * z, pc, fma(-0.5, z, 1.0));
+  const int iq = static_cast<int>(q) & 3;
+  const double ss = (iq & 1) ? cr : sr, cc = (iq & 1) ? sr : cr;
+  *s = (iq & 2) ? -ss : ss;
+  *c = ((iq + 1) & 2) ? -cc : cc;
+}
+
 // Packs (count, trial) so that a max picks the largest count and, on ties,
 // the lowest trial -- the ascending strict-> scan of src/ransac.cpp:181-189.
 __device__ __forceinline__ unsigned long long pack_best(int count, int trial) {

@@ -1312,7 +1312,7 @@ struct RefitAcc {
   }
   __device__ __forceinline__ void add(int k, double a, double d) {
     double s, c;
-    sincos(a, &s, &c);
+    sincos_az(a, &s, &c);
     add_cs(k, c, s, d);
   }
   // add_cs for a staged point whose (c, s, d) are zeros unless it is an
@@ -1374,7 +1374,7 @@ __device__ __noinline__ void finish_refit(const RefitAcc& a, const double* __res
   }
   if (nin == 1) {  // velocity.cpp:63-67
     double s, c;
-    sincos(az[first], &s, &c);
+    sincos_az(az[first], &s, &c);
     e.v_x = dop[first] * c;
     e.v_y = dop[first] * s;
     e.condition_ok = 0;
@@ -1406,7 +1406,7 @@ __device__ __noinline__ void finish_refit(const RefitAcc& a, const double* __res
         u1 /= nr;
       }
       double s0, c0;
-      sincos(az[first], &s0, &c0);
+      sincos_az(az[first], &s0, &c0);
       if (u0 * c0 + u1 * s0 < 0.0) {
         u0 = -u0;
         u1 = -u1;
@@ -1441,7 +1441,7 @@ __device__ void block_refit(int n, const double* __restrict__ az, const double* 
       st.in[i] = in;
       double sn = 0.0, cs = 0.0, dd = 0.0;
       if (in) {
-        sincos(az[k], &sn, &cs);
+        sincos_az(az[k], &sn, &cs);
         dd = dop[k];
       }
       st.c[i] = cs;
@@ -1575,7 +1575,7 @@ __device__ __forceinline__ void select_cluster(
           if (refit) {
             rst.in[k - kb] = in;
             double sn = 0.0, cs = 0.0;
-            if (in) sincos(pa[u], &sn, &cs);
+            if (in) sincos_az(pa[u], &sn, &cs);
             rst.c[k - kb] = cs;
             rst.s[k - kb] = sn;
             rst.d[k - kb] = in ? pd[u] : 0.0;
