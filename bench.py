@@ -655,8 +655,11 @@ def main():
                 "avg_ms_per_step": ms,
                 "traffic": cap.get(ncu_key, {}).get("dram_bytes")}
     roofline["hbm"] = None if whole_path else {
-        "ingest": None if fused else hbm_line("prep kernels (normalize, median, MAD, "
-                                              "hypotheses)", 0, INGEST_B_PT, INGEST_B_CL, "prep"),
+        "ingest": hbm_line("fused prep + score kernel: the ingest shares the kernel (and its "
+                           "time) with the scoring loop, so this is a lower bound of the "
+                           "ingest rate", 1, INGEST_B_PT, INGEST_B_CL, "fused")
+        if fused else hbm_line("prep kernels (normalize, median, MAD, hypotheses)", 0,
+                               INGEST_B_PT, INGEST_B_CL, "prep"),
         "refit": hbm_line("select kernel (exact winner, mask, LSQ refit + heading)", 3,
                           REFIT_B_PT, REFIT_B_CL, "select")}
 
