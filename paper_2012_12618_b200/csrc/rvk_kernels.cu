@@ -2157,8 +2157,9 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     while (nb < n) nb <<= 1;
     for (int i = lane; i < nb; i += 32) hist[i] = 0;
     double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
+#pragma unroll 2
     for (int k = lane; k < n; k += 32) {
-      const double a = caz[k], d = cdop[k];
+      const double a = __ldcs(caz + k), d = __ldcs(cdop + k);  // read once: streaming
       xs[k] = a;  // raw values, normalized in place below (same lane)
       ys[k] = d;
       lo0 = a < lo0 ? a : lo0;
