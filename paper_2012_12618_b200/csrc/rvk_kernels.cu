@@ -1864,9 +1864,8 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 
 // --------------------------------------------- fused warp-per-cluster path
 //
-// One warp owns one cluster of up to kFusedCap points from the raw FP64 input
-// to the outputs; every intermediate lives in the warp's shared-memory slot
-// or in registers:
+// One warp owns one cluster from the raw FP64 input onwards; every
+// intermediate lives in the warp's shared-memory slot or in registers:
 //   1. load az/dop once (coalesced) into the slot, min/max (first-occurrence
 //      +-0 semantics), exact normalisation in place (normalize_cluster,
 //      src/ransac.cpp:69-87) + FP32 point pairs for the scoring loop;
@@ -1876,16 +1875,22 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
 //   3. per block of 256 trials: lane j builds trials 8j..8j+7 (seed pairs,
 //      src/ransac.cpp:111-123; FP32 coefficients of the line, :35-46) in
 //      registers and scores them against the staged points (the FFMA2 loop
-//      of score_kernel): upper-bound counts, kept as u16 in the slot;
-//   4. the exact argmax / verification / winner mask / LSQ refit of
-//      select_warp_kernel (src/ransac.cpp:158-199, src/velocity.cpp:26-90).
-// HBM sees only the input (16 B/pt), the mask (1 B/pt) and the per-cluster
-// outputs -- no xy64 / xy32 / hypothesis / upper-bound round trips.
+//      of score_kernel): upper-bound counts;
+//   4. (kSelect) the exact argmax / verification / winner mask / LSQ refit
+//      of select_warp_kernel (src/ransac.cpp:158-199, src/velocity.cpp:26-90).
+// Two instantiations:
+//   * whole path (kSelect, 508-point slots): HBM sees only the input
+//     (16 B/pt), the mask and the per-cluster outputs; one launch -- the
+//     default for a call of at most one small-cluster frame;
+//   * prep + score (!kSelect, 384-point slots): steps 1-3, then xy64, the
+//     xy32 pairs, stat and the upper bounds go to HBM for select_warp_kernel
+//     -- the default for batches of small clusters. Without the select code
+//     the hot instructions fit the instruction caches, which the whole-path
+//     kernel does not on full batches.
 // Persistent: warps claim clusters from a counter, so the latency-bound
 // phases of some warps overlap the FMA-bound scoring of the others.
-// Clusters larger than kFusedCap (or calls with T > kFusedMaxT) go to the
+// Clusters larger than the slot (or whole-path calls with T > 1024) go to the
 // list for the CTA path (prep_hyp_kernel -> score_kernel -> select list).
-// 508 points: four 4-warp CTAs per SM fit the 228 KB of shared memory
 constexpr int kFusedWarps = 4;
 
 // One warp's shared-memory slot for clusters of up to kCap points. The pair
