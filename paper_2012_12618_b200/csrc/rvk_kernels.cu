@@ -1715,7 +1715,10 @@ constexpr int kSelectWarps = 4;
 // 5 CTAs per SM (<= 96 registers, a few spills): config 4 select 0.305 ->
 // 0.260 ms against the unbounded 123-register build (4 CTAs); 6 (80
 // registers) measured slower.
-__global__ void __launch_bounds__(kSelectWarps * 32, 5)
+#ifndef RVK_SELECT_WARP_MINB  // A/B builds (RVK_NVCC_FLAGS)
+#define RVK_SELECT_WARP_MINB 5
+#endif
+__global__ void __launch_bounds__(kSelectWarps * 32, RVK_SELECT_WARP_MINB)
 select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                    const double* __restrict__ az, const double* __restrict__ dop,
                    const int32_t* __restrict__ keys, const int32_t* __restrict__ cluster_ids,
