@@ -2117,6 +2117,171 @@ struct PrepScoreOut {
   int Tg;
 };
 
+// Steps 1-2 of a fused warp and the slot's FP32 pairs: normalize, median,
+// MAD interval (kWrite: xy64, stat and the xy32 pairs to HBM as well, for
+// select_warp_kernel). The raw points are read once.
+template <bool kWrite>
+__device__ __forceinline__ void fused_prep_cluster(
+    const double* __restrict__ caz, const double* __restrict__ cdop, int n, int64_t b, int c,
+    double scale, const int64_t* __restrict__ offsets, double* xs, double* ys, float4* pairs,
+    unsigned int* hist, unsigned long long* cand, int lane, const PrepScoreOut& ps,
+    double& thr_lo, double& thr_hi, double& med) {
+  constexpr bool kSelect = !kWrite;
+  // ---- 1. load, min/max, normalize (src/ransac.cpp:69-87)
+  int nb = 32;  // median buckets: about one per point, a power of two
+  while (nb < n) nb <<= 1;
+  for (int i = lane; i < nb; i += 32) hist[i] = 0;
+  double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
+#pragma unroll 2
+  for (int k = lane; k < n; k += 32) {
+    const double a = __ldcs(caz + k), d = __ldcs(cdop + k);  // read once: streaming
+    xs[k] = a;  // raw values, normalized in place below (same lane)
+    ys[k] = d;
+    lo0 = a < lo0 ? a : lo0;
+    hi0 = a > hi0 ? a : hi0;
+    lo1 = d < lo1 ? d : lo1;
+    hi1 = d > hi1 ? d : hi1;
+  }
+  warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
+  __syncwarp();  // the zeroed buckets and the raw slot before any other lane uses them
+  if (lo0 == 0.0 || hi0 == 0.0 || lo1 == 0.0 || hi1 == 0.0) {
+    lo0 = warp_first_zero(lo0, xs, n, lane);
+    hi0 = warp_first_zero(hi0, xs, n, lane);
+    lo1 = warp_first_zero(lo1, ys, n, lane);
+    hi1 = warp_first_zero(hi1, ys, n, lane);
+  }
+  const double s0 = __dsub_rn(hi0, lo0);
+  const double s1 = __dsub_rn(hi1, lo1);
+  {
+    const bool f0 = div_span_ok(s0), f1 = div_span_ok(s1);
+    const double r0 = f0 ? fast_rcp(s0) : 0.0, r1 = f1 ? fast_rcp(s1) : 0.0;
+    for (int k = lane; k < n; k += 32) {
+      const double x = s0 == 0.0 ? 0.5
+                       : (f0 ? div_rn_shared(__dsub_rn(xs[k], lo0), s0, r0)
+                             : __ddiv_rn(__dsub_rn(xs[k], lo0), s0));
+      const double y = s1 == 0.0 ? 0.5
+                       : (f1 ? div_rn_shared(__dsub_rn(ys[k], lo1), s1, r1)
+                             : __ddiv_rn(__dsub_rn(ys[k], lo1), s1));
+      xs[k] = x;
+      ys[k] = y;
+      if (!kSelect) ps.xy64[b + k] = make_double2(x, y);
+      atomicAdd(&hist[med_bin(fused_key(ys, k), nb)], 1u);
+    }
+  }
+  __syncwarp();
+
+  // ---- 2. median (ransac.hpp:53-70) and the MAD interval (prep_cluster)
+  {
+    const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
+    unsigned long long v0 = 0, v1 = 0;
+    fused_select_pair(ys, hist, cand, n, k0, (n & 1) == 0, nb, lane, v0, v1);
+    const double d0 = __longlong_as_double(static_cast<long long>(v0));
+    med = (n & 1) ? d0
+                  : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))),
+                              2.0);
+    double part = 0.0;
+    for (int k = lane; k < n; k += 32)
+      part += fabs(__dsub_rn(__longlong_as_double(static_cast<long long>(fused_key(ys, k))), med));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const double mid = scale * (part / n);
+    const double delta = (4.0 * n + 16.0) * 0x1p-53;
+    thr_lo = mid * (1.0 - delta);
+    thr_hi = mid * (1.0 + delta);
+    if (!kSelect && lane == 0) ps.stat[c] = make_double4(thr_lo, thr_hi, med, CUDART_NAN);
+  }
+  __syncwarp();  // cand and hist are free: the pairs and the upper bounds reuse them
+  // FP32 point pairs (x_2q, x_2q+1, y_2q, y_2q+1) for the scoring loop;
+  // odd n padded with an inert point, plus the loop's read-ahead slack
+  {
+    const int m2 = (n + 1) >> 1;
+    for (int q = lane; q < m2 + 3; q += 32) {
+      float4 v = make_float4(0.f, 0.f, kPadY, kPadY);
+      const int k0 = 2 * q, k1 = 2 * q + 1;
+      if (k0 < n) {
+        v.x = __double2float_rn(xs[k0]);
+        v.z = __double2float_rn(ys[k0]);
+      }
+      if (k1 < n) {
+        v.y = __double2float_rn(xs[k1]);
+        v.w = __double2float_rn(ys[k1]);
+      }
+      pairs[q] = v;
+      if (!kSelect && q < m2)  // the same pair layout as xy32_put's
+        reinterpret_cast<float4*>(ps.xy32 + xy32_base(offsets, c))[q] = v;
+    }
+  }
+  __syncwarp();
+
+}
+
+// Step 3 for one block of 256 trials: lane j builds trials tb + 8j .. +7 in
+// registers and scores them against the slot's point pairs -> cnt[q].
+__device__ __forceinline__ void fused_score_block(int tb, int T, uint64_t seed, uint64_t k1,
+                                              int n, const double* xs, const double* ys,
+                                              const float4* pairs, double thr_lo,
+                                              double thr_hi, int lane,
+                                              uint32_t (&cnt)[kNH]) {
+  const int m2 = (n + 1) >> 1;
+  float A[kNH], B[kNH];
+  float2 Cc[kNH], T2[kNH];
+  // kHU trials per step (independent chains), the code of one step once:
+  // the step's trials enter at slots kNH-kHU.. and the registers rotate
+  // down by kHU, so slot q holds trial 8 lane + q at the end (static
+  // register indices; rotating one trial at a time cost 336 moves per
+  // lane and block, measured)
+  constexpr int kHU = 4;
+#pragma unroll 1
+  for (int q0 = 0; q0 < kNH; q0 += kHU) {
+    FastHyp f[kHU];
+#pragma unroll
+    for (int u = 0; u < kHU; ++u) {
+      const int t = tb + 8 * lane + q0 + u;
+      f[u] = inert_fast();
+      if (t < T) {
+        int i, j;
+        seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
+        f[u] = make_fast_from_seeds(xs[i], ys[i], xs[j], ys[j], thr_lo, thr_hi);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r + kHU < kNH; ++r) {
+      A[r] = A[r + kHU];
+      B[r] = B[r + kHU];
+      Cc[r] = Cc[r + kHU];
+      T2[r] = T2[r + kHU];
+    }
+#pragma unroll
+    for (int u = 0; u < kHU; ++u) {
+      A[kNH - kHU + u] = f[u].A;
+      B[kNH - kHU + u] = f[u].B;
+      Cc[kNH - kHU + u] = make_float2(f[u].C, f[u].C);
+      T2[kNH - kHU + u] = make_float2(-f[u].t2hi, -f[u].t2hi);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kNH; ++q) cnt[q] = 0;
+  auto score_pair = [&](const float4& v) {
+    const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+    for (int h = 0; h < kNH; ++h) {
+      float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
+                            __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
+      e = __ffma2_rn(e, e, T2[h]);
+      cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
+    }
+  };
+  // four pairs per iteration; the padded slack is inert (e^2 overflows)
+#pragma unroll 1
+  for (int q2 = 0; q2 < m2; q2 += 4) {
+    const float4 v0 = pairs[q2], v1 = pairs[q2 + 1], v2 = pairs[q2 + 2], v3 = pairs[q2 + 3];
+    score_pair(v0);
+    score_pair(v1);
+    score_pair(v2);
+    score_pair(v3);
+  }
+}
+
 template <bool kSelect, class G, int kMinBlocks>
 __global__ void __launch_bounds__(kFusedWarps * 32, kMinBlocks)
 fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
@@ -2160,92 +2325,9 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const double* caz = az + b;
     const double* cdop = dop + b;
 
-    // ---- 1. load, min/max, normalize (src/ransac.cpp:69-87)
-    int nb = 32;  // median buckets: about one per point, a power of two
-    while (nb < n) nb <<= 1;
-    for (int i = lane; i < nb; i += 32) hist[i] = 0;
-    double lo0 = DBL_MAX, hi0 = -DBL_MAX, lo1 = DBL_MAX, hi1 = -DBL_MAX;
-#pragma unroll 2
-    for (int k = lane; k < n; k += 32) {
-      const double a = __ldcs(caz + k), d = __ldcs(cdop + k);  // read once: streaming
-      xs[k] = a;  // raw values, normalized in place below (same lane)
-      ys[k] = d;
-      lo0 = a < lo0 ? a : lo0;
-      hi0 = a > hi0 ? a : hi0;
-      lo1 = d < lo1 ? d : lo1;
-      hi1 = d > hi1 ? d : hi1;
-    }
-    warp_minmax2(lo0, hi0, lo1, hi1);  // the loop above never takes a NaN
-    __syncwarp();  // the zeroed buckets and the raw slot before any other lane uses them
-    if (lo0 == 0.0 || hi0 == 0.0 || lo1 == 0.0 || hi1 == 0.0) {
-      lo0 = warp_first_zero(lo0, xs, n, lane);
-      hi0 = warp_first_zero(hi0, xs, n, lane);
-      lo1 = warp_first_zero(lo1, ys, n, lane);
-      hi1 = warp_first_zero(hi1, ys, n, lane);
-    }
-    const double s0 = __dsub_rn(hi0, lo0);
-    const double s1 = __dsub_rn(hi1, lo1);
-    {
-      const bool f0 = div_span_ok(s0), f1 = div_span_ok(s1);
-      const double r0 = f0 ? fast_rcp(s0) : 0.0, r1 = f1 ? fast_rcp(s1) : 0.0;
-      for (int k = lane; k < n; k += 32) {
-        const double x = s0 == 0.0 ? 0.5
-                         : (f0 ? div_rn_shared(__dsub_rn(xs[k], lo0), s0, r0)
-                               : __ddiv_rn(__dsub_rn(xs[k], lo0), s0));
-        const double y = s1 == 0.0 ? 0.5
-                         : (f1 ? div_rn_shared(__dsub_rn(ys[k], lo1), s1, r1)
-                               : __ddiv_rn(__dsub_rn(ys[k], lo1), s1));
-        xs[k] = x;
-        ys[k] = y;
-        if (!kSelect) ps.xy64[b + k] = make_double2(x, y);
-        atomicAdd(&hist[med_bin(fused_key(ys, k), nb)], 1u);
-      }
-    }
-    __syncwarp();
-
-    // ---- 2. median (ransac.hpp:53-70) and the MAD interval (prep_cluster)
     double thr_lo, thr_hi, med;
-    {
-      const int k0 = (n & 1) ? n / 2 : n / 2 - 1;
-      unsigned long long v0 = 0, v1 = 0;
-      fused_select_pair(ys, hist, cand, n, k0, (n & 1) == 0, nb, lane, v0, v1);
-      const double d0 = __longlong_as_double(static_cast<long long>(v0));
-      med = (n & 1) ? d0
-                    : __ddiv_rn(__dadd_rn(d0, __longlong_as_double(static_cast<long long>(v1))),
-                                2.0);
-      double part = 0.0;
-      for (int k = lane; k < n; k += 32)
-        part += fabs(__dsub_rn(__longlong_as_double(static_cast<long long>(fused_key(ys, k))), med));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      const double mid = scale * (part / n);
-      const double delta = (4.0 * n + 16.0) * 0x1p-53;
-      thr_lo = mid * (1.0 - delta);
-      thr_hi = mid * (1.0 + delta);
-      if (!kSelect && lane == 0) ps.stat[c] = make_double4(thr_lo, thr_hi, med, CUDART_NAN);
-    }
-    __syncwarp();  // cand and hist are free: the pairs and the upper bounds reuse them
-    // FP32 point pairs (x_2q, x_2q+1, y_2q, y_2q+1) for the scoring loop;
-    // odd n padded with an inert point, plus the loop's read-ahead slack
-    {
-      const int m2 = (n + 1) >> 1;
-      for (int q = lane; q < m2 + 3; q += 32) {
-        float4 v = make_float4(0.f, 0.f, kPadY, kPadY);
-        const int k0 = 2 * q, k1 = 2 * q + 1;
-        if (k0 < n) {
-          v.x = __double2float_rn(xs[k0]);
-          v.z = __double2float_rn(ys[k0]);
-        }
-        if (k1 < n) {
-          v.y = __double2float_rn(xs[k1]);
-          v.w = __double2float_rn(ys[k1]);
-        }
-        pairs[q] = v;
-        if (!kSelect && q < m2)  // the same pair layout as xy32_put's
-          reinterpret_cast<float4*>(ps.xy32 + xy32_base(offsets, c))[q] = v;
-      }
-    }
-    __syncwarp();
+    fused_prep_cluster<!kSelect>(caz, cdop, n, b, c, scale, offsets, xs, ys, pairs, hist, cand,
+                                 lane, ps, thr_lo, thr_hi, med);
 
     // ---- 3. hypotheses + FP32 upper-bound scoring, 256 trials per block
     const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
@@ -2254,64 +2336,8 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const int m2 = (n + 1) >> 1;
 #pragma unroll 1
     for (int tb = 0; tb < T; tb += 8 * 32) {
-      float A[kNH], B[kNH];
-      float2 Cc[kNH], T2[kNH];
-      // kHU trials per step (independent chains), the code of one step once:
-      // the step's trials enter at slots kNH-kHU.. and the registers rotate
-      // down by kHU, so slot q holds trial 8 lane + q at the end (static
-      // register indices; rotating one trial at a time cost 336 moves per
-      // lane and block, measured)
-      constexpr int kHU = 4;
-#pragma unroll 1
-      for (int q0 = 0; q0 < kNH; q0 += kHU) {
-        FastHyp f[kHU];
-#pragma unroll
-        for (int u = 0; u < kHU; ++u) {
-          const int t = tb + 8 * lane + q0 + u;
-          f[u] = inert_fast();
-          if (t < T) {
-            int i, j;
-            seed_pair_k(seed, k1, static_cast<uint32_t>(t), static_cast<uint32_t>(n), i, j);
-            f[u] = make_fast_from_seeds(xs[i], ys[i], xs[j], ys[j], thr_lo, thr_hi);
-          }
-        }
-#pragma unroll
-        for (int r = 0; r + kHU < kNH; ++r) {
-          A[r] = A[r + kHU];
-          B[r] = B[r + kHU];
-          Cc[r] = Cc[r + kHU];
-          T2[r] = T2[r + kHU];
-        }
-#pragma unroll
-        for (int u = 0; u < kHU; ++u) {
-          A[kNH - kHU + u] = f[u].A;
-          B[kNH - kHU + u] = f[u].B;
-          Cc[kNH - kHU + u] = make_float2(f[u].C, f[u].C);
-          T2[kNH - kHU + u] = make_float2(-f[u].t2hi, -f[u].t2hi);
-        }
-      }
       uint32_t cnt[kNH];
-#pragma unroll
-      for (int q = 0; q < kNH; ++q) cnt[q] = 0;
-      auto score_pair = [&](const float4& v) {
-        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
-#pragma unroll
-        for (int h = 0; h < kNH; ++h) {
-          float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
-                                __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
-          e = __ffma2_rn(e, e, T2[h]);
-          cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
-        }
-      };
-      // four pairs per iteration; the padded slack is inert (e^2 overflows)
-#pragma unroll 1
-      for (int q2 = 0; q2 < m2; q2 += 4) {
-        const float4 v0 = pairs[q2], v1 = pairs[q2 + 1], v2 = pairs[q2 + 2], v3 = pairs[q2 + 3];
-        score_pair(v0);
-        score_pair(v1);
-        score_pair(v2);
-        score_pair(v3);
-      }
+      fused_score_block(tb, T, seed, k1, n, xs, ys, pairs, thr_lo, thr_hi, lane, cnt);
       if (!kSelect) {  // this warp saw every point: plain stores, trials padded to 8
         int32_t* gu = ps.upper + static_cast<int64_t>(c) * ps.Tg * 8;
         if (8 * (tb / 8 + lane) < ps.Tg * 8) {
@@ -2584,6 +2610,7 @@ void launch_prep_score(const FrameDev& f, const rvk_ransac_params& p, const Scra
   if (f.n_clusters == 0) return;
   ScoreGeom g = score_geom(p.max_trials);
   cudaMemsetAsync(s.big_ctl, 0, sizeof(int32_t) * 4, st);
+
   const int64_t want = (static_cast<int64_t>(f.n_clusters) + kFusedWarps - 1) / kFusedWarps;
   const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(false), want));
   const PrepScoreOut ps{s.xy64, s.xy32, s.stat, s.upper, g.Tg};
