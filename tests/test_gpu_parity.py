@@ -608,3 +608,79 @@ np.testing.assert_array_equal(np.concatenate([mask[off[c]:off[c + 1]] for c in v
 assert est[vc].tobytes() == e.tobytes()
 print("ok")
 """
+
+
+_MIXED_BATCH_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2012_12618_b200 as rvk
+from paper_2012_12618_b200 import _native
+from tools import workloads as W
+# > 6144 small clusters (the fused prep + score path) with large clusters
+# (> 384 and > 508 points: the CTA path) interleaved, T = 300
+wi = W.imaging(seed=31, n_clusters=7000, total=1_400_000)
+wa = W.automotive(seed=32, n_clusters=30, lo_pts=300, hi_pts=1800)
+cl = []
+for c in range(wi.n_clusters):
+    s = slice(wi.offsets[c], wi.offsets[c + 1])
+    cl.append(np.stack([wi.azimuth[s], wi.doppler[s]], 1))
+    if c % 250 == 0 and c // 250 < wa.n_clusters:
+        a = c // 250
+        s2 = slice(wa.offsets[a], wa.offsets[a + 1])
+        cl.append(np.stack([wa.azimuth[s2], wa.doppler[s2]], 1))
+off, az, dop = rvk.clusters_to_csr(cl)
+p = rvk.RansacParams(300, 1.0, 12)
+h = hashlib.sha256()
+r, e = rvk.ransac_estimate_csr(off, az, dop, p)
+for a in (r.inlier_count, r.winning_trial, r.mask, e.tobytes()):
+    h.update(np.asarray(a).tobytes() if not isinstance(a, bytes) else a)
+dev = torch.device("cuda", 0)
+d = [torch.from_numpy(a).to(dev) for a in (off, az, dop)]
+C_, P_ = off.size - 1, int(off[-1])
+o = {"inlier_count": torch.zeros(C_, dtype=torch.int32, device=dev),
+     "winning_trial": torch.zeros(C_, dtype=torch.int32, device=dev),
+     "mask": torch.zeros(P_, dtype=torch.uint8, device=dev),
+     "est": torch.zeros(C_ * 48, dtype=torch.uint8, device=dev)}
+rvk.ransac_estimate_device(d[0], d[1], d[2], p, o)
+torch.cuda.synchronize()
+assert (o["inlier_count"].cpu().numpy() == r.inlier_count).all()
+assert (o["mask"].cpu().numpy() == r.mask).all()
+assert o["est"].cpu().numpy().tobytes() == e.tobytes()
+np.save(sys.argv[2], np.concatenate([[0], np.cumsum([len(x) for x in cl])]))
+if len(sys.argv) > 3:  # the large clusters (the CTA path) against the C oracle
+    from oracle.binding import Oracle, make_params
+    orc = Oracle()
+    big = np.nonzero(np.diff(off) > 384)[0]
+    assert big.size >= 10
+    for c in big:
+        ro, _ = orc.ransac_estimate_range(off, az, dop, make_params(300, 1.0, 12), int(c),
+                                          int(c) + 1)
+        s = slice(off[c], off[c + 1])
+        assert (ro.mask[s] == r.mask[s]).all(), c
+        assert ro.winning_trial[c] == r.winning_trial[c] and ro.inlier_count[c] == r.inlier_count[c]
+print(h.hexdigest())
+"""
+
+
+def test_mixed_batch_small_and_large_clusters(gpu_lib, oracle, tmp_path):
+    """A batch of > 6144 small clusters (the fused prep + score path) with
+    clusters of 300-1800 points interleaved (the CTA path: listed by the
+    fused kernel, prepared by persistent CTAs, scored by score_kernel,
+    selected by select_warp_kernel): host and device API agree, every path
+    (default, fused prep+score off, whole-path fused forced) gives the same
+    bytes, and the large clusters match the oracle."""
+    digests = {}
+    for name, env in (("default", {}), ("no_prep_score", {"RVK_PREP_SCORE": "0"}),
+                      ("cta", {"RVK_PREP_SCORE": "0", "RVK_PREP_WARP": "0",
+                               "RVK_SELECT_WARP": "0"})):
+        r = subprocess.run([sys.executable, "-c", _MIXED_BATCH_SCRIPT, ROOT,
+                            str(tmp_path / "off.npy")] + (["check"] if name == "default" else []),
+                           capture_output=True, text=True,
+                           env=dict(os.environ, **env), cwd=ROOT, timeout=900)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        digests[name] = r.stdout.strip().splitlines()[-1]
+    assert len(set(digests.values())) == 1, digests
+    sizes = np.diff(np.load(tmp_path / "off.npy"))
+    assert (sizes > 508).any() and (sizes.size > 6144)
