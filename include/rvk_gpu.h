@@ -145,6 +145,19 @@ int rvk_ransac_estimate_packed(int64_t frame_id, int32_t n_clusters, const int64
                                const int32_t* rng_cluster_index, int32_t* inlier_count,
                                int32_t* winning_trial, uint8_t* mask_bits, rvk_estimate* out);
 
+/* rvk_ransac_estimate with one frame's clusters split over several GPUs for
+ * latency: contiguous cluster ranges of about equal points,
+ * one host thread per range, each on devices[i] (a device may repeat); the RNG
+ * keys and cluster ids stay frame-positional, so the outputs are byte-identical
+ * to the single-device call. Validation and messages as rvk_ransac_estimate,
+ * on the whole frame. */
+int rvk_ransac_estimate_multi(int32_t n_devices, const int32_t* devices, int64_t frame_id,
+                              int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                              const double* doppler, const int32_t* cluster_ids,
+                              const rvk_ransac_params* params, const int32_t* rng_cluster_index,
+                              int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                              rvk_estimate* out);
+
 /* Device-pointer variant of rvk_ransac_estimate (all arrays in HBM, async on
  * `stream`, a cudaStream_t or NULL for the legacy default stream). The
  * caller must keep the inputs alive until the stream reaches this point.

@@ -12,7 +12,8 @@ from .api import (ClusterTooSmall, Cluster, ClusteringParams, DeviceError, Frame
                   extract_clusters, extract_clusters_labels,
                   RansacResult, VelocityEstimate, clusters_to_csr, cluster_thresholds_csr,
                   draw_seed_pair, estimate_all, estimate_all_csr, gather_cluster_points,
-                  ransac_estimate_csr, ransac_estimate_device, run_ransac, run_ransac_csr,
+                  ransac_estimate_csr, ransac_estimate_device, ransac_estimate_multi_csr,
+                  run_ransac, run_ransac_csr,
                   seed_pairs_csr, trial_counts_csr)
 
 __all__ = [
@@ -22,6 +23,7 @@ __all__ = [
     "extract_clusters_labels",
     "RansacResult", "VelocityEstimate", "clusters_to_csr", "cluster_thresholds_csr",
     "draw_seed_pair", "estimate_all", "estimate_all_csr", "gather_cluster_points",
-    "ransac_estimate_csr", "ransac_estimate_device", "run_ransac", "run_ransac_csr",
+    "ransac_estimate_csr", "ransac_estimate_device", "ransac_estimate_multi_csr",
+    "run_ransac", "run_ransac_csr",
     "seed_pairs_csr", "trial_counts_csr",
 ]

@@ -67,6 +67,8 @@ GPU_SIGNATURES = {
     "rvk_ransac_estimate": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "rvk_ransac_estimate_packed": (C.c_int, [_I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                                              _P]),
+    "rvk_ransac_estimate_multi": (C.c_int, [_I32, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                                            _P, _P]),
     "rvk_ransac_estimate_device": (C.c_int, [_I64, _I32, _I64, _P, _P, _P, _P, _P, _P, _P, _P,
                                              _P, _P, _P]),
     "rvk_trial_counts": (C.c_int, [_I32, _P, _P, _P, _P, _P, _P]),

@@ -215,6 +215,27 @@ def ransac_estimate_csr(offsets, azimuth, doppler, params: RansacParams, frame_i
     return RansacResult(cnt, tr, mask), est
 
 
+def ransac_estimate_multi_csr(offsets, azimuth, doppler, params: RansacParams, devices,
+                              frame_id: int = 0, cluster_ids=None, rng_cluster_index=None):
+    """rvk_ransac_estimate_multi: one frame's clusters split over `devices`
+    (CUDA ordinals, may repeat), byte-identical to ransac_estimate_csr."""
+    offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)
+    n = offsets.size - 1
+    cnt = np.zeros(n, np.int32)
+    tr = np.zeros(n, np.int32)
+    mask = np.zeros(azimuth.size, np.uint8)
+    est = np.zeros(n, N.ESTIMATE_DTYPE)
+    ids = _opt_i32(cluster_ids, n)
+    keys = _opt_i32(rng_cluster_index, n)
+    devs = np.ascontiguousarray(devices, np.int32)
+    p = params.c()
+    _check(N.gpu().rvk_ransac_estimate_multi(devs.size, N.ptr(devs), frame_id, n, N.ptr(offsets),
+                                             N.ptr(azimuth), N.ptr(doppler), N.ptr(ids),
+                                             C.addressof(p), N.ptr(keys), N.ptr(cnt), N.ptr(tr),
+                                             N.ptr(mask), N.ptr(est)))
+    return RansacResult(cnt, tr, mask), est
+
+
 def estimate_all_csr(offsets, azimuth, doppler, mask, frame_id: int = 0, cluster_ids=None):
     """rvk_estimate_all: LSQ refit + heading for caller masks (uint8 [P])."""
     offsets, azimuth, doppler = _csr(offsets, azimuth, doppler)

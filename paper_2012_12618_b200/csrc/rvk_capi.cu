@@ -9,14 +9,17 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -245,6 +248,62 @@ void lpt_order(int32_t n_clusters, const int64_t* offsets, int32_t* order) {
   std::stable_sort(order, order + n_clusters, [&](int32_t a, int32_t b) {
     return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
   });
+}
+
+// Persistent host workers for rvk_ransac_estimate_multi: part 0 runs on the
+// caller, part i > 0 on worker i, which keeps its thread_local per-device
+// contexts (streams, pinned and device buffers) across calls. One multi call
+// at a time per process; the pool is never torn down (workers park on a
+// condition variable at exit).
+class MultiPool {
+ public:
+  void run(int n, const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> call(call_m_);
+    while (static_cast<int>(w_.size()) < n - 1) w_.emplace_back(new Worker(static_cast<int>(w_.size()) + 1));
+    for (int i = 0; i < n - 1; ++i) w_[i]->post(&f);
+    f(0);
+    for (int i = 0; i < n - 1; ++i) w_[i]->wait();
+  }
+
+ private:
+  struct Worker {
+    explicit Worker(int idx) : idx(idx), t([this] { loop(); }) { t.detach(); }
+    void post(const std::function<void(int)>* f) {
+      std::lock_guard<std::mutex> g(m);
+      job = f;
+      cv.notify_all();
+    }
+    void wait() {
+      std::unique_lock<std::mutex> g(m);
+      cv.wait(g, [this] { return job == nullptr; });
+    }
+    void loop() {
+      for (;;) {
+        const std::function<void(int)>* f;
+        {
+          std::unique_lock<std::mutex> g(m);
+          cv.wait(g, [this] { return job != nullptr; });
+          f = job;
+        }
+        (*f)(idx);
+        std::lock_guard<std::mutex> g(m);
+        job = nullptr;
+        cv.notify_all();
+      }
+    }
+    const int idx;
+    std::mutex m;
+    std::condition_variable cv;
+    const std::function<void(int)>* job = nullptr;
+    std::thread t;
+  };
+  std::mutex call_m_;
+  std::vector<Worker*> w_;
+};
+
+MultiPool& multi_pool() {
+  static MultiPool* p = new MultiPool;  // intentionally leaked, see above
+  return *p;
 }
 
 template <class F>
@@ -839,6 +898,74 @@ int rvk_ransac_estimate_packed(int64_t frame_id, int32_t n_clusters, const int64
     return ransac_estimate_host(frame_id, n_clusters, offsets, azimuth, doppler, cluster_ids,
                                 params, rng_cluster_index, inlier_count, winning_trial, mask_bits,
                                 out, true, true);
+  });
+}
+
+int rvk_ransac_estimate_multi(int32_t n_devices, const int32_t* devices, int64_t frame_id,
+                              int32_t n_clusters, const int64_t* offsets, const double* azimuth,
+                              const double* doppler, const int32_t* cluster_ids,
+                              const rvk_ransac_params* params, const int32_t* rng_cluster_index,
+                              int32_t* inlier_count, int32_t* winning_trial, uint8_t* mask,
+                              rvk_estimate* out) {
+  return guarded([&]() -> int {
+    if (n_devices < 1 || devices == nullptr)
+      return fail(RVK_EINVAL, "rvk_ransac_estimate_multi: need at least one device");
+    // the reference's checks on the whole frame first, so messages and the
+    // offending cluster index refer to the caller's frame
+    int st = validate_params(params, "run_ransac");
+    if (st != RVK_OK) return st;
+    st = validate_offsets(n_clusters, offsets, kMinClusterSize, "run_ransac");
+    if (st != RVK_OK) return st;
+    if (n_clusters == 0) return RVK_OK;
+    if ((azimuth == nullptr || doppler == nullptr) && offsets[n_clusters] > 0)
+      return fail(RVK_EINVAL, "run_ransac: null point arrays");
+    // contiguous cluster ranges of about equal points (the work is T x points)
+    const int64_t P = offsets[n_clusters];
+    std::vector<int32_t> cut(1, 0);
+    for (int i = 1; i < n_devices; ++i) {
+      int32_t c = cut.back();
+      while (c < n_clusters && offsets[c] < P * i / n_devices) ++c;
+      cut.push_back(c);
+    }
+    cut.push_back(n_clusters);
+    struct Part {
+      int status = RVK_OK;
+      std::string error;
+      int32_t error_cluster = -1;
+    };
+    std::vector<Part> part(n_devices);
+    auto work = [&](int i) {
+      const int32_t c0 = cut[i], nc = cut[i + 1] - cut[i];
+      if (nc == 0) return;
+      part[i].status = guarded([&]() -> int {
+        RVK_CUDA(cudaSetDevice(devices[i]));
+        std::vector<int64_t> off(static_cast<size_t>(nc) + 1);
+        std::vector<int32_t> key(static_cast<size_t>(nc)), ids(static_cast<size_t>(nc));
+        for (int32_t j = 0; j <= nc; ++j) off[j] = offsets[c0 + j] - offsets[c0];
+        for (int32_t j = 0; j < nc; ++j) {  // RNG keys and ids stay frame-positional
+          key[j] = rng_cluster_index ? rng_cluster_index[c0 + j] : c0 + j;
+          ids[j] = cluster_ids ? cluster_ids[c0 + j] : c0 + j;
+        }
+        const int64_t p0 = offsets[c0];
+        return ransac_estimate_host(frame_id, nc, off.data(), azimuth + p0, doppler + p0,
+                                    ids.data(), params, key.data(),
+                                    inlier_count ? inlier_count + c0 : nullptr,
+                                    winning_trial ? winning_trial + c0 : nullptr,
+                                    mask ? mask + p0 : nullptr, out ? out + c0 : nullptr, true);
+      });
+      part[i].error = g_error;
+      part[i].error_cluster = g_error_cluster >= 0 ? g_error_cluster + c0 : -1;
+    };
+    int saved = 0;
+    RVK_CUDA(cudaGetDevice(&saved));
+    multi_pool().run(n_devices, work);
+    cudaSetDevice(saved);
+    for (const Part& q : part)
+      if (q.status != RVK_OK) {
+        g_error_cluster = q.error_cluster;
+        return fail(q.status, "%s", q.error.c_str());
+      }
+    return RVK_OK;
   });
 }
 

@@ -684,3 +684,28 @@ def test_mixed_batch_small_and_large_clusters(gpu_lib, oracle, tmp_path):
     assert len(set(digests.values())) == 1, digests
     sizes = np.diff(np.load(tmp_path / "off.npy"))
     assert (sizes > 508).any() and (sizes.size > 6144)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0, 0]])
+def test_multi_device_split_is_byte_identical(gpu_lib, devices):
+    """rvk_ransac_estimate_multi (single-frame latency): the frame
+    split into point-balanced cluster ranges, one host worker per entry of
+    `devices` (the one GPU repeated here); RNG keys and ids stay frame-positional,
+    so every output equals the single call byte for byte -- with and without
+    caller keys/ids, and more parts than clusters."""
+    cases = [W.single_frame(), W.automotive(seed=8, n_clusters=60),
+             W.imaging(seed=9, n_clusters=900, total=200_000)]
+    for w in cases:
+        p = rvk.RansacParams(w.max_trials, w.threshold_scale, 5)
+        C_ = w.offsets.size - 1
+        for ids, keys in [(None, None), (np.arange(C_)[::-1] + 7, (np.arange(C_) * 3) % 1000)]:
+            r, e = rvk.ransac_estimate_csr(w.offsets, w.azimuth, w.doppler, p, frame_id=4,
+                                           cluster_ids=ids, rng_cluster_index=keys)
+            for _ in range(2):  # the second call reuses the workers' contexts
+                rm, em = rvk.ransac_estimate_multi_csr(w.offsets, w.azimuth, w.doppler, p,
+                                                       devices, frame_id=4, cluster_ids=ids,
+                                                       rng_cluster_index=keys)
+                np.testing.assert_array_equal(rm.mask, r.mask)
+                np.testing.assert_array_equal(rm.inlier_count, r.inlier_count)
+                np.testing.assert_array_equal(rm.winning_trial, r.winning_trial)
+                assert em.tobytes() == e.tobytes()

@@ -147,6 +147,14 @@ def test_host_validation_without_gpu():
     # params are checked before cluster sizes (src/ransac.cpp:140-154)
     with pytest.raises(ValueError):
         rvk.run_ransac_csr(off, az, az, rvk.RansacParams(max_trials=0))
+    # the multi-device split validates the whole frame first: the index is frame-global
+    off4 = np.array([0, 5, 10, 15, 17], np.int64)
+    with pytest.raises(rvk.ClusterTooSmall, match="cluster 3 has 2 points") as e:
+        rvk.ransac_estimate_multi_csr(off4, np.zeros(17), np.zeros(17), rvk.RansacParams(),
+                                      [0, 0])
+    assert e.value.cluster == 3
+    with pytest.raises(ValueError, match="at least one device"):
+        rvk.ransac_estimate_multi_csr(off, az, az, rvk.RansacParams(), [])
     # empty input -> empty output, no device work
     r = rvk.run_ransac_csr(np.array([0], np.int64), np.zeros(0), np.zeros(0), rvk.RansacParams())
     assert r.inlier_count.size == 0
