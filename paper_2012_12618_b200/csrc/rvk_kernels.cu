@@ -1715,6 +1715,36 @@ constexpr int kSelectWarps = 4;
 // 5 CTAs per SM (<= 96 registers, a few spills): config 4 select 0.305 ->
 // 0.260 ms against the unbounded 123-register build (4 CTAs); 6 (80
 // registers) measured slower.
+// Asynchronous global -> shared copies (LDGSTS) and their completion.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// A warp's shared slot: the cluster's FP32 pairs and raw az / dop.
+constexpr int kSelStage = 384;
+struct SelSlot {
+  float4 p32[kSelStage / 2];
+  double az[kSelStage];
+  double dop[kSelStage];
+};
+constexpr size_t kSelSmem = sizeof(SelSlot) * kSelectWarps;
+extern __shared__ __align__(16) unsigned char sel_dyn[];
+
 #ifndef RVK_SELECT_WARP_MINB  // A/B builds (RVK_NVCC_FLAGS)
 #define RVK_SELECT_WARP_MINB 5
 #endif
@@ -1747,6 +1777,21 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   uint8_t* cmask = mask + b;
   const int32_t* U = upper + static_cast<int64_t>(c) * ((T + 7) / 8) * 8;
   const bool refit = est != nullptr;
+  // the passes read every point: a cluster of <= kSelStage points is copied
+  // into the warp's shared slot (cp.async) while the upper bounds are scanned
+  // and t0's line is built, instead of one global round trip per 64 points
+  const bool staged = n <= kSelStage;
+  if (staged) {
+    SelSlot& sl = reinterpret_cast<SelSlot*>(sel_dyn)[threadIdx.x >> 5];
+    const float4* g4 = reinterpret_cast<const float4*>(p32);
+    for (int q = lane; 2 * q < n; q += 32) cp_async16(sl.p32 + q, g4 + q);
+    if (refit)
+      for (int k = lane; k < n; k += 32) {
+        cp_async8(sl.az + k, caz + k);
+        cp_async8(sl.dop + k, cdop + k);
+      }
+    cp_async_commit();
+  }
 
   auto go_exact = [&]() {  // the exact sequential threshold (rare)
     double t = 0.0;
@@ -1809,6 +1854,14 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const int u0 = unpack_count(v);
 
   // 2. its exact count, mask and refit sums in one pass
+  if (staged) {
+    SelSlot& sl = reinterpret_cast<SelSlot*>(sel_dyn)[threadIdx.x >> 5];
+    cp_async_wait_all();
+    __syncwarp();
+    p32 = reinterpret_cast<const float2*>(sl.p32);
+    caz = sl.az;
+    cdop = sl.dop;
+  }
   int e0 = 0;
   RefitAcc tot;
   if (!pass(t0, e0, tot)) {
@@ -2768,8 +2821,8 @@ void launch_select(const FrameDev& f, const rvk_ransac_params& p, const Scratch&
     return;
   }
   if (prep_score_path(f, p) || env_int("RVK_SELECT_WARP", avg < 384 ? 1 : 0) != 0) {
-    select_warp_kernel<<<(f.n_clusters + kSelectWarps - 1) / kSelectWarps, kSelectWarps * 32, 0,
-                         st>>>(f.n_clusters, f.offsets, f.azimuth, f.doppler, f.keys,
+    select_warp_kernel<<<(f.n_clusters + kSelectWarps - 1) / kSelectWarps, kSelectWarps * 32,
+                         kSelSmem, st>>>(f.n_clusters, f.offsets, f.azimuth, f.doppler, f.keys,
                                f.cluster_ids, f.frame_id, s.xy64, s.xy32, s.stat,
                                p.threshold_scale, s.upper, p.max_trials, p.rng_seed,
                                o.inlier_count, o.winning_trial, o.mask, o.est);

@@ -148,6 +148,28 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
             cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
           }
         }
+      } else if (V == 9 || V == 10) {
+        // V=9: V=2 with the hypothesis scaled so that t = 1: the square step
+        // as two scalar FFMA with the immediate -1 (FFMA imm-form)
+        // V=10: the same as FFMA2 with a constant (-1, -1)
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float a = hh ? h.A[q].y : h.A[q].x, b = hh ? h.B[q].y : h.B[q].x;
+            const float c = hh ? h.C[q].y : h.C[q].x;
+            const float2 e = __ffma2_rn(X, make_float2(a, a), __ffma2_rn(Y, make_float2(b, b), make_float2(c, c)));
+            float2 g;
+            if (V == 9) {
+              g.x = __fmaf_rn(e.x, e.x, -1.0f);
+              g.y = __fmaf_rn(e.y, e.y, -1.0f);
+            } else {
+              g = __ffma2_rn(e, e, make_float2(-1.0f, -1.0f));
+            }
+            cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+          }
+        }
       } else {
         // v = (x1, x2, y1, y2)
         const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
@@ -225,6 +247,10 @@ int main() {
   }
   run<2, 256, 2, 2>(sms, peak, du);
   run<2, 128, 4, 2>(sms, peak, du);
+  run<9, 256, 2, 2>(sms, peak, du);
+  run<9, 128, 4, 2>(sms, peak, du);
+  run<10, 256, 2, 2>(sms, peak, du);
+  run<10, 128, 4, 2>(sms, peak, du);
   run<6, 256, 2, 2>(sms, peak, du);
   run<6, 128, 4, 2>(sms, peak, du);
   run<7, 256, 2, 2>(sms, peak, du);
