@@ -1735,6 +1735,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// (t0, u0) -- the trial with the largest upper bound and that bound -- in
+// stat.w: the bits (u0 << 32 | t0) are a zero or subnormal double (u0 < 2^20),
+// never the NaN the prep kernels leave there.
+__device__ __forceinline__ double pack_t0(int t0, int u0) {
+  return __longlong_as_double((static_cast<long long>(u0) << 32) | static_cast<uint32_t>(t0));
+}
+__device__ __forceinline__ int unpack_t0_trial(double w) {
+  return static_cast<int>(static_cast<uint32_t>(__double_as_longlong(w)));
+}
+__device__ __forceinline__ int unpack_t0_count(double w) {
+  return static_cast<int>(__double_as_longlong(w) >> 32);
+}
+
 // A warp's shared slot: the cluster's FP32 pairs and raw az / dop.
 constexpr int kSelStage = 384;
 struct SelSlot {
@@ -1836,9 +1849,12 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     return true;
   };
 
-  // 1. trial with the largest upper bound (lowest index on ties)
+  // 1. trial with the largest upper bound (lowest index on ties): handed over
+  //    in stat.w by the fused prep + score kernel, else a scan of the bounds
   unsigned long long v = 0;
-  {
+  if (!isnan(st.w)) {
+    v = pack_best(unpack_t0_count(st.w), unpack_t0_trial(st.w));
+  } else {
     const int4* U4 = reinterpret_cast<const int4*>(U);
     for (int q = lane; 4 * q < T; q += 32) {
       const int4 w = U4[q];
@@ -1848,8 +1864,8 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
       if (t + 2 < T) v = MaxU64()(v, pack_best(w.z, t + 2));
       if (t + 3 < T) v = MaxU64()(v, pack_best(w.w, t + 3));
     }
+    v = warp_reduce(v, MaxU64());
   }
-  v = warp_reduce(v, MaxU64());
   const int t0 = unpack_trial(v);
   const int u0 = unpack_count(v);
 
@@ -2398,6 +2414,10 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
           g4[0] = make_int4(cnt[0], cnt[1], cnt[2], cnt[3]);
           g4[1] = make_int4(cnt[4], cnt[5], cnt[6], cnt[7]);
         }
+#pragma unroll
+        for (int q = 0; q < kNH; ++q)
+          if (tb + 8 * lane + q < T)
+            vbest = MaxU64()(vbest, pack_best(static_cast<int>(cnt[q]), tb + 8 * lane + q));
         continue;
       }
 #pragma unroll
@@ -2409,7 +2429,9 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
         }
       }
     }
-    if (!kSelect) {  // select_warp_kernel takes it from here
+    if (!kSelect) {  // select_warp_kernel takes it from here, t0 and u0 in stat.w
+      vbest = warp_reduce(vbest, MaxU64());
+      if (lane == 0) ps.stat[c].w = pack_t0(unpack_trial(vbest), unpack_count(vbest));
       __syncwarp();
       continue;
     }
