@@ -1708,13 +1708,16 @@ select_kernel(const int64_t* __restrict__ offsets, const double* __restrict__ az
 // of a few hundred points, where select_kernel's CTAs spend their time in
 // barrier and latency chains). Candidates are found 32 trials at a time
 // with a ballot over the upper bounds.
-constexpr int kSelectWarps = 4;
+// One-warp CTAs, 20 per SM (<= 102 registers: 94, no spills): a finished
+// warp frees its slot at once (config 4 select 0.239 -> 0.234 ms against
+// 4-warp CTAs; 2-warp CTAs 0.240, 24 warps at 80 registers 0.236). Round 2
+// before: 5 CTAs of 4 warps took 0.305 -> 0.260 ms against the unbounded
+// 123-register build.
+#ifndef RVK_SELECT_WARPS  // A/B builds (RVK_NVCC_FLAGS)
+#define RVK_SELECT_WARPS 1
+#endif
+constexpr int kSelectWarps = RVK_SELECT_WARPS;
 
-
-
-// 5 CTAs per SM (<= 96 registers, a few spills): config 4 select 0.305 ->
-// 0.260 ms against the unbounded 123-register build (4 CTAs); 6 (80
-// registers) measured slower.
 // Asynchronous global -> shared copies (LDGSTS) and their completion.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
@@ -1759,7 +1762,7 @@ constexpr size_t kSelSmem = sizeof(SelSlot) * kSelectWarps;
 extern __shared__ __align__(16) unsigned char sel_dyn[];
 
 #ifndef RVK_SELECT_WARP_MINB  // A/B builds (RVK_NVCC_FLAGS)
-#define RVK_SELECT_WARP_MINB 5
+#define RVK_SELECT_WARP_MINB (20 / kSelectWarps)
 #endif
 __global__ void __launch_bounds__(kSelectWarps * 32, RVK_SELECT_WARP_MINB)
 select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,

@@ -42,6 +42,8 @@ def main():
     rvk.ransac_estimate_csr(wi.offsets, wi.azimuth, wi.doppler, p, packed_mask=True)
     with rvk.FrameStream(p, depth=2) as fs:
         fs.result(fs.submit(wi.offsets, wi.azimuth, wi.doppler, packed_mask=True))
+    # one frame split over two workers (the multi-GPU latency API, one device here)
+    rvk.ransac_estimate_multi_csr(wi.offsets, wi.azimuth, wi.doppler, p, [0, 0])
     # device API with clusters below the minimum (sentinel path)
     import torch
     sizes = np.array([30, 1, 0, 2, 600, 5])
