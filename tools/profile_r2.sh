@@ -3,7 +3,7 @@
 #   step (16 frames) per configuration. Outputs under gpurun_out/.
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_cli.py tests/test_gpu_parity.py -m gpu -x -q -k "cli or bench_harness or too_small or packed" > gpurun_out/r2d_pytest.log 2>&1; tail -3 gpurun_out/r2d_pytest.log
+timeout 900 python -m pytest tests/test_cli.py tests/test_gpu_parity.py -m gpu -x -q -k "cli or bench_harness or too_small or packed or multi" > gpurun_out/r2d_pytest.log 2>&1; tail -3 gpurun_out/r2d_pytest.log
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r2_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 2 --latency-reps 3 > gpurun_out/r2_launches_bench.log 2>&1
 for spec in "4 256" "4 1024" "2 0" "3 0"; do
