@@ -2302,7 +2302,10 @@ __device__ __forceinline__ void fused_score_block(int tb, int T, uint64_t seed, 
   // down by kHU, so slot q holds trial 8 lane + q at the end (static
   // register indices; rotating one trial at a time cost 336 moves per
   // lane and block, measured)
-  constexpr int kHU = 4;
+#ifndef RVK_FUSED_HU  // A/B builds (RVK_NVCC_FLAGS)
+#define RVK_FUSED_HU 4
+#endif
+  constexpr int kHU = RVK_FUSED_HU;
 #pragma unroll 1
   for (int q0 = 0; q0 < kNH; q0 += kHU) {
     FastHyp f[kHU];
@@ -2405,7 +2408,6 @@ fused_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
     const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
     const uint64_t k1 = seed_key(key);
     unsigned long long vbest = 0;
-    const int m2 = (n + 1) >> 1;
 #pragma unroll 1
     for (int tb = 0; tb < T; tb += 8 * 32) {
       uint32_t cnt[kNH];
