@@ -1776,6 +1776,10 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * kSelectWarps + (threadIdx.x >> 5);
   if (c >= n_clusters) return;
+  // stat and the key do not depend on the offsets: their loads go out first,
+  // so the two global latencies overlap (stat is in-bounds for every cluster)
+  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
+  const double4 st = stat[c];
   const int64_t b = offsets[c];
   const int n = static_cast<int>(offsets[c + 1] - b);
   if (n < kMinClusterPoints) {
@@ -1783,8 +1787,6 @@ select_warp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                     mask + b, est, lane, 32);
     return;
   }
-  const uint32_t key = keys ? static_cast<uint32_t>(keys[c]) : static_cast<uint32_t>(c);
-  const double4 st = stat[c];
   double thr_lo = st.x, thr_hi = st.y;
   const float2* p32 = xy32 + xy32_base(offsets, c);
   const double2* p64 = xy64 + b;
