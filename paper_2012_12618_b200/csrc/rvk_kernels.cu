@@ -1973,7 +1973,10 @@ constexpr int kFusedWarps = 4;
 // One warp's shared-memory slot for clusters of up to kCap points. The pair
 // region holds the median's candidates until the pairs are written (after
 // the median); the bucket region holds the u16 upper bounds after it.
-template <int kCap>
+// kHistInPairs (prep + score: no u16 upper bounds in the slot): the buckets
+// live in the pair region too, after the candidates -- both are dead once
+// the pairs are written -- so the slot is 18 % smaller.
+template <int kCap, bool kHistInPairs = false>
 struct FusedGeom {
   static constexpr int cap = kCap;
   static constexpr int hist = kCap <= 256 ? 256 : 512;  // median buckets (power of two >= cap)
@@ -1981,18 +1984,26 @@ struct FusedGeom {
   static constexpr int pairs = kCap / 2 + 3;            // float4 (two points), + read-ahead
   static constexpr size_t x = 0;                        // double x[cap]  (normalized)
   static constexpr size_t y = x + 8 * kCap;             // double y[cap]  (normalized)
-  static constexpr size_t p = y + 8 * kCap;             // float4 pairs | u64 cand
-  static constexpr size_t h = p + 16 * pairs;           // u32 hist | u16 upper
-  static constexpr size_t slot = h + 4 * hist;
+  static constexpr size_t p = y + 8 * kCap;             // float4 pairs | u64 cand (| u32 hist)
+  static constexpr size_t h = kHistInPairs ? p + 8 * kWarpCand  // u32 hist | u16 upper
+                                           : p + 16 * pairs;
+  static constexpr size_t slot = kHistInPairs ? p + 16 * pairs : h + 4 * hist;
   static constexpr size_t smem = slot * kFusedWarps;
   static_assert(8 * kWarpCand <= 16 * pairs, "median candidates live in the pair region");
+  static_assert(!kHistInPairs || 8 * kWarpCand + 4 * hist <= 16 * pairs, "buckets in pairs");
   static_assert(kCap <= 512, "bucket region");
 };
+#ifndef RVK_FUSED_PS_HIP  // A/B builds (RVK_NVCC_FLAGS): prep + score buckets in the pair region
+#define RVK_FUSED_PS_HIP 1
+#endif
+#ifndef RVK_FUSED_PS_MINB  // A/B builds: prep + score CTAs per SM (register budget)
+#define RVK_FUSED_PS_MINB 5
+#endif
 // the whole path, one warp per cluster: 508 points, four 4-warp CTAs per SM
 using FusedFull = FusedGeom<508>;
 // prep + score only (select_warp_kernel follows): 384 points (every config-4
 // cluster), five 4-warp CTAs per SM at <= 102 registers
-using FusedPrepScore = FusedGeom<384>;
+using FusedPrepScore = FusedGeom<384, RVK_FUSED_PS_HIP != 0>;
 constexpr int kFusedCap = FusedFull::cap;
 constexpr int kFusedMaxT = FusedFull::max_t;
 
@@ -2696,7 +2707,7 @@ void launch_prep_score(const FrameDev& f, const rvk_ransac_params& p, const Scra
   const int64_t want = (static_cast<int64_t>(f.n_clusters) + kFusedWarps - 1) / kFusedWarps;
   const int grid = static_cast<int>(std::min<int64_t>(fused_resident_ctas(false), want));
   const PrepScoreOut ps{s.xy64, s.xy32, s.stat, s.upper, g.Tg};
-  fused_warp_kernel<false, FusedPrepScore, 5><<<grid, kFusedWarps * 32, FusedPrepScore::smem,
+  fused_warp_kernel<false, FusedPrepScore, RVK_FUSED_PS_MINB><<<grid, kFusedWarps * 32, FusedPrepScore::smem,
                                                  st>>>(
       f.n_clusters, f.offsets, f.azimuth, f.doppler, p.threshold_scale, f.keys, f.cluster_ids,
       f.frame_id, p.max_trials, p.rng_seed, nullptr, nullptr, nullptr, nullptr, s.big_list,
@@ -2786,7 +2797,7 @@ int fused_resident_ctas(bool select) {
   if (g == 0) {
     int per_sm = 0;
     auto k = select ? fused_warp_kernel<true, FusedFull, 4>
-                    : fused_warp_kernel<false, FusedPrepScore, 5>;
+                    : fused_warp_kernel<false, FusedPrepScore, RVK_FUSED_PS_MINB>;
     const size_t smem = select ? FusedFull::smem : FusedPrepScore::smem;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kFusedWarps * 32, smem);

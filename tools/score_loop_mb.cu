@@ -18,6 +18,12 @@ __device__ __forceinline__ uint32_t hsh(uint32_t x) {
 }
 __device__ __forceinline__ float u01(uint32_t x) { return (hsh(x) >> 8) * (1.0f / 16777216.0f); }
 
+__device__ __forceinline__ uint32_t le_mask(float e, float t) {
+  uint32_t m;
+  asm("set.le.u32.f32 %0, %1, %2;" : "=r"(m) : "f"(fabsf(e)), "f"(t));
+  return m;
+}
+
 struct Hy { float2 A[4], B[4], C[4], T[4]; };
 __device__ __forceinline__ void init_h(Hy& h, uint32_t base) {
 #pragma unroll
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
           cnt[2 * q] += __float_as_uint(eb.x) >> 31;
           cnt[2 * q + 1] += __float_as_uint(eb.y) >> 31;
         }
-      } else if (V >= 6) {
+      } else if (V >= 6 && V <= 8) {
         // V=6: as V=2 but the square step as two scalar FFMA
         // V=7: as V=2 but the B step as two scalar FFMA
         // V=8: all scalar FFMA (3 per eval)
@@ -168,6 +174,29 @@ __global__ void __launch_bounds__(TH, MINB) loop_mb(int reps, uint32_t* out) {
               g = __ffma2_rn(e, e, make_float2(-1.0f, -1.0f));
             }
             cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+          }
+        }
+      } else if (V >= 11 && V <= 14) {
+        // V=11..14: V=2 with the last NL hypotheses of the 8 scored by the
+        // linear compare |e| <= thi on the ALU pipe (FSET -> 0 / -1 masks,
+        // one IADD3 per two masks) instead of the square step (FFMA2) and the
+        // sign count: NL = 4, 3, 2, 8 -- balances the FMA and ALU pipes
+        constexpr int NL = V == 11 ? 4 : V == 12 ? 3 : V == 13 ? 2 : 8;
+        const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float a = hh ? h.A[q].y : h.A[q].x, b = hh ? h.B[q].y : h.B[q].x;
+            const float c = hh ? h.C[q].y : h.C[q].x, t = hh ? h.T[q].y : h.T[q].x;
+            const float2 e = __ffma2_rn(X, make_float2(a, a), __ffma2_rn(Y, make_float2(b, b), make_float2(c, c)));
+            if (2 * q + hh >= 8 - NL) {
+              const float tl = sqrtf(-t);  // (hoisted: loop-invariant)
+              cnt[2 * q + hh] -= le_mask(e.x, tl) + le_mask(e.y, tl);
+            } else {
+              const float2 g = __ffma2_rn(e, e, make_float2(t, t));
+              cnt[2 * q + hh] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+            }
           }
         }
       } else {
@@ -247,6 +276,12 @@ int main() {
   }
   run<2, 256, 2, 2>(sms, peak, du);
   run<2, 128, 4, 2>(sms, peak, du);
+  run<11, 256, 2, 2>(sms, peak, du);
+  run<11, 128, 4, 2>(sms, peak, du);
+  run<12, 256, 2, 2>(sms, peak, du);
+  run<12, 128, 4, 2>(sms, peak, du);
+  run<13, 256, 2, 2>(sms, peak, du);
+  run<14, 256, 2, 2>(sms, peak, du);
   run<9, 256, 2, 2>(sms, peak, du);
   run<9, 128, 4, 2>(sms, peak, du);
   run<10, 256, 2, 2>(sms, peak, du);
