@@ -53,6 +53,38 @@ namespace {
 constexpr int kPrepThreads = 256;
 constexpr int kSelectThreads = 256;
 constexpr int kNH = 8;            // hypotheses per scoring thread (four FFMA2 pairs)
+
+// Sign counting in the scoring loops. g = e^2 - t2hi comes out of FFMA2 as a
+// pair (point 2q in .x, point 2q+1 in .y); a point is a possible inlier when
+// its g is negative. RVK_SIGN_PRMT=0: one LEA.HI per point (cnt += bits >> 31).
+// RVK_SIGN_PRMT=1: one PRMT per pair packs both signs, sign-replicated, into
+// the bytes (sx, sx, sy, sy) = 65535 sx - 65536 sy (mod 2^32), and one IADD3
+// adds two such words to the accumulator: 1.5 ALU instructions per pair
+// instead of 2. After A even-point and B odd-point hits the accumulator holds
+// V = 65535 A - 65536 B (mod 2^32): A = -V mod 2^16 (A < 2^16), and
+// A - B = (V + A) / 2^16 as a signed value, so the count A + B is exact.
+// Measured (B200, profiles/r2_sign_prmt.md): score_kernel 0.924 -> 0.915 ms on
+// config 3, 0.249 -> 0.248 ms on config 2 (kept); the fused prep + score
+// kernel 0.900 -> 0.909 ms at T = 256, 2.681 -> 2.672 ms at T = 1024 (off).
+#ifndef RVK_SIGN_PRMT  // A/B builds (RVK_NVCC_FLAGS): score_kernel
+#define RVK_SIGN_PRMT 1
+#endif
+#ifndef RVK_FUSED_SIGN_PRMT  // A/B builds: fused_score_block
+#define RVK_FUSED_SIGN_PRMT 0
+#endif
+__device__ __forceinline__ uint32_t sign_pair(float2 g) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0xFFBB;"
+      : "=r"(r)
+      : "r"(__float_as_uint(g.x)), "r"(__float_as_uint(g.y)));
+  return r;
+}
+__device__ __forceinline__ uint32_t sign_pair_count(uint32_t v) {
+  const uint32_t a = (0u - v) & 0xFFFFu;
+  const int32_t a_minus_b = static_cast<int32_t>(v + a) >> 16;
+  return 2u * a - static_cast<uint32_t>(a_minus_b);
+}
+static_assert(kScorePPT < 32768, "sign_pair_count: A < 2^16 and |A - B| < 2^15 per unit");
 constexpr float kPadY = 1e30f;    // padding point: e^2 overflows any corridor
 
 // ---------------------------------------------------------------- helpers
@@ -1229,14 +1261,18 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
     for (int q = 0; q < kNH; ++q) cnt[q] = 0;
     // v = (x_2q, x_2q+1, y_2q, y_2q+1): per hypothesis 3 FFMA2 over the two
     // points (e = A x + (B y + C); g = e^2 - t2hi) and two sign bits
-    auto score_pair = [&](const float4& v) {
+    auto g_of = [&](const float4& v, int h) {
       const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
+      const float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
+                                  __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
+      return __ffma2_rn(e, e, T2[h]);
+    };
+    auto score_pair = [&](const float4& v) {
 #pragma unroll
       for (int h = 0; h < kNH; ++h) {
-        float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
-                              __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
-        e = __ffma2_rn(e, e, T2[h]);
-        cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
+        const float2 g = g_of(v, h);
+        if (RVK_SIGN_PRMT) cnt[h] += sign_pair(g);
+        else cnt[h] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
       }
     };
     // 4. broadcast LDS.128 (two points each), four float4 per iteration
@@ -1247,13 +1283,25 @@ score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ ti
 #pragma unroll 1
     for (; q2 + 4 <= m2; q2 += 4) {
       const float4 v0 = cp[q2], v1 = cp[q2 + 1], v2 = cp[q2 + 2], v3 = cp[q2 + 3];
-      score_pair(v0);
-      score_pair(v1);
-      score_pair(v2);
-      score_pair(v3);
+      if (RVK_SIGN_PRMT) {
+#pragma unroll
+        for (int h = 0; h < kNH; ++h) {
+          cnt[h] += sign_pair(g_of(v0, h)) + sign_pair(g_of(v1, h));
+          cnt[h] += sign_pair(g_of(v2, h)) + sign_pair(g_of(v3, h));
+        }
+      } else {
+        score_pair(v0);
+        score_pair(v1);
+        score_pair(v2);
+        score_pair(v3);
+      }
     }
 #pragma unroll 1
     for (; q2 < m2; ++q2) score_pair(cp[q2]);
+    if (RVK_SIGN_PRMT) {
+#pragma unroll
+      for (int q = 0; q < kNH; ++q) cnt[q] = sign_pair_count(cnt[q]);
+    }
     if (active) {
       int32_t* up = upper + (static_cast<int64_t>(d.x) * g.Tg + gi) * 8;
 #pragma unroll
@@ -2349,24 +2397,39 @@ __device__ __forceinline__ void fused_score_block(int tb, int T, uint64_t seed, 
   }
 #pragma unroll
   for (int q = 0; q < kNH; ++q) cnt[q] = 0;
-  auto score_pair = [&](const float4& v) {
+  auto g_of = [&](const float4& v, int h) {
     const float2 X = make_float2(v.x, v.y), Y = make_float2(v.z, v.w);
-#pragma unroll
-    for (int h = 0; h < kNH; ++h) {
-      float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
-                            __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
-      e = __ffma2_rn(e, e, T2[h]);
-      cnt[h] += (__float_as_uint(e.x) >> 31) + (__float_as_uint(e.y) >> 31);
-    }
+    const float2 e = __ffma2_rn(X, make_float2(A[h], A[h]),
+                                __ffma2_rn(Y, make_float2(B[h], B[h]), Cc[h]));
+    return __ffma2_rn(e, e, T2[h]);
   };
   // four pairs per iteration; the padded slack is inert (e^2 overflows)
 #pragma unroll 1
   for (int q2 = 0; q2 < m2; q2 += 4) {
     const float4 v0 = pairs[q2], v1 = pairs[q2 + 1], v2 = pairs[q2 + 2], v3 = pairs[q2 + 3];
-    score_pair(v0);
-    score_pair(v1);
-    score_pair(v2);
-    score_pair(v3);
+    if (RVK_FUSED_SIGN_PRMT) {
+#pragma unroll
+      for (int h = 0; h < kNH; ++h) {
+        cnt[h] += sign_pair(g_of(v0, h)) + sign_pair(g_of(v1, h));
+        cnt[h] += sign_pair(g_of(v2, h)) + sign_pair(g_of(v3, h));
+      }
+    } else {
+      auto score_pair = [&](const float4& v) {
+#pragma unroll
+        for (int h = 0; h < kNH; ++h) {
+          const float2 g = g_of(v, h);
+          cnt[h] += (__float_as_uint(g.x) >> 31) + (__float_as_uint(g.y) >> 31);
+        }
+      };
+      score_pair(v0);
+      score_pair(v1);
+      score_pair(v2);
+      score_pair(v3);
+    }
+  }
+  if (RVK_FUSED_SIGN_PRMT) {
+#pragma unroll
+    for (int q = 0; q < kNH; ++q) cnt[q] = sign_pair_count(cnt[q]);
   }
 }
 
