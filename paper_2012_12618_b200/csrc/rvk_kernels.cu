@@ -717,6 +717,7 @@ prep_hyp_kernel(int32_t n_clusters, const int64_t* __restrict__ offsets,
                   stat, hyp, upper, tiles, tile_count, tile_cap);
     return;
   }
+  if (*reinterpret_cast<volatile int32_t*>(&big_ctl[0]) == 0) return;  // nothing listed
   for (;;) {
     if (threadIdx.x == 0) s_idx = atomicAdd(&big_ctl[1], 1);
     __syncthreads();
@@ -1171,7 +1172,12 @@ __device__ __forceinline__ void stage_points_bulk(float4* slot, uint64_t* bar,
 __global__ void __launch_bounds__(kScoreThreads, 3)
 score_kernel(const int32_t* __restrict__ tile_count, const int4* __restrict__ tiles,
              int64_t tile_cap, const float2* __restrict__ xy32, const float* __restrict__ hyp,
-             ScoreGeom g, int32_t* __restrict__ upper) {
+             ScoreGeom g, int32_t* __restrict__ upper, const int32_t* __restrict__ list_n) {
+  // CTA path behind the fused kernels (list_n = big_ctl: its units come only
+  // from the listed clusters): nothing listed, nothing to score -- the host
+  // cannot know that for device-resident offsets, so the launch stays and
+  // every CTA leaves before the prologue
+  if (list_n != nullptr && *list_n == 0) return;
   constexpr int kSlot = kScorePPT / 2 + 2;  // float4 per slot (+2: read-ahead slack)
   __shared__ int bstart[kTileBuckets + 1];
   // two point slots per warp: the current unit's and the next unit's (prefetch)
@@ -2905,8 +2911,10 @@ void launch_score(const FrameDev& f, const rvk_ransac_params& p, const Scratch& 
   ScoreGeom g = score_geom(p.max_trials);
   set_ppt(g, s.ppt);
   const int64_t max_units = static_cast<int64_t>(g.nhb) * (f.n_points / g.ppt + f.n_clusters);
+  const bool listed = fused_path(f, p) || prep_score_path(f, p);
   score_kernel<<<score_grid(max_units), kScoreThreads, kScoreSmemBytes, st>>>(
-      s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper);
+      s.tile_count, s.tiles, s.tile_cap, s.xy32, s.hyp, g, s.upper,
+      listed ? s.big_ctl : nullptr);
   count_launch();
 }
 
